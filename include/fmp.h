@@ -1,0 +1,173 @@
+/*
+ * fmp.h — C ABI of the B200 OMP correlation path (libfmp_cuda.so).
+ *
+ * This is the drop-in boundary for the reference library's correlation / OMP
+ * interface, /root/reference/proj/include/fastmp (a C++20 library with no FFI
+ * of its own).  Each entry point names the reference interface it replaces;
+ * the C++ facade include/fastmp_b200/fastmp.hpp re-exposes those signatures
+ * on top of this ABI, and INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no C++ or torch types
+ *   - complex vectors are interleaved (re, im); `dtype` selects the element:
+ *       FMP_C128 complex double, FMP_C64 complex float,
+ *       FMP_F64 / FMP_F32 real (Hadamard operators with real data only)
+ *   - atom and row indices are 1-based, as in the reference
+ *     (transform.hpp:32-34); supports are in selection order
+ *   - batched calls process `batch` independent vectors laid out back to back
+ *   - functions without a `_dev` suffix take HOST buffers, copy in, compute
+ *     on the context's GPU and copy out before returning (the reference's
+ *     value semantics);  `_dev` variants take DEVICE pointers and enqueue on
+ *     `stream` (NULL = the context stream) without synchronising
+ *   - every call returns a status; fmp_last_error() describes the last
+ *     failure on the calling thread.  Status codes map 1:1 onto the
+ *     reference's exceptions: FMP_EINVAL = std::invalid_argument
+ *     (kernel.cpp:213-222, sensing.cpp:94,104, transform.cpp:121,138),
+ *     FMP_ERANK = RankDeficientError (solvers.hpp:42-51)
+ *   - handles are re-entrant per handle; use one context per host thread
+ *     for concurrent work
+ */
+#ifndef FMP_H
+#define FMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fmp_status {
+  FMP_OK = 0,
+  FMP_EINVAL = 1,       /* std::invalid_argument in the reference */
+  FMP_ERANK = 2,        /* RankDeficientError */
+  FMP_ECUDA = 3,        /* CUDA runtime / launch failure */
+  FMP_ENOMEM = 4,       /* device allocation failed */
+  FMP_EUNSUPPORTED = 5, /* shape outside what the GPU path implements */
+  FMP_ENCCL = 6         /* collective failure (sharded solve) */
+};
+
+enum fmp_kind { FMP_FOURIER = 0, FMP_HADAMARD = 1 };       /* TransformKind, types.hpp:28 */
+enum fmp_dtype { FMP_C128 = 0, FMP_C64 = 1, FMP_F64 = 2, FMP_F32 = 3 };
+/* CorrelationMode (cost_model.hpp:58); FMP_MODE_CUSTOM uses fast_until */
+enum fmp_mode {
+  FMP_MODE_CONVENTIONAL = 0,
+  FMP_MODE_FAST = 1,
+  FMP_MODE_ADAPTIVE = 2,
+  FMP_MODE_CUSTOM = 3
+};
+
+typedef struct fmp_ctx_s* fmp_ctx;
+typedef struct fmp_op_s* fmp_op;
+
+int fmp_version(void);
+const char* fmp_last_error(void);
+/* number of kernel launches the last call on this thread issued */
+int fmp_last_launch_count(void);
+
+/* ---------------------------------------------------------------- context */
+int fmp_ctx_create(int device, fmp_ctx* out);
+int fmp_ctx_destroy(fmp_ctx ctx);
+/* cudaStream_t to enqueue on (NULL restores the context-owned stream) */
+int fmp_ctx_set_stream(fmp_ctx ctx, void* stream);
+void* fmp_ctx_stream(fmp_ctx ctx);
+int fmp_ctx_synchronize(fmp_ctx ctx);
+
+/* --------------------------------------------------------------- operator */
+/* SensingOperator(StructuredUnitary(kind, n), make_row_selection(n, rows))
+ * (sensing.hpp:39-44, sensing.cpp:72-80 validation): rows are 1-based,
+ * distinct, in [1, n]; they are sorted here as the reference does.  Builds
+ * the correlation kernel c = Phi^H Phi e_1 on the device
+ * (compute_kernel, kernel.hpp:42-43).  n must be a power of two. */
+int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows_1based,
+                        uint64_t m, fmp_op* out);
+int fmp_operator_destroy(fmp_op op);
+int fmp_operator_info(fmp_op op, int* kind, uint64_t* n, uint64_t* m);
+/* CorrelationKernel readback (kernel.hpp:31-40): c (2n doubles); Hadamard
+ * also the sorted distinct values (up to m+1) and value_index (n); Fourier
+ * sets *nvalues = 0.  values / value_index may be NULL. */
+int fmp_operator_kernel(fmp_op op, double* c_out, double* values_out,
+                        uint32_t* value_index_out, uint64_t* nvalues);
+/* crossover_iteration (cost_model.hpp:76): the Adaptive switch point */
+uint64_t fmp_crossover_iteration(int kind, uint64_t n);
+
+/* ------------------------------------------------------ transforms (batched) */
+/* SensingOperator::apply, Phi x (sensing.cpp:93-100): x batch x n -> y batch x m */
+int fmp_apply(fmp_op op, int dtype, const void* x, uint64_t batch, void* y_out);
+int fmp_apply_dev(fmp_op op, int dtype, const void* x, uint64_t batch, void* y_out, void* stream);
+/* SensingOperator::apply_adjoint, Phi^H r (sensing.cpp:102-109) — the
+ * conventional correlation: r batch x m -> h batch x n.  argmax_out
+ * (optional, batch) receives the 1-based band argmax of |h| (solvers.cpp:90-101)
+ * and h_out may then be NULL. */
+int fmp_apply_adjoint(fmp_op op, int dtype, const void* r, uint64_t batch, void* h_out,
+                      uint64_t* argmax_out);
+int fmp_apply_adjoint_dev(fmp_op op, int dtype, const void* r, uint64_t batch, void* h_out,
+                          uint64_t* argmax_out, void* stream);
+/* StructuredUnitary::forward / adjoint (transform.hpp:46-47), dense n -> n */
+int fmp_unitary_forward(fmp_op op, int dtype, const void* v, uint64_t batch, void* out);
+int fmp_unitary_adjoint(fmp_op op, int dtype, const void* v, uint64_t batch, void* out);
+
+/* --------------------------------------------------- fast update (batched) */
+/* fast_update (kernel.hpp:95-98): h = h0 - sum_tau coeffs[tau] P_{support[tau]} c
+ * for `batch` problems, each with t atoms: h0 batch x n, support batch x t
+ * (1-based, distinct per problem), coeffs batch x t.  h_out (batch x n) and/or
+ * argmax_out (batch, 1-based band argmax) may be NULL (not both). */
+int fmp_fast_update(fmp_op op, int dtype, const void* h0, const uint64_t* support,
+                    const void* coeffs, uint64_t t, uint64_t batch, void* h_out,
+                    uint64_t* argmax_out);
+int fmp_fast_update_dev(fmp_op op, int dtype, const void* h0, const uint32_t* support0,
+                        const void* coeffs, uint64_t t, uint64_t batch, void* h_out,
+                        uint64_t* argmax_out, void* stream);
+
+/* argmax_magnitude with the 1e-9 tie band (solvers.cpp:90-101): 1-based */
+int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t batch,
+                    uint64_t* idx_out);
+
+/* ----------------------------------------------------------- OMP (batched) */
+typedef struct {
+  uint64_t max_iterations;     /* SolveConfig::max_iterations (>= 1) */
+  double tolerance;            /* residual_tolerance used when tolerances == NULL */
+  const double* tolerances;    /* optional per-problem tolerances (batch) */
+  int mode;                    /* fmp_mode */
+  uint64_t fast_until;         /* FMP_MODE_CUSTOM: t <= fast_until use the fast update */
+  int record_correlations;     /* keep every correlation vector (history) */
+} fmp_omp_config;
+
+typedef struct {
+  uint64_t* support;      /* batch x max_iterations, 1-based, selection order, 0 padded */
+  double* coeffs;         /* batch x max_iterations complex (always fp64) */
+  uint64_t* support_size; /* batch */
+  uint64_t* iterations;   /* batch: iterations_run */
+  double* residual;       /* batch: residual_norm */
+  int32_t* aborted;       /* batch: rank_deficient_abort */
+  uint8_t* modes;         /* optional batch x max_iterations: 1 fast, 0 conventional */
+  uint64_t* history_len;  /* optional batch: correlation vectors recorded */
+  void* history;          /* optional batch x max_iterations x n (dtype) */
+} fmp_omp_result;
+
+/* omp_solve (solvers.hpp:70-71) over `batch` measurement vectors y (batch x m)
+ * sharing one operator.  Selected supports follow the reference's
+ * identification rule exactly; least squares runs in fp64. */
+int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch,
+                  const fmp_omp_config* cfg, fmp_omp_result* out);
+int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
+                      const fmp_omp_config* cfg, fmp_omp_result* out, void* stream);
+
+/* ------------------------------------------------------ instance generation */
+/* seeded synthetic problems for the bench / parity harness, following the
+ * reference's make_row_selection / make_instance recipes (sensing.cpp:61-70,
+ * :119-153) with its Rng (random.cpp).  y is synthesised directly from the
+ * K nonzeros (identical up to rounding to op.apply(x)). real != 0 draws
+ * real N(0,1) nonzeros.  Host memory; threads 0 = all cores. */
+int fmp_make_row_selection(uint64_t n, uint64_t m, uint64_t seed, uint64_t* rows_out);
+int fmp_make_batch(int kind, uint64_t n, const uint64_t* rows_1based, uint64_t m, uint64_t k,
+                   double noise_stddev, int real, uint64_t base_seed, uint64_t first,
+                   uint64_t batch, int threads, double* y_out, double* x_out,
+                   double* noise_norm_out);
+uint64_t fmp_derive_seed(uint64_t base, uint64_t index);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FMP_H */

@@ -1,0 +1,541 @@
+"""paper_1205_4139_b200 — B200-native OMP correlation path.
+
+Python host side of the drop-in for the reference library ``fastmp``
+(/root/reference/proj/include/fastmp).  Every call goes through the C ABI of
+``libfmp_cuda.so`` (``include/fmp.h``); there is no CPU fallback: importing
+this package without the built library raises immediately.
+
+Names and argument meaning follow the reference:
+
+==========================  ===============================================
+this module                 reference (proj/include/fastmp)
+==========================  ===============================================
+SensingOperator             sensing.hpp:39-66  (apply / apply_adjoint / column)
+compute_kernel              kernel.hpp:42-43   -> CorrelationKernel
+fast_update                 kernel.hpp:95-98
+argmax_magnitude            solvers.cpp:90-101 (tie band 1e-9)
+SolveConfig/default_config  solvers.hpp:26-37
+omp_solve                   solvers.hpp:70-71  -> RecoveryResult
+crossover_iteration         cost_model.hpp:76
+make_row_selection          sensing.hpp:31-33
+==========================  ===============================================
+
+Atom / row indices are 1-based as in the reference.  Batched variants take a
+leading batch dimension.  ``*_dev`` helpers take torch CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmp_cuda.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_1205_4139_b200.build` "
+        "(the GPU path has no fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+FOURIER, HADAMARD = 0, 1
+KINDS = {"fourier": FOURIER, "hadamard": HADAMARD}
+C128, C64, F64, F32 = 0, 1, 2, 3
+DTYPES = {np.dtype(np.complex128): C128, np.dtype(np.complex64): C64,
+          np.dtype(np.float64): F64, np.dtype(np.float32): F32}
+NP_OF = {C128: np.complex128, C64: np.complex64, F64: np.float64, F32: np.float32}
+MODES = {"conventional": 0, "fast": 1, "adaptive": 2, "custom": 3}
+
+_vp = C.c_void_p
+_u64 = C.c_uint64
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+class OmpConfig(C.Structure):
+    _fields_ = [("max_iterations", _u64), ("tolerance", C.c_double),
+                ("tolerances", C.POINTER(C.c_double)), ("mode", C.c_int),
+                ("fast_until", _u64), ("record_correlations", C.c_int)]
+
+
+class OmpResult(C.Structure):
+    _fields_ = [("support", _vp), ("coeffs", _vp), ("support_size", _vp), ("iterations", _vp),
+                ("residual", _vp), ("aborted", _vp), ("modes", _vp), ("history_len", _vp),
+                ("history", _vp)]
+
+
+_sig("fmp_version", C.c_int)
+_sig("fmp_last_error", C.c_char_p)
+_sig("fmp_last_launch_count", C.c_int)
+_sig("fmp_ctx_create", C.c_int, C.c_int, C.POINTER(_vp))
+_sig("fmp_ctx_destroy", C.c_int, _vp)
+_sig("fmp_ctx_set_stream", C.c_int, _vp, _vp)
+_sig("fmp_ctx_stream", _vp, _vp)
+_sig("fmp_ctx_synchronize", C.c_int, _vp)
+_sig("fmp_operator_create", C.c_int, _vp, C.c_int, _u64, _vp, _u64, C.POINTER(_vp))
+_sig("fmp_operator_destroy", C.c_int, _vp)
+_sig("fmp_operator_info", C.c_int, _vp, C.POINTER(C.c_int), C.POINTER(_u64), C.POINTER(_u64))
+_sig("fmp_operator_kernel", C.c_int, _vp, _vp, _vp, _vp, C.POINTER(_u64))
+_sig("fmp_crossover_iteration", _u64, C.c_int, _u64)
+_sig("fmp_apply", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
+_sig("fmp_apply_dev", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
+_sig("fmp_apply_adjoint", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
+_sig("fmp_apply_adjoint_dev", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp, _vp)
+_sig("fmp_unitary_forward", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
+_sig("fmp_unitary_adjoint", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
+_sig("fmp_fast_update", C.c_int, _vp, C.c_int, _vp, _vp, _vp, _u64, _u64, _vp, _vp)
+_sig("fmp_fast_update_dev", C.c_int, _vp, C.c_int, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp)
+_sig("fmp_argmax_band", C.c_int, _vp, C.c_int, _vp, _u64, _u64, _vp)
+_sig("fmp_omp_solve", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig), C.POINTER(OmpResult))
+_sig("fmp_omp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig),
+     C.POINTER(OmpResult), _vp)
+_sig("fmp_make_row_selection", C.c_int, _u64, _u64, _u64, _vp)
+_sig("fmp_make_batch", C.c_int, C.c_int, _u64, _vp, _u64, _u64, C.c_double, C.c_int, _u64, _u64,
+     _u64, C.c_int, _vp, _vp, _vp)
+_sig("fmp_derive_seed", _u64, _u64, _u64)
+
+
+# ---------------------------------------------------------------- errors
+class FmpError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[fmp status {status}] {message}")
+        self.status = status
+
+
+class InvalidArgument(FmpError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class RankDeficientError(FmpError):
+    """RankDeficientError (solvers.hpp:42-51)."""
+
+
+class Unsupported(FmpError):
+    pass
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = (_lib.fmp_last_error() or b"").decode()
+    cls = {1: InvalidArgument, 2: RankDeficientError, 5: Unsupported}.get(status, FmpError)
+    raise cls(status, msg)
+
+
+def last_launch_count() -> int:
+    return int(_lib.fmp_last_launch_count())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_vp)
+
+
+def _dtype_code(arr) -> int:
+    dt = np.dtype(arr.dtype) if not hasattr(arr, "is_cuda") else _torch_np_dtype(arr.dtype)
+    if dt not in DTYPES:
+        raise InvalidArgument(1, f"unsupported dtype {dt}")
+    return DTYPES[dt]
+
+
+def _torch_np_dtype(tdt):
+    import torch
+    return np.dtype({torch.complex128: np.complex128, torch.complex64: np.complex64,
+                     torch.float64: np.float64, torch.float32: np.float32}[tdt])
+
+
+# --------------------------------------------------------------- context
+class Context:
+    """A GPU, a stream and a device workspace (one per host thread)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(_lib.fmp_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        _check(_lib.fmp_ctx_set_stream(self.handle, stream_ptr))
+
+    @property
+    def stream(self) -> int:
+        return _lib.fmp_ctx_stream(self.handle) or 0
+
+    def synchronize(self) -> None:
+        _check(_lib.fmp_ctx_synchronize(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.fmp_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+# ---------------------------------------------------------- sensing / kernel
+def crossover_iteration(kind, n: int) -> int:
+    kind = KINDS.get(kind, kind)
+    return int(_lib.fmp_crossover_iteration(kind, n))
+
+
+def make_row_selection(n: int, m: int, seed: int) -> np.ndarray:
+    out = np.zeros(max(m, 1), np.uint64)
+    _check(_lib.fmp_make_row_selection(n, m, seed, _ptr(out)))
+    return out[:m]
+
+
+def derive_seed(base: int, index: int) -> int:
+    return int(_lib.fmp_derive_seed(base, index))
+
+
+@dataclass
+class CorrelationKernel:
+    """kernel.hpp:31-40"""
+    kind: str
+    n: int
+    m: int
+    c: np.ndarray
+    values: np.ndarray
+    value_index: np.ndarray
+
+
+class SensingOperator:
+    """Phi = S_Omega U (sensing.hpp:39-66) resident on one GPU."""
+
+    def __init__(self, kind, n: int, rows: Sequence[int], ctx: Optional[Context] = None):
+        self.kind_name = kind if isinstance(kind, str) else ("fourier" if kind == 0 else "hadamard")
+        self.kind = KINDS[self.kind_name]
+        self.ctx = ctx or default_context()
+        rows = np.ascontiguousarray(np.asarray(rows, dtype=np.uint64))
+        h = _vp()
+        _check(_lib.fmp_operator_create(self.ctx.handle, self.kind, int(n), _ptr(rows), len(rows),
+                                        C.byref(h)))
+        self.handle = h
+        self.n = int(n)
+        self.omega = np.sort(rows)
+        self.m = len(rows)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.fmp_operator_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _default_dtype(self, a):
+        return np.asarray(a).dtype if np.iscomplexobj(a) or self.kind == HADAMARD else np.complex128
+
+    def _prep(self, a, length: int, dtype=None):
+        a = np.asarray(a)
+        if dtype is None:
+            dtype = a.dtype if a.dtype in DTYPES else np.complex128
+            if self.kind == FOURIER and not np.issubdtype(dtype, np.complexfloating):
+                dtype = np.complex128
+        a = np.ascontiguousarray(a, dtype=dtype)
+        if a.shape[-1] != length:
+            raise InvalidArgument(1, f"length mismatch: expected {length}, got {a.shape[-1]}")
+        return a
+
+    def apply(self, x, dtype=None) -> np.ndarray:
+        """Phi x (sensing.cpp:93-100); x of shape (n,) or (batch, n)."""
+        x = self._prep(x, self.n, dtype)
+        b = 1 if x.ndim == 1 else x.shape[0]
+        out = np.empty(x.shape[:-1] + (self.m,), x.dtype)
+        _check(_lib.fmp_apply(self.handle, DTYPES[x.dtype], _ptr(x), b, _ptr(out)))
+        return out
+
+    def apply_adjoint(self, r, dtype=None, argmax: bool = False):
+        """Phi^H r (sensing.cpp:102-109): the conventional correlation."""
+        r = self._prep(r, self.m, dtype)
+        b = 1 if r.ndim == 1 else r.shape[0]
+        out = np.empty(r.shape[:-1] + (self.n,), r.dtype)
+        idx = np.zeros(b, np.uint64)
+        _check(_lib.fmp_apply_adjoint(self.handle, DTYPES[r.dtype], _ptr(r), b, _ptr(out),
+                                      _ptr(idx) if argmax else None))
+        if argmax:
+            return out, (idx if r.ndim > 1 else int(idx[0]))
+        return out
+
+    def forward(self, v, dtype=None) -> np.ndarray:
+        """StructuredUnitary::forward (transform.hpp:46)."""
+        v = self._prep(v, self.n, dtype)
+        out = np.empty_like(v)
+        _check(_lib.fmp_unitary_forward(self.handle, DTYPES[v.dtype], _ptr(v),
+                                        1 if v.ndim == 1 else v.shape[0], _ptr(out)))
+        return out
+
+    def adjoint(self, v, dtype=None) -> np.ndarray:
+        """StructuredUnitary::adjoint (transform.hpp:47)."""
+        v = self._prep(v, self.n, dtype)
+        out = np.empty_like(v)
+        _check(_lib.fmp_unitary_adjoint(self.handle, DTYPES[v.dtype], _ptr(v),
+                                        1 if v.ndim == 1 else v.shape[0], _ptr(out)))
+        return out
+
+    def column(self, j: int) -> np.ndarray:
+        """Column j (1-based) of Phi (sensing.cpp:111-117), as Phi e_j on the GPU."""
+        if not 1 <= j <= self.n:
+            raise InvalidArgument(1, "column: index out of range")
+        e = np.zeros(self.n, np.complex128)
+        e[j - 1] = 1.0
+        return self.apply(e)
+
+    def kernel(self) -> CorrelationKernel:
+        c = np.zeros(self.n, np.complex128)
+        vals = np.zeros(self.m + 1)
+        vidx = np.zeros(self.n, np.uint32)
+        nv = _u64(0)
+        had = self.kind == HADAMARD
+        _check(_lib.fmp_operator_kernel(self.handle, _ptr(c), _ptr(vals) if had else None,
+                                        _ptr(vidx) if had else None, C.byref(nv)))
+        return CorrelationKernel(self.kind_name, self.n, self.m, c, vals[: nv.value].copy(),
+                                 vidx if had else np.zeros(0, np.uint32))
+
+
+def compute_kernel(op: SensingOperator) -> CorrelationKernel:
+    """compute_kernel (kernel.hpp:42-43); built on the device at operator creation."""
+    return op.kernel()
+
+
+def fast_update(h0, op: SensingOperator, support, coeffs, argmax: bool = False, want_h: bool = True):
+    """fast_update (kernel.hpp:95-98).
+
+    h0: (n,) or (batch, n); support: (t,) or (batch, t) 1-based; coeffs alike.
+    Returns h (and the 1-based band argmax when ``argmax``)."""
+    h0 = np.asarray(h0)
+    dt = h0.dtype if h0.dtype in DTYPES else np.complex128
+    h0 = np.ascontiguousarray(h0, dtype=dt)
+    batched = h0.ndim > 1
+    b = h0.shape[0] if batched else 1
+    support = np.ascontiguousarray(np.asarray(support, dtype=np.uint64).reshape(b, -1))
+    t = support.shape[1]
+    coeffs = np.ascontiguousarray(np.asarray(coeffs).astype(dt, copy=False).reshape(b, t))
+    if h0.shape[-1] != op.n:
+        raise InvalidArgument(1, "fast_update: h0 length")
+    out = np.empty_like(h0) if want_h else None
+    idx = np.zeros(b, np.uint64)
+    _check(_lib.fmp_fast_update(op.handle, DTYPES[h0.dtype], _ptr(h0), _ptr(support) if t else None,
+                                _ptr(coeffs) if t else None, t, b,
+                                _ptr(out) if want_h else None, _ptr(idx) if argmax else None))
+    if argmax:
+        return out, (idx if batched else int(idx[0]))
+    return out
+
+
+def argmax_magnitude(h, ctx: Optional[Context] = None):
+    """1-based band argmax (solvers.cpp:90-101); h (n,) or (batch, n)."""
+    h = np.asarray(h)
+    dt = h.dtype if h.dtype in DTYPES else np.complex128
+    h = np.ascontiguousarray(h, dtype=dt)
+    b = h.shape[0] if h.ndim > 1 else 1
+    out = np.zeros(b, np.uint64)
+    ctx = ctx or default_context()
+    _check(_lib.fmp_argmax_band(ctx.handle, DTYPES[h.dtype], _ptr(h), h.shape[-1], b, _ptr(out)))
+    return out if h.ndim > 1 else int(out[0])
+
+
+# ------------------------------------------------------------------- OMP
+@dataclass
+class SolveConfig:
+    """SolveConfig (solvers.hpp:26-34); ls_method is fixed to the GPU's
+    incremental Cholesky on Gram entries."""
+    max_iterations: int = 1
+    residual_tolerance: float = 0.0
+    correlation_mode: str = "conventional"
+    fast_until: int = 0                # used when correlation_mode == "custom"
+    record_correlations: bool = False
+
+
+def default_config(k: int, y_norm: float) -> SolveConfig:
+    """solvers.cpp:216-221"""
+    return SolveConfig(max_iterations=max(1, int(k)), residual_tolerance=1e-9 * float(y_norm))
+
+
+@dataclass
+class RecoveryResult:
+    """RecoveryResult (solvers.hpp:53-64)."""
+    x_hat: np.ndarray
+    support: list
+    coeffs: np.ndarray
+    iterations_run: int
+    residual_norm: float
+    rank_deficient_abort: bool
+    support_history: list = field(default_factory=list)
+    correlation_history: list = field(default_factory=list)
+    modes_used: list = field(default_factory=list)
+
+
+@dataclass
+class BatchResult:
+    support: np.ndarray        # (batch, T) 1-based, 0 padded
+    coeffs: np.ndarray         # (batch, T) complex128
+    support_size: np.ndarray
+    iterations: np.ndarray
+    residual: np.ndarray
+    aborted: np.ndarray
+    modes: np.ndarray
+    history_len: np.ndarray
+    history: Optional[np.ndarray]
+
+
+def _config(cfg: SolveConfig, tolerances=None):
+    c = OmpConfig()
+    c.max_iterations = int(cfg.max_iterations)
+    c.tolerance = float(cfg.residual_tolerance)
+    c.tolerances = tolerances
+    c.mode = MODES[cfg.correlation_mode]
+    c.fast_until = int(cfg.fast_until)
+    c.record_correlations = int(cfg.record_correlations)
+    return c
+
+
+def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
+                    dtype=None) -> BatchResult:
+    """omp_solve over a batch of measurements Y (batch, m) sharing `op`."""
+    Y = np.asarray(Y)
+    if dtype is None:
+        dtype = Y.dtype if Y.dtype in DTYPES else np.complex128
+        if op.kind == FOURIER and not np.issubdtype(dtype, np.complexfloating):
+            dtype = np.complex128
+    Y = np.ascontiguousarray(Y, dtype=dtype)
+    if Y.ndim == 1:
+        Y = Y[None]
+    if Y.shape[-1] != op.m:
+        raise InvalidArgument(1, "omp_solve: measurement length mismatch")
+    B, T, n = Y.shape[0], int(cfg.max_iterations), op.n
+    if T < 1:
+        raise InvalidArgument(1, "omp_solve: max_iterations must be >= 1")
+    sup = np.zeros((B, T), np.uint64)
+    co = np.zeros((B, T), np.complex128)
+    sz = np.zeros(B, np.uint64)
+    it = np.zeros(B, np.uint64)
+    rn = np.zeros(B)
+    ab = np.zeros(B, np.int32)
+    md = np.zeros((B, T), np.uint8)
+    hl = np.zeros(B, np.uint64)
+    hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
+    tol = None
+    if tolerances is not None:
+        tarr = np.ascontiguousarray(np.broadcast_to(np.asarray(tolerances, np.float64), (B,)))
+        tol = tarr.ctypes.data_as(C.POINTER(C.c_double))
+    res = OmpResult(_ptr(sup), _ptr(co), _ptr(sz), _ptr(it), _ptr(rn), _ptr(ab), _ptr(md), _ptr(hl),
+                    _ptr(hist) if hist is not None else None)
+    c = _config(cfg, tol)
+    _check(_lib.fmp_omp_solve(op.handle, DTYPES[Y.dtype], _ptr(Y), B, C.byref(c), C.byref(res)))
+    return BatchResult(sup, co, sz, it, rn, ab.astype(bool), md, hl, hist)
+
+
+def omp_solve(op: SensingOperator, y, cfg: SolveConfig, dtype=None) -> RecoveryResult:
+    """omp_solve (solvers.hpp:70-71) for one measurement vector."""
+    r = omp_solve_batch(op, np.asarray(y)[None], cfg, dtype=dtype)
+    s = int(r.support_size[0])
+    support = [int(v) for v in r.support[0, :s]]
+    coeffs = r.coeffs[0, :s].copy()
+    x = np.zeros(op.n, np.complex128)
+    for a, v in zip(support, coeffs):
+        x[a - 1] = v
+    iters = int(r.iterations[0])
+    hl = int(r.history_len[0])
+    hist = [r.history[0, i].copy() for i in range(hl)] if r.history is not None else []
+    return RecoveryResult(x, support, coeffs, iters, float(r.residual[0]), bool(r.aborted[0]),
+                          [support[: i + 1] for i in range(iters)], hist,
+                          [int(v) for v in r.modes[0, :hl]])
+
+
+def make_batch(kind, n: int, rows, k: int, batch: int, base_seed: int, first: int = 0,
+               noise_stddev: float = 0.0, real: bool = False, want_x: bool = False, threads: int = 0):
+    """Seeded synthetic measurements (see fmp.h fmp_make_batch).
+
+    Returns (Y (batch, m) complex128, X or None, noise_norms)."""
+    rows = np.ascontiguousarray(np.asarray(rows, np.uint64))
+    m = len(rows)
+    Y = np.zeros((batch, m), np.complex128)
+    X = np.zeros((batch, n), np.complex128) if want_x else None
+    nn = np.zeros(batch)
+    _check(_lib.fmp_make_batch(KINDS.get(kind, kind), n, _ptr(rows), m, k, noise_stddev, int(real),
+                               base_seed, first, batch, threads, _ptr(Y),
+                               _ptr(X) if want_x else None, _ptr(nn)))
+    return Y, X, nn
+
+
+# --------------------------------------------------- device (torch) variants
+def omp_solve_dev(op: SensingOperator, y, cfg: SolveConfig, out: dict, tolerances=None,
+                  stream: Optional[int] = None) -> None:
+    """Enqueue a batched solve on device tensors (no host synchronisation).
+
+    y: torch (batch, m) of a supported dtype; out: dict of preallocated torch
+    tensors from :func:`alloc_dev_result`; tolerances: torch float64 (batch,)."""
+    B = y.shape[0]
+    c = _config(cfg, C.cast(C.c_void_p(tolerances.data_ptr()), C.POINTER(C.c_double))
+                if tolerances is not None else None)
+    res = OmpResult(out["support"].data_ptr(), out["coeffs"].data_ptr(), out["support_size"].data_ptr(),
+                    out["iterations"].data_ptr(), out["residual"].data_ptr(), out["aborted"].data_ptr(),
+                    out["modes"].data_ptr() if "modes" in out else None,
+                    out["history_len"].data_ptr() if "history_len" in out else None,
+                    out["history"].data_ptr() if "history" in out else None)
+    _check(_lib.fmp_omp_solve_dev(op.handle, _dtype_code(y), y.data_ptr(), B, C.byref(c), C.byref(res),
+                                  stream))
+
+
+def alloc_dev_result(B: int, T: int, device="cuda") -> dict:
+    import torch
+    return {
+        "support": torch.zeros((B, T), dtype=torch.int64, device=device),
+        "coeffs": torch.zeros((B, T), dtype=torch.complex128, device=device),
+        "support_size": torch.zeros(B, dtype=torch.int64, device=device),
+        "iterations": torch.zeros(B, dtype=torch.int64, device=device),
+        "residual": torch.zeros(B, dtype=torch.float64, device=device),
+        "aborted": torch.zeros(B, dtype=torch.int32, device=device),
+    }
+
+
+def fast_update_dev(op: SensingOperator, h0, support0, coeffs, h_out=None, argmax_out=None,
+                    stream: Optional[int] = None) -> None:
+    """Device variant: h0 (batch, n), support0 int32 0-based (batch, t), coeffs (batch, t)."""
+    B, t = support0.shape
+    _check(_lib.fmp_fast_update_dev(op.handle, _dtype_code(h0), h0.data_ptr(), support0.data_ptr(),
+                                    coeffs.data_ptr(), t, B,
+                                    h_out.data_ptr() if h_out is not None else None,
+                                    argmax_out.data_ptr() if argmax_out is not None else None, stream))
+
+
+def apply_adjoint_dev(op: SensingOperator, r, h_out=None, argmax_out=None,
+                      stream: Optional[int] = None) -> None:
+    B = r.shape[0]
+    _check(_lib.fmp_apply_adjoint_dev(op.handle, _dtype_code(r), r.data_ptr(), B,
+                                      h_out.data_ptr() if h_out is not None else None,
+                                      argmax_out.data_ptr() if argmax_out is not None else None,
+                                      stream))
+
+
+__all__ = [
+    "Context", "SensingOperator", "CorrelationKernel", "compute_kernel", "fast_update",
+    "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
+    "omp_solve_batch", "crossover_iteration", "make_row_selection", "make_batch", "derive_seed",
+    "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
+]

@@ -1,0 +1,644 @@
+// C ABI (include/fmp.h) over the sm_100a kernels.  Validation mirrors the
+// reference's std::invalid_argument checks so callers see the same error
+// behaviour (kernel.cpp:212-222, sensing.cpp:27-38/94/104, solvers.cpp:299-304).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <type_traits>
+#include <string>
+#include <vector>
+
+#include "fmp.h"
+#include "fmp_kernels.cuh"
+
+using fmp::DevOp;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launch_count = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? FMP_ENOMEM : FMP_ECUDA,        \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+bool pow2(uint64_t n) { return n && !(n & (n - 1)); }
+int ilog2(uint64_t n) {
+  int p = 0;
+  while (n >>= 1) ++p;
+  return p;
+}
+
+// grow-only device scratch, one buffer per slot
+struct Workspace {
+  std::vector<std::pair<void*, size_t>> slot;
+  void* get(int i, size_t bytes, cudaError_t* err) {
+    if ((int)slot.size() <= i) slot.resize(i + 1, {nullptr, 0});
+    bytes = std::max<size_t>(bytes, 256);
+    if (slot[i].second < bytes) {
+      if (slot[i].first) cudaFree(slot[i].first);
+      slot[i] = {nullptr, 0};
+      void* p = nullptr;
+      *err = cudaMalloc(&p, bytes);
+      if (*err != cudaSuccess) return nullptr;
+      slot[i] = {p, bytes};
+    }
+    return slot[i].first;
+  }
+  ~Workspace() {
+    for (auto& s : slot)
+      if (s.first) cudaFree(s.first);
+  }
+};
+
+enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
+            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX };
+
+}  // namespace
+
+struct fmp_ctx_s {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t cur = nullptr;
+  Workspace ws;
+  std::mutex mu;
+};
+
+struct fmp_op_s {
+  fmp_ctx_s* ctx = nullptr;
+  DevOp d;
+  std::vector<uint64_t> rows;  // sorted, 1-based
+};
+
+namespace {
+
+#define ALLOC(var, slot, bytes)                                       \
+  do {                                                                \
+    cudaError_t e_ = cudaSuccess;                                     \
+    var = (std::remove_reference_t<decltype(var)>)ctx->ws.get(slot, (bytes), &e_);             \
+    if (!var) return fail(FMP_ENOMEM, "device workspace (%zu bytes): %s", \
+                          (size_t)(bytes), cudaGetErrorString(e_));   \
+  } while (0)
+
+int check_dtype(const DevOp& d, int dtype) {
+  if (dtype < 0 || dtype > 3) return fail(FMP_EINVAL, "unknown dtype %d", dtype);
+  if (d.kind == fmp::FOURIER && !fmp::is_complex(dtype))
+    return fail(FMP_EINVAL, "real dtypes need a Hadamard operator");
+  return FMP_OK;
+}
+
+cudaStream_t pick_stream(fmp_ctx_s* ctx, void* s) {
+  return s ? (cudaStream_t)s : ctx->cur;
+}
+
+// batched transform on device pointers
+int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_omega,
+                  const void* in, void* out, uint64_t batch, uint64_t* amax, cudaStream_t st) {
+  fmp_ctx_s* ctx = op->ctx;
+  fmp::TransformArgs a{};
+  a.op = &op->d;
+  a.dtype = dtype;
+  a.inverse = inverse;
+  a.in_omega = in_omega;
+  a.out_omega = out_omega;
+  a.in = in;
+  a.out = out;
+  a.batch = (int64_t)batch;
+  a.argmax_out = amax;
+  if (op->d.n > fmp::transform_max_n(dtype)) {
+    void* w;
+    ALLOC(w, S_WORK, (size_t)batch * op->d.n * fmp::elem_bytes(dtype));
+    a.work = w;
+  }
+  CU(fmp::launch_transform(a, st));
+  g_launch_count = fmp::last_launch_count();
+  return FMP_OK;
+}
+
+int copy_in(fmp_ctx_s* ctx, int slot, const void* host, size_t bytes, void** dev, cudaStream_t st) {
+  ALLOC(*dev, slot, bytes);
+  CU(cudaMemcpyAsync(*dev, host, bytes, cudaMemcpyHostToDevice, st));
+  return FMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmp_version(void) { return 1; }
+const char* fmp_last_error(void) { return g_err.c_str(); }
+int fmp_last_launch_count(void) { return g_launch_count; }
+
+uint64_t fmp_crossover_iteration(int kind, uint64_t n) {
+  // cost_model.cpp:62-74 (power-of-two sizes)
+  if (!pow2(n)) return 0;
+  const uint64_t logn = (uint64_t)ilog2(n);
+  return kind == FMP_FOURIER ? (5 * logn) / 6 + 1 : logn + 1;
+}
+
+int fmp_ctx_create(int device, fmp_ctx* out) {
+  if (!out) return fail(FMP_EINVAL, "null output handle");
+  int count = 0;
+  CU(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(FMP_EINVAL, "device %d of %d", device, count);
+  CU(cudaSetDevice(device));
+  fmp_ctx_s* c = new fmp_ctx_s;
+  c->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FMP_ECUDA, "stream: %s", cudaGetErrorString(e));
+  }
+  c->cur = c->own;
+  *out = c;
+  return FMP_OK;
+}
+
+int fmp_ctx_destroy(fmp_ctx ctx) {
+  if (!ctx) return FMP_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->cur);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+  return FMP_OK;
+}
+
+int fmp_ctx_set_stream(fmp_ctx ctx, void* stream) {
+  if (!ctx) return fail(FMP_EINVAL, "null context");
+  ctx->cur = stream ? (cudaStream_t)stream : ctx->own;
+  return FMP_OK;
+}
+
+void* fmp_ctx_stream(fmp_ctx ctx) { return ctx ? (void*)ctx->cur : nullptr; }
+
+int fmp_ctx_synchronize(fmp_ctx ctx) {
+  if (!ctx) return fail(FMP_EINVAL, "null context");
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->cur));
+  return FMP_OK;
+}
+
+int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows, uint64_t m,
+                        fmp_op* out) {
+  if (!ctx || !out) return fail(FMP_EINVAL, "null handle");
+  if (kind != FMP_FOURIER && kind != FMP_HADAMARD) return fail(FMP_EINVAL, "unknown kind %d", kind);
+  if (n == 0) return fail(FMP_EINVAL, "transform size must be positive");
+  if (!pow2(n)) {
+    if (kind == FMP_HADAMARD) return fail(FMP_EINVAL, "hadamard size must be a power of two");
+    return fail(FMP_EUNSUPPORTED, "non power-of-two Fourier sizes (the reference's dense "
+                                  "fallback) are not implemented on the GPU path");
+  }
+  if (n > (1ull << 28)) return fail(FMP_EUNSUPPORTED, "n = %llu exceeds 2^28", (unsigned long long)n);
+  if (!rows || m == 0) return fail(FMP_EINVAL, "row selection must be non-empty");
+  if (m > n) return fail(FMP_EINVAL, "row selection larger than the transform size");
+  std::vector<uint64_t> r(rows, rows + m);
+  std::sort(r.begin(), r.end());
+  for (uint64_t i = 0; i < m; ++i) {
+    if (r[i] < 1 || r[i] > n) return fail(FMP_EINVAL, "row index out of range");
+    if (i && r[i] == r[i - 1]) return fail(FMP_EINVAL, "row indices must be distinct");
+  }
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  fmp_op_s* op = new fmp_op_s;
+  op->ctx = ctx;
+  op->rows = r;
+  DevOp& d = op->d;
+  d.kind = kind;
+  d.n = (int64_t)n;
+  d.m = (int64_t)m;
+  d.log2n = ilog2(n);
+  auto cleanup = [&](int code) {
+    fmp_operator_destroy(op);
+    return code;
+  };
+  std::vector<uint32_t> om(m);
+  for (uint64_t i = 0; i < m; ++i) om[i] = (uint32_t)(r[i] - 1);
+  cudaError_t e = cudaSuccess;
+#define OPALLOC(p, bytes) \
+  if ((e = cudaMalloc(&p, (bytes))) != cudaSuccess) return cleanup(fail(FMP_ENOMEM, "operator alloc: %s", cudaGetErrorString(e)))
+  OPALLOC(d.omega, m * 4);
+  OPALLOC(d.g64, n * 16);
+  if (kind == FMP_FOURIER) {
+    OPALLOC(d.tw64, n * 16);
+    OPALLOC(d.tw32, n * 8);
+    OPALLOC(d.g32, n * 8);
+  } else {
+    OPALLOC(d.gr64, n * 8);
+    if (m <= 32767) OPALLOC(d.glat, n * 2);
+  }
+#undef OPALLOC
+  cudaStream_t st = ctx->cur;
+  int launches = 0;
+  if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cleanup(fail(FMP_ECUDA, "omega copy: %s", cudaGetErrorString(e)));
+  if (kind == FMP_FOURIER) {
+    if ((e = fmp::launch_twiddles(d, st)) != cudaSuccess)
+      return cleanup(fail(FMP_ECUDA, "twiddles: %s", cudaGetErrorString(e)));
+    ++launches;
+  }
+  // c = apply_adjoint(apply(e1)) with apply(e1) = 1/sqrt(N) on every row
+  // (kernel.cpp:33); the transform runs in fp64
+  std::vector<double> ones(2 * m, 0.0);
+  const double isn = 1.0 / std::sqrt((double)n);
+  for (uint64_t i = 0; i < m; ++i) ones[2 * i] = isn;
+  void* din = nullptr;
+  int st2 = copy_in(ctx, S_AUX, ones.data(), ones.size() * 8, &din, st);
+  if (st2) return cleanup(st2);
+  st2 = run_transform(op, FMP_C128, 1, 1, 0, din, d.g64, 1, nullptr, st);
+  if (st2) return cleanup(st2);
+  launches += g_launch_count;
+  if ((e = fmp::launch_kernel_finish(d, st)) != cudaSuccess)
+    return cleanup(fail(FMP_ECUDA, "kernel finish: %s", cudaGetErrorString(e)));
+  launches += 2;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return cleanup(fail(FMP_ECUDA, "operator build: %s", cudaGetErrorString(e)));
+  g_launch_count = launches;
+  *out = op;
+  return FMP_OK;
+}
+
+int fmp_operator_destroy(fmp_op op) {
+  if (!op) return FMP_OK;
+  cudaSetDevice(op->ctx->device);
+  cudaStreamSynchronize(op->ctx->cur);
+  DevOp& d = op->d;
+  for (void* p : {(void*)d.omega, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
+                  (void*)d.gr64, (void*)d.glat})
+    if (p) cudaFree(p);
+  delete op;
+  return FMP_OK;
+}
+
+int fmp_operator_info(fmp_op op, int* kind, uint64_t* n, uint64_t* m) {
+  if (!op) return fail(FMP_EINVAL, "null operator");
+  if (kind) *kind = op->d.kind;
+  if (n) *n = (uint64_t)op->d.n;
+  if (m) *m = (uint64_t)op->d.m;
+  return FMP_OK;
+}
+
+int fmp_operator_kernel(fmp_op op, double* c_out, double* values_out, uint32_t* value_index_out,
+                        uint64_t* nvalues) {
+  if (!op || !c_out) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(op->ctx->device));
+  const uint64_t n = (uint64_t)op->d.n;
+  CU(cudaMemcpyAsync(c_out, op->d.g64, n * 16, cudaMemcpyDeviceToHost, op->ctx->cur));
+  CU(cudaStreamSynchronize(op->ctx->cur));
+  if (op->d.kind == fmp::FOURIER) {
+    if (nvalues) *nvalues = 0;
+    return FMP_OK;
+  }
+  // value table of the snapped lattice (kernel.cpp:56-69), from the exact c
+  std::vector<double> scaled(n);
+  for (uint64_t j = 0; j < n; ++j) scaled[j] = std::round(c_out[2 * j] * (double)n);
+  std::vector<double> distinct = scaled;
+  std::sort(distinct.begin(), distinct.end());
+  distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+  if (nvalues) *nvalues = distinct.size();
+  if (values_out)
+    for (size_t i = 0; i < distinct.size(); ++i) values_out[i] = distinct[i] / (double)n;
+  if (value_index_out)
+    for (uint64_t j = 0; j < n; ++j)
+      value_index_out[j] = (uint32_t)(std::lower_bound(distinct.begin(), distinct.end(), scaled[j]) -
+                                      distinct.begin());
+  return FMP_OK;
+}
+
+// ------------------------------------------------------------- transforms
+static int transform_host(fmp_op op, int dtype, int inverse, int in_omega, int out_omega,
+                          const void* in, uint64_t batch, void* out, uint64_t* amax) {
+  if (!op) return fail(FMP_EINVAL, "null operator");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  if (!in || (!out && !amax)) return fail(FMP_EINVAL, "null buffer");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  const size_t eb = fmp::elem_bytes(dtype);
+  const size_t inb = batch * (in_omega ? op->d.m : op->d.n) * eb;
+  const size_t outb = batch * (out_omega ? op->d.m : op->d.n) * eb;
+  cudaStream_t st = ctx->cur;
+  void *din = nullptr, *dout = nullptr;
+  uint64_t* damax = nullptr;
+  if (int s = copy_in(ctx, S_IN, in, inb, &din, st)) return s;
+  if (out) ALLOC(dout, S_OUT, outb);
+  if (amax) ALLOC(damax, S_IDX, batch * 8);
+  if (int s = run_transform(op, dtype, inverse, in_omega, out_omega, din, dout, batch, damax, st))
+    return s;
+  if (out) CU(cudaMemcpyAsync(out, dout, outb, cudaMemcpyDeviceToHost, st));
+  if (amax) CU(cudaMemcpyAsync(amax, damax, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+int fmp_apply(fmp_op op, int dtype, const void* x, uint64_t batch, void* y_out) {
+  if (!y_out) return fail(FMP_EINVAL, "null output");
+  return transform_host(op, dtype, 0, 0, 1, x, batch, y_out, nullptr);
+}
+
+int fmp_apply_adjoint(fmp_op op, int dtype, const void* r, uint64_t batch, void* h_out,
+                      uint64_t* argmax_out) {
+  return transform_host(op, dtype, 1, 1, 0, r, batch, h_out, argmax_out);
+}
+
+int fmp_unitary_forward(fmp_op op, int dtype, const void* v, uint64_t batch, void* out) {
+  if (!out) return fail(FMP_EINVAL, "null output");
+  return transform_host(op, dtype, 0, 0, 0, v, batch, out, nullptr);
+}
+
+int fmp_unitary_adjoint(fmp_op op, int dtype, const void* v, uint64_t batch, void* out) {
+  if (!out) return fail(FMP_EINVAL, "null output");
+  return transform_host(op, dtype, 1, 0, 0, v, batch, out, nullptr);
+}
+
+int fmp_apply_dev(fmp_op op, int dtype, const void* x, uint64_t batch, void* y_out, void* stream) {
+  if (!op || !x || !y_out) return fail(FMP_EINVAL, "null argument");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  CU(cudaSetDevice(op->ctx->device));
+  std::lock_guard<std::mutex> lk(op->ctx->mu);
+  return run_transform(op, dtype, 0, 0, 1, x, y_out, batch, nullptr, pick_stream(op->ctx, stream));
+}
+
+int fmp_apply_adjoint_dev(fmp_op op, int dtype, const void* r, uint64_t batch, void* h_out,
+                          uint64_t* argmax_out, void* stream) {
+  if (!op || !r || (!h_out && !argmax_out)) return fail(FMP_EINVAL, "null argument");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  CU(cudaSetDevice(op->ctx->device));
+  std::lock_guard<std::mutex> lk(op->ctx->mu);
+  return run_transform(op, dtype, 1, 1, 0, r, h_out, batch, argmax_out,
+                       pick_stream(op->ctx, stream));
+}
+
+// ------------------------------------------------------------ fast update
+static int fast_update_dev_locked(fmp_op op, int dtype, const void* h0, const uint32_t* sup0,
+                                  const void* coeffs, uint64_t t, uint64_t batch, void* h_out,
+                                  uint64_t* amax, cudaStream_t st) {
+  fmp_ctx_s* ctx = op->ctx;
+  if (op->d.kind == fmp::HADAMARD && !op->d.glat)
+    return fail(FMP_EUNSUPPORTED, "hadamard fast update needs m <= 32767 (int16 lattice)");
+  fmp::FastUpdateArgs a{};
+  a.op = &op->d;
+  a.dtype = dtype;
+  a.h0 = h0;
+  a.support = sup0;
+  a.coeffs = coeffs;
+  a.t = (int64_t)t;
+  a.batch = (int64_t)batch;
+  a.h_out = h_out;
+  a.argmax_out = amax;
+  a.grid = fmp::fast_update_grid(op->d, dtype, (int64_t)batch);
+  if (!h_out && t > 1024) {
+    void* hb;
+    ALLOC(hb, S_AUX, batch * op->d.n * fmp::elem_bytes(dtype));
+    a.h_out = hb;
+  }
+  double* mag;
+  ALLOC(mag, S_MAG, (size_t)a.grid * op->d.n * 8);
+  a.mag_ws = mag;
+  CU(fmp::launch_fast_update(a, st));
+  g_launch_count = fmp::last_launch_count();
+  return FMP_OK;
+}
+
+int fmp_fast_update(fmp_op op, int dtype, const void* h0, const uint64_t* support,
+                    const void* coeffs, uint64_t t, uint64_t batch, void* h_out,
+                    uint64_t* argmax_out) {
+  if (!op) return fail(FMP_EINVAL, "null operator");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  if (!h0 || (t && (!support || !coeffs)) || (!h_out && !argmax_out))
+    return fail(FMP_EINVAL, "null buffer");
+  const uint64_t n = (uint64_t)op->d.n;
+  // kernel.cpp:213-222: support within 1..n and distinct, per problem
+  std::vector<uint32_t> s0(batch * t);
+  std::vector<uint64_t> tmp(t);
+  for (uint64_t b = 0; b < batch; ++b) {
+    for (uint64_t i = 0; i < t; ++i) {
+      const uint64_t v = support[b * t + i];
+      if (v < 1 || v > n) return fail(FMP_EINVAL, "fast_update: support index out of range");
+      s0[b * t + i] = (uint32_t)(v - 1);
+      tmp[i] = v;
+    }
+    std::sort(tmp.begin(), tmp.end());
+    for (uint64_t i = 1; i < t; ++i)
+      if (tmp[i] == tmp[i - 1]) return fail(FMP_EINVAL, "fast_update: duplicate support index");
+  }
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->cur;
+  const size_t eb = fmp::elem_bytes(dtype);
+  void *dh0, *dsup = nullptr, *dco = nullptr, *dout = nullptr;
+  uint64_t* damax = nullptr;
+  if (int s = copy_in(ctx, S_IN, h0, batch * n * eb, &dh0, st)) return s;
+  if (t) {
+    if (int s = copy_in(ctx, S_SUP, s0.data(), s0.size() * 4, &dsup, st)) return s;
+    if (int s = copy_in(ctx, S_CO, coeffs, batch * t * eb, &dco, st)) return s;
+  }
+  if (h_out) ALLOC(dout, S_OUT, batch * n * eb);
+  if (argmax_out) ALLOC(damax, S_IDX, batch * 8);
+  if (int s = fast_update_dev_locked(op, dtype, dh0, (const uint32_t*)dsup, dco, t, batch, dout,
+                                     damax, st))
+    return s;
+  if (h_out) CU(cudaMemcpyAsync(h_out, dout, batch * n * eb, cudaMemcpyDeviceToHost, st));
+  if (argmax_out) CU(cudaMemcpyAsync(argmax_out, damax, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+int fmp_fast_update_dev(fmp_op op, int dtype, const void* h0, const uint32_t* support0,
+                        const void* coeffs, uint64_t t, uint64_t batch, void* h_out,
+                        uint64_t* argmax_out, void* stream) {
+  if (!op) return fail(FMP_EINVAL, "null operator");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  if (!h0 || (t && (!support0 || !coeffs)) || (!h_out && !argmax_out))
+    return fail(FMP_EINVAL, "null buffer");
+  CU(cudaSetDevice(op->ctx->device));
+  std::lock_guard<std::mutex> lk(op->ctx->mu);
+  return fast_update_dev_locked(op, dtype, h0, support0, coeffs, t, batch, h_out, argmax_out,
+                                pick_stream(op->ctx, stream));
+}
+
+int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t batch,
+                    uint64_t* idx_out) {
+  if (!ctx || !h || !idx_out) return fail(FMP_EINVAL, "null argument");
+  if (dtype < 0 || dtype > 3) return fail(FMP_EINVAL, "unknown dtype");
+  if (n == 0) return fail(FMP_EINVAL, "empty vector");
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->cur;
+  void* dh;
+  uint64_t* di;
+  if (int s = copy_in(ctx, S_IN, h, batch * n * fmp::elem_bytes(dtype), &dh, st)) return s;
+  ALLOC(di, S_IDX, batch * 8);
+  fmp::ArgmaxArgs a{dtype, dh, (int64_t)n, (int64_t)batch, di};
+  CU(fmp::launch_argmax(a, st));
+  g_launch_count = 1;
+  CU(cudaMemcpyAsync(idx_out, di, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+// -------------------------------------------------------------------- OMP
+static int omp_validate(fmp_op op, int dtype, const fmp_omp_config* cfg) {
+  if (!op || !cfg) return fail(FMP_EINVAL, "null argument");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  if (cfg->max_iterations < 1) return fail(FMP_EINVAL, "omp_solve: max_iterations must be >= 1");
+  if (!cfg->tolerances && !(cfg->tolerance >= 0.0))
+    return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
+  if (cfg->mode < 0 || cfg->mode > 3) return fail(FMP_EINVAL, "unknown correlation mode");
+  if (cfg->max_iterations > 4096) return fail(FMP_EUNSUPPORTED, "max_iterations > 4096");
+  if (op->d.kind == fmp::HADAMARD && !op->d.glat)
+    return fail(FMP_EUNSUPPORTED, "hadamard solve needs m <= 32767 (int16 lattice)");
+  return FMP_OK;
+}
+
+static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg) {
+  switch (cfg->mode) {
+    case FMP_MODE_CONVENTIONAL: return 0;
+    case FMP_MODE_FAST: return std::numeric_limits<int64_t>::max();
+    case FMP_MODE_ADAPTIVE: return (int64_t)fmp_crossover_iteration(op->d.kind, (uint64_t)op->d.n);
+    default: return (int64_t)std::min<uint64_t>(cfg->fast_until, (uint64_t)INT64_MAX);
+  }
+}
+
+static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
+                          const fmp_omp_config* cfg, const double* dtol, fmp_omp_result* out,
+                          cudaStream_t st) {
+  fmp_ctx_s* ctx = op->ctx;
+  const int64_t T = (int64_t)cfg->max_iterations;
+  const int64_t n = op->d.n, m = op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  fmp::OmpArgs a{};
+  a.op = &op->d;
+  a.dtype = dtype;
+  a.y = y;
+  a.tol = dtol;
+  a.batch = (int64_t)batch;
+  a.max_iter = T;
+  a.fast_until = fast_until_of(op, cfg);
+  a.support = out->support;
+  a.coeffs = (double2*)out->coeffs;
+  a.size = out->support_size;
+  a.iters = out->iterations;
+  a.resid = out->residual;
+  a.aborted = out->aborted;
+  a.modes = out->modes;
+  a.hlen = out->history_len;
+  a.hist = cfg->record_correlations ? out->history : nullptr;
+  a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
+  double2* w;
+  ALLOC(w, S_W, (size_t)a.grid * (T * (T + 1) / 2) * 16);
+  a.w_ws = w;
+  void* h0;
+  ALLOC(h0, S_H0, (size_t)a.grid * n * eb);
+  a.h0_ws = h0;
+  double* mag;
+  ALLOC(mag, S_MAG, (size_t)a.grid * n * 8);
+  a.mag_ws = mag;
+  void* r;
+  ALLOC(r, S_R, (size_t)a.grid * m * eb);
+  a.r_ws = r;
+  int* q;
+  ALLOC(q, S_Q, 64);
+  a.queue = q;
+  CU(cudaMemsetAsync(q, 0, 4, st));
+  cudaError_t e = fmp::launch_omp(a, st);
+  g_launch_count = fmp::last_launch_count();
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(FMP_EUNSUPPORTED, "n = %lld, max_iterations = %lld exceed the fused solver's "
+                "shared-memory plan", (long long)n, (long long)T);
+  CU(e);
+  return FMP_OK;
+}
+
+int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
+                      const fmp_omp_config* cfg, fmp_omp_result* out, void* stream) {
+  if (int s = omp_validate(op, dtype, cfg)) return s;
+  if (!y || !out || !out->support || !out->coeffs || !out->support_size || !out->iterations ||
+      !out->residual || !out->aborted)
+    return fail(FMP_EINVAL, "null buffer");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = pick_stream(ctx, stream);
+  const double* dtol = cfg->tolerances;
+  if (!dtol) {
+    std::vector<double> tv(batch, cfg->tolerance);
+    void* p;
+    if (int s = copy_in(ctx, S_TOL, tv.data(), batch * 8, &p, st)) return s;
+    CU(cudaStreamSynchronize(st));  // the host vector dies here
+    dtol = (const double*)p;
+  }
+  return omp_dev_locked(op, dtype, y, batch, cfg, dtol, out, st);
+}
+
+int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp_omp_config* cfg,
+                  fmp_omp_result* out) {
+  if (int s = omp_validate(op, dtype, cfg)) return s;
+  if (!y || !out || !out->support || !out->coeffs || !out->support_size || !out->iterations ||
+      !out->residual || !out->aborted)
+    return fail(FMP_EINVAL, "null buffer");
+  if (cfg->record_correlations && !out->history)
+    return fail(FMP_EINVAL, "record_correlations needs a history buffer");
+  if (cfg->tolerances)
+    for (uint64_t b = 0; b < batch; ++b)
+      if (!(cfg->tolerances[b] >= 0.0)) return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->cur;
+  const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  void* dy;
+  if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
+  std::vector<double> tv;
+  if (!cfg->tolerances) tv.assign(batch, cfg->tolerance);
+  void* dtol;
+  if (int s = copy_in(ctx, S_TOL, cfg->tolerances ? cfg->tolerances : tv.data(), batch * 8, &dtol, st))
+    return s;
+  fmp_omp_result d{};
+  ALLOC(d.support, S_OSUP, batch * T * 8);
+  ALLOC(d.coeffs, S_OCO, batch * T * 16);
+  ALLOC(d.support_size, S_OSZ, batch * 8);
+  ALLOC(d.iterations, S_OIT, batch * 8);
+  ALLOC(d.residual, S_ORES, batch * 8);
+  ALLOC(d.aborted, S_OAB, batch * 4);
+  if (out->modes) ALLOC(d.modes, S_OMOD, batch * T);
+  if (out->history_len || cfg->record_correlations) ALLOC(d.history_len, S_OHL, batch * 8);
+  if (cfg->record_correlations) ALLOC(d.history, S_OHIST, batch * T * n * eb);
+  if (int s = omp_dev_locked(op, dtype, dy, batch, cfg, (const double*)dtol, &d, st)) return s;
+  CU(cudaMemcpyAsync(out->support, d.support, batch * T * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->coeffs, d.coeffs, batch * T * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->support_size, d.support_size, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->iterations, d.iterations, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->residual, d.residual, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->aborted, d.aborted, batch * 4, cudaMemcpyDeviceToHost, st));
+  if (out->modes) CU(cudaMemcpyAsync(out->modes, d.modes, batch * T, cudaMemcpyDeviceToHost, st));
+  if (out->history_len)
+    CU(cudaMemcpyAsync(out->history_len, d.history_len, batch * 8, cudaMemcpyDeviceToHost, st));
+  if (cfg->record_correlations)
+    CU(cudaMemcpyAsync(out->history, d.history, batch * T * n * eb, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+// Device building blocks for the OMP correlation path on sm_100a.
+//
+// Element types: complex data is double2 (c128) or float2 (c64); real
+// (Hadamard with real data) is double (f64) or float (f32).  Atom and row
+// indices are 0-based on the device (the C ABI converts from the reference's
+// 1-based convention, proj/include/fastmp/transform.hpp:32-34).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fmp {
+
+constexpr double kTieBandRel = 1e-9;  // solvers.cpp:40
+
+// ------------------------------------------------------------ element ops
+template <class T> struct vec2;
+template <> struct vec2<double> { using type = double2; };
+template <> struct vec2<float> { using type = float2; };
+
+template <class T, bool CPLX> struct elem { using V = typename vec2<T>::type; };
+template <class T> struct elem<T, false> { using V = T; };
+
+__device__ __forceinline__ double2 zero_of(double2) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ float2 zero_of(float2) { return make_float2(0.f, 0.f); }
+__device__ __forceinline__ double zero_of(double) { return 0.0; }
+__device__ __forceinline__ float zero_of(float) { return 0.f; }
+
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ float add(float a, float b) { return a + b; }
+__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__device__ __forceinline__ float sub(float a, float b) { return a - b; }
+
+__device__ __forceinline__ double2 scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 scale(float2 a, double s) { return make_float2(a.x * (float)s, a.y * (float)s); }
+__device__ __forceinline__ double scale(double a, double s) { return a * s; }
+__device__ __forceinline__ float scale(float a, double s) { return a * (float)s; }
+
+// |z|^2 evaluated in fp64 (float products are exact in double)
+__device__ __forceinline__ double mag2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double mag2(float2 a) { return (double)a.x * a.x + (double)a.y * a.y; }
+__device__ __forceinline__ double mag2(double a) { return a * a; }
+__device__ __forceinline__ double mag2(float a) { return (double)a * a; }
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 conj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ float2 conj(float2 a) { return make_float2(a.x, -a.y); }
+
+// to/from the fp64 complex the least-squares state is kept in
+__device__ __forceinline__ void from_c128(double2 v, double2& o) { o = v; }
+__device__ __forceinline__ void from_c128(double2 v, float2& o) { o = make_float2((float)v.x, (float)v.y); }
+__device__ __forceinline__ void from_c128(double2 v, double& o) { o = v.x; }
+__device__ __forceinline__ void from_c128(double2 v, float& o) { o = (float)v.x; }
+__device__ __forceinline__ double2 to_c128(double2 v) { return v; }
+__device__ __forceinline__ double2 to_c128(float2 v) { return make_double2(v.x, v.y); }
+__device__ __forceinline__ double2 to_c128(double v) { return make_double2(v, 0.0); }
+__device__ __forceinline__ double2 to_c128(float v) { return make_double2(v, 0.0); }
+
+// acc -= x * g, with x complex (xn = -x pre-negated) and g complex or real
+__device__ __forceinline__ void msub(double2& acc, double2 xn, double2 g) {
+  acc.x = fma(xn.x, g.x, acc.x);
+  acc.x = fma(-xn.y, g.y, acc.x);
+  acc.y = fma(xn.x, g.y, acc.y);
+  acc.y = fma(xn.y, g.x, acc.y);
+}
+__device__ __forceinline__ void msub(float2& acc, float2 xn, float2 g) {
+  acc.x = fmaf(xn.x, g.x, acc.x);
+  acc.x = fmaf(-xn.y, g.y, acc.x);
+  acc.y = fmaf(xn.x, g.y, acc.y);
+  acc.y = fmaf(xn.y, g.x, acc.y);
+}
+__device__ __forceinline__ void msub(double2& acc, double2 xn, double g) {
+  acc.x = fma(xn.x, g, acc.x);
+  acc.y = fma(xn.y, g, acc.y);
+}
+__device__ __forceinline__ void msub(float2& acc, float2 xn, float g) {
+  acc.x = fmaf(xn.x, g, acc.x);
+  acc.y = fmaf(xn.y, g, acc.y);
+}
+__device__ __forceinline__ void msub(double& acc, double xn, double g) { acc = fma(xn, g, acc); }
+__device__ __forceinline__ void msub(float& acc, float xn, float g) { acc = fmaf(xn, g, acc); }
+
+// ------------------------------------------------------ transform passes
+//
+// In-place transforms on a buffer laid out with one pad slot every RMAX
+// elements (conflict-free strided smem access for every pass).  The Fourier
+// transform is a decimation-in-time FFT that consumes bit-reversed input and
+// produces natural order (the same factorisation as the reference's radix-2
+// DIT, transform.cpp:60-84, grouped into radix-R passes); callers scatter
+// their input straight to bit-reversed slots, so no permutation pass exists.
+// The Hadamard transform (transform.cpp:86-100) runs on natural order.
+
+__host__ __device__ constexpr double c16(int k) {  // cos(2 pi k / 16)
+  return (k & 15) == 0 ? 1.0
+       : (k & 15) == 1 ? 0.92387953251128675613
+       : (k & 15) == 2 ? 0.70710678118654752440
+       : (k & 15) == 3 ? 0.38268343236508977173
+       : (k & 15) == 4 ? 0.0
+       : (k & 15) == 5 ? -0.38268343236508977173
+       : (k & 15) == 6 ? -0.70710678118654752440
+       : (k & 15) == 7 ? -0.92387953251128675613
+       : (k & 15) == 8 ? -1.0
+       : (k & 15) == 9 ? -0.92387953251128675613
+       : (k & 15) == 10 ? -0.70710678118654752440
+       : (k & 15) == 11 ? -0.38268343236508977173
+       : (k & 15) == 12 ? 0.0
+       : (k & 15) == 13 ? 0.38268343236508977173
+       : (k & 15) == 14 ? 0.70710678118654752440
+       : 0.92387953251128675613;
+}
+
+// v * W_len^j, W = exp(-2 pi i / len) (conjugated when INV); len <= 16
+template <bool INV, class V>
+__device__ __forceinline__ V mul_wconst(V v, int len, int j) {
+  if (j == 0) return v;
+  const int k = j * (16 / len);  // W_16^k
+  if (k == 4) {  // -i (forward) / +i (inverse)
+    V o;
+    if (INV) { o.x = -v.y; o.y = v.x; } else { o.x = v.y; o.y = -v.x; }
+    return o;
+  }
+  const double c = c16(k), s = INV ? c16(k - 4) : -c16(k - 4);  // W = c + i s
+  V w;
+  w.x = (decltype(v.x))c;
+  w.y = (decltype(v.x))s;
+  return cmul(v, w);
+}
+
+// R-point DFT in registers, input in bit-reversed order, output natural
+template <int R, bool INV, class V>
+__device__ __forceinline__ void dft_reg(V (&v)[R]) {
+#pragma unroll
+  for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+    for (int base = 0; base < R; base += len) {
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        const V t = mul_wconst<INV>(v[base + j + len / 2], len, j);
+        const V u = v[base + j];
+        v[base + j] = add(u, t);
+        v[base + j + len / 2] = sub(u, t);
+      }
+    }
+  }
+}
+
+// R-point Walsh-Hadamard in registers (natural order)
+template <int R, class V>
+__device__ __forceinline__ void wht_reg(V (&v)[R]) {
+#pragma unroll
+  for (int half = 1; half < R; half <<= 1) {
+#pragma unroll
+    for (int base = 0; base < R; base += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const V a = v[base + j], b = v[base + j + half];
+        v[base + j] = add(a, b);
+        v[base + j + half] = sub(a, b);
+      }
+    }
+  }
+}
+
+template <int LOGR>
+__device__ __forceinline__ int padx(int p) { return p + (p >> LOGR); }
+
+__device__ __forceinline__ unsigned brev_n(unsigned x, int log2n) {
+  return log2n ? (__brev(x) >> (32 - log2n)) : 0u;
+}
+
+template <int R>
+__host__ __device__ constexpr int brev_small(int j) {
+  int r = 0;
+  for (int b = 1, rb = R >> 1; b < R; b <<= 1, rb >>= 1)
+    if (j & b) r |= rb;
+  return r;
+}
+
+template <int R> struct log2_of { static constexpr int v = R <= 1 ? 0 : 1 + log2_of<R / 2>::v; };
+template <> struct log2_of<1> { static constexpr int v = 0; };
+
+// One radix-R sub-problem u of the pass over sub-blocks of span S = 2^logS
+// (see file comment).  Twiddles tw[k] = exp(-2 pi i k / 2^log2tab)
+// (conjugated when INV); the table may be longer than the vector.
+template <int R, int LOGP, bool INV, bool HAD, class V>
+__device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2tab,
+                                         const V* __restrict__ tw, int u) {
+  constexpr int LOGR = log2_of<R>::v;
+  const int S = 1 << logS;
+  const int o = u & (S - 1);
+  const int base = ((u >> logS) << (logS + LOGR)) + o;
+  V v[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) v[j] = buf[padx<LOGP>(base + j * S)];
+  if constexpr (HAD) {
+    wht_reg<R>(v);
+  } else {
+    if (logS > 0) {
+      // twiddle index brev(j) * o * 2^log2tab / (R S)
+      const int step = o << (log2tab - logS - LOGR);
+#pragma unroll
+      for (int j = 1; j < R; ++j) {
+        V w = tw[brev_small<R>(j) * step];
+        if (INV) w.y = -w.y;
+        v[j] = cmul(v[j], w);
+      }
+    }
+    dft_reg<R, INV>(v);
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) buf[padx<LOGP>(base + j * S)] = v[j];
+}
+
+template <int R, int LOGP, bool INV, bool HAD, class V>
+__device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS,
+                                               const V* __restrict__ tw,
+                                               int tid, int nth) {
+  constexpr int LOGR = log2_of<R>::v;
+  const int nsub = 1 << (log2n - LOGR);
+  for (int u = tid; u < nsub; u += nth)
+    pass_one<R, LOGP, INV, HAD>(buf, log2n, logS, log2n, tw, u);
+}
+
+// Whole in-place transform of one vector held by the calling block.
+// Ends with a __syncthreads().
+template <int RMAX, bool INV, bool HAD, class V>
+__device__ void block_transform(V* buf, int log2n, const V* __restrict__ tw,
+                                int tid, int nth) {
+  constexpr int LOGP = log2_of<RMAX>::v;
+  int s = 0;
+  for (; log2n - s >= LOGP; s += LOGP) {
+    transform_pass<RMAX, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth);
+    __syncthreads();
+  }
+  switch (log2n - s) {
+    case 1: transform_pass<2, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
+    case 2: transform_pass<4, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
+    case 3: transform_pass<8, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
+    default: break;
+  }
+}
+
+// ------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned warp_min_u(unsigned v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block-wide reductions; `red` needs 32 doubles of shared scratch.  Every
+// thread receives the result.  Contains two __syncthreads().
+__device__ __forceinline__ double block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = lane < nw ? red[lane] : 0.0;
+  return warp_max(r);
+}
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = lane < nw ? red[lane] : 0.0;
+  return warp_sum(r);
+}
+__device__ __forceinline__ unsigned block_min_u(unsigned v, unsigned* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_min_u(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  unsigned r = lane < nw ? red[lane] : 0xffffffffu;
+  return warp_min_u(r);
+}
+
+}  // namespace fmp

@@ -1,0 +1,148 @@
+// Internal helpers shared by the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "fmp_device.cuh"
+#include "fmp_kernels.cuh"
+
+namespace fmp {
+extern thread_local int g_launches;
+}  // namespace fmp
+
+namespace fmp {
+
+namespace {
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 1;
+  }
+  return sms;
+}
+
+int smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (v <= 0) v = 48 * 1024;
+  }
+  return v;
+}
+
+template <class V> struct scal;
+template <> struct scal<double2> { using T = double; };
+template <> struct scal<float2> { using T = float; };
+template <> struct scal<double> { using T = double; };
+template <> struct scal<float> { using T = float; };
+
+template <class V> __device__ __forceinline__ const V* twiddles(const DevOp& op);
+template <> __device__ __forceinline__ const double2* twiddles<double2>(const DevOp& op) { return op.tw64; }
+template <> __device__ __forceinline__ const float2* twiddles<float2>(const DevOp& op) { return op.tw32; }
+template <> __device__ __forceinline__ const double* twiddles<double>(const DevOp&) { return nullptr; }
+template <> __device__ __forceinline__ const float* twiddles<float>(const DevOp&) { return nullptr; }
+
+template <class V> __device__ __forceinline__ const V* fourier_table(const DevOp& op);
+template <> __device__ __forceinline__ const double2* fourier_table<double2>(const DevOp& op) { return op.g64; }
+template <> __device__ __forceinline__ const float2* fourier_table<float2>(const DevOp& op) { return op.g32; }
+template <> __device__ __forceinline__ const double* fourier_table<double>(const DevOp&) { return nullptr; }
+template <> __device__ __forceinline__ const float* fourier_table<float>(const DevOp&) { return nullptr; }
+
+constexpr int RMAX = 16;
+constexpr int LOGP = 4;
+constexpr int OMP_THREADS = 512;
+constexpr int FU_THREADS = 512;
+
+__device__ __forceinline__ double inv_sqrt_n(int n) { return 1.0 / sqrt((double)n); }
+
+// slot of logical input position p for the in-place transform
+template <bool HAD>
+__device__ __forceinline__ int in_slot(unsigned p, int log2n) {
+  return padx<LOGP>(HAD ? (int)p : (int)brev_n(p, log2n));
+}
+
+// ------------------------------------------------------------ fast tile
+// acc[r] (outputs i0 + lane + 32 r) -= sum_tau xn-scaled kernel entries.
+// Fourier: source (i - lambda) mod n (kernel.cpp:247-255, map_index
+// kernel.cpp:111-118); Hadamard: i XOR lambda on the integer lattice N*c
+// (kernel.cpp:227-238), xn = -x/N so that xn * k == -x * c exactly.
+template <class V, bool HAD, int RPT>
+__device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n,
+                                          const V* __restrict__ gF,
+                                          const int16_t* __restrict__ gH,
+                                          const unsigned* lam, const V* xn, int t) {
+  using T = typename scal<V>::T;
+  const int mask = n - 1;
+  if constexpr (!HAD) {
+#pragma unroll 2
+    for (int tau = 0; tau < t; ++tau) {
+      const int l = (int)lam[tau];
+      const V x = xn[tau];
+      const int w0 = (i0 - l) & mask;
+      if (w0 + 32 * RPT <= n) {
+        const V* p = gF + w0 + lane;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) msub(acc[r], x, p[32 * r]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) msub(acc[r], x, gF[(w0 + lane + 32 * r) & mask]);
+      }
+    }
+  } else {
+#pragma unroll 2
+    for (int tau = 0; tau < t; ++tau) {
+      const int l = (int)lam[tau];
+      const V x = xn[tau];
+      const int base = (i0 ^ (l & ~(32 * RPT - 1))) + (lane ^ (l & 31));
+      const int lr = (l >> 5) & (RPT - 1);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) msub(acc[r], x, (T)gH[base + 32 * (r ^ lr)]);
+    }
+  }
+}
+
+// single output (small n): h0 value in acc
+template <class V, bool HAD>
+__device__ __forceinline__ void fast_point(V& acc, int i, int n, const V* __restrict__ gF,
+                                           const int16_t* __restrict__ gH,
+                                           const unsigned* lam, const V* xn, int t) {
+  using T = typename scal<V>::T;
+  for (int tau = 0; tau < t; ++tau) {
+    const int l = (int)lam[tau];
+    if constexpr (!HAD) msub(acc, xn[tau], gF[(i - l) & (n - 1)]);
+    else msub(acc, xn[tau], (T)gH[i ^ l]);
+  }
+}
+
+// ----------------------------------------------------------------- argmax
+template <class V>
+__global__ void __launch_bounds__(512) k_argmax(const V* __restrict__ h, int64_t n,
+                                                int64_t batch, uint64_t* __restrict__ out) {
+  __shared__ double red[32];
+  __shared__ unsigned redu[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const V* hb = h + b * n;
+    double best = 0.0;
+    for (int64_t k = tid; k < n; k += nth) best = fmax(best, mag2(hb[k]));
+    best = block_max(best, red);
+    const double cut = best * (1.0 - kTieBandRel);
+    unsigned first = 0xffffffffu;
+    for (int64_t k = tid; k < n; k += nth)
+      if (mag2(hb[k]) >= cut) { first = (unsigned)k; break; }
+    first = block_min_u(first, redu);
+    if (tid == 0) out[b] = (first == 0xffffffffu ? 0u : first) + 1;  // 1-based
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace fmp

@@ -1,0 +1,109 @@
+// Kernel launch interface shared by the C ABI (fmp_capi.cu) and the kernels
+// (fmp_kernels.cu).  Plain structs of device pointers; no torch types.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fmp {
+
+enum Kind { FOURIER = 0, HADAMARD = 1 };
+enum DType { C128 = 0, C64 = 1, F64 = 2, F32 = 3 };
+
+inline int elem_bytes(int dt) { return dt == C128 ? 16 : (dt == F32 ? 4 : 8); }
+inline bool is_complex(int dt) { return dt == C128 || dt == C64; }
+inline bool is_double(int dt) { return dt == C128 || dt == F64; }
+
+// Device-resident operator Phi = S_Omega U (sensing.hpp:39-66) plus its
+// correlation kernel c = Phi^H Phi e_1 (kernel.hpp:31-40) in every storage
+// form the kernels read.
+struct DevOp {
+  int kind = 0;
+  int log2n = 0;
+  int64_t n = 0, m = 0;
+  uint32_t* omega = nullptr;  // m, 0-based rows, ascending
+  double2* tw64 = nullptr;    // n twiddles exp(-2 pi i k / n) (Fourier)
+  float2* tw32 = nullptr;
+  double2* g64 = nullptr;     // c, n entries, fp64 (Fourier: exact conj symmetry)
+  float2* g32 = nullptr;      // c rounded to c64 (Fourier)
+  double* gr64 = nullptr;     // c real part (Hadamard), exact k/N
+  int16_t* glat = nullptr;    // Hadamard lattice N*c (|N c| <= M); null if M > 32767
+};
+
+struct TransformArgs {
+  const DevOp* op;  // host copy of the device op (pointers are device)
+  int dtype;
+  int inverse;      // 1: adjoint U^H, 0: forward U
+  int in_omega;     // 1: input is m values scattered at Omega, 0: dense n
+  int out_omega;    // 1: output gathered at Omega (m values), 0: dense n
+  const void* in;
+  void* out;        // may be null when only the argmax is wanted
+  int64_t batch;
+  uint64_t* argmax_out;  // optional: band argmax of |out|^2 per vector (dense out only)
+  void* work;            // batch x n scratch, required when n > transform_max_n(dtype)
+};
+
+struct FastUpdateArgs {
+  const DevOp* op;
+  int dtype;
+  const void* h0;           // batch x n
+  const uint32_t* support;  // batch x t, 0-based atoms
+  const void* coeffs;       // batch x t, data dtype
+  int64_t t;
+  int64_t batch;
+  void* h_out;              // optional batch x n
+  uint64_t* argmax_out;     // optional batch
+  double* mag_ws;           // workspace (grid x n doubles) for the argmax
+  int grid;
+};
+
+struct ArgmaxArgs {
+  int dtype;
+  const void* h;
+  int64_t n, batch;
+  uint64_t* out;
+};
+
+struct OmpArgs {
+  const DevOp* op;
+  int dtype;
+  const void* y;            // batch x m (data dtype)
+  const double* tol;        // batch absolute tolerances
+  int64_t batch;
+  int64_t max_iter;         // T
+  int64_t fast_until;       // iterations t <= fast_until (t >= 2) use the fast update
+  // outputs
+  uint64_t* support;        // batch x T, 1-based atoms in selection order, 0 padded
+  double2* coeffs;          // batch x T
+  uint64_t* iters;          // batch (iterations_run)
+  uint64_t* size;           // batch (support size)
+  uint64_t* hlen;           // batch (correlation vectors computed), optional
+  double* resid;            // batch
+  int32_t* aborted;         // batch
+  uint8_t* modes;           // batch x T (1 fast, 0 conventional), optional
+  void* hist;               // batch x T x n (data dtype), optional
+  // workspace, per resident CTA
+  double2* w_ws;            // grid x T(T+1)/2
+  void* h0_ws;              // grid x n (data dtype)
+  double* mag_ws;           // grid x n
+  void* r_ws;               // grid x m (data dtype) when r is not in smem
+  int* queue;               // work counter (zeroed before launch)
+  int grid;
+};
+
+// launchers (return cudaError_t); all async on `stream`
+cudaError_t launch_transform(const TransformArgs& a, cudaStream_t stream);
+cudaError_t launch_fast_update(const FastUpdateArgs& a, cudaStream_t stream);
+cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t stream);
+cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t stream);
+cudaError_t launch_twiddles(const DevOp& op, cudaStream_t stream);
+cudaError_t launch_omp(const OmpArgs& a, cudaStream_t stream);
+// resident CTA count the OMP launcher will use (sizes the workspaces)
+int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
+int fast_update_grid(const DevOp& op, int dtype, int64_t batch);
+// largest n the smem-resident transform handles for this element size
+int64_t transform_max_n(int dtype);
+// number of kernel launches issued by the last launch_* call on this thread
+int last_launch_count();
+
+}  // namespace fmp

@@ -1,0 +1,271 @@
+// Batched structured transforms: conventional correlation Phi^H r,
+// Phi x, U v (transform.cpp:120-152, sensing.cpp:93-109), the band argmax
+// (solvers.cpp:90-101) and the correlation-kernel build (kernel.cpp:24-72).
+#include "fmp_kcommon.cuh"
+
+namespace fmp {
+namespace {
+// ------------------------------------------------------------- transform
+template <class V, bool INV, bool HAD>
+__global__ void __launch_bounds__(512) k_transform(DevOp op, const V* __restrict__ in,
+                                                   V* __restrict__ out, int64_t batch,
+                                                   int in_omega, int out_omega,
+                                                   uint64_t* __restrict__ amax) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[32];
+  __shared__ unsigned redu[32];
+  V* buf = reinterpret_cast<V*>(smem_raw);
+  const int n = (int)op.n, m = (int)op.m, log2n = op.log2n;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int nbuf = n + (n >> LOGP);
+  const V* tw = twiddles<V>(op);
+  const double sc = inv_sqrt_n(n);
+  const V z = zero_of(V{});
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    if (in_omega) {
+      for (int i = tid; i < nbuf; i += nth) buf[i] = z;
+      __syncthreads();
+      const V* r = in + b * m;
+      for (int j = tid; j < m; j += nth) buf[in_slot<HAD>(op.omega[j], log2n)] = r[j];
+    } else {
+      const V* v = in + b * n;
+      for (int k = tid; k < n; k += nth) buf[in_slot<HAD>((unsigned)k, log2n)] = v[k];
+    }
+    __syncthreads();
+    block_transform<RMAX, INV, HAD>(buf, log2n, tw, tid, nth);
+    if (out_omega) {
+      V* o = out + b * m;
+      for (int j = tid; j < m; j += nth) o[j] = scale(buf[padx<LOGP>((int)op.omega[j])], sc);
+    } else {
+      V* o = out ? out + b * n : nullptr;
+      double best = 0.0;
+      for (int k = tid; k < n; k += nth) {
+        const V v = scale(buf[padx<LOGP>(k)], sc);
+        if (o) o[k] = v;
+        best = fmax(best, mag2(v));
+      }
+      if (amax) {
+        best = block_max(best, red);
+        const double cut = best * (1.0 - kTieBandRel);
+        unsigned first = 0xffffffffu;
+        for (int k = tid; k < n; k += nth)
+          if (mag2(scale(buf[padx<LOGP>(k)], sc)) >= cut) { first = (unsigned)k; break; }
+        first = block_min_u(first, redu);
+        if (tid == 0) amax[b] = (first == 0xffffffffu ? 0u : first) + 1;  // 1-based
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ large-n transform path
+// n beyond one CTA's shared memory: the same radix passes, one launch per
+// pass, each thread one radix-R sub-problem of one vector in global memory.
+template <class V, bool HAD>
+__global__ void k_scatter_in(const V* __restrict__ in, V* __restrict__ work, int64_t batch,
+                             int in_omega, const uint32_t* __restrict__ omega, int64_t m,
+                             int log2n) {
+  const int64_t n = 1ll << log2n;
+  const int64_t len = in_omega ? m : n;
+  const int64_t total = batch * len;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u / len, j = u - b * len;
+    const unsigned p = in_omega ? omega[j] : (unsigned)j;
+    const unsigned slot = HAD ? p : brev_n(p, log2n);
+    work[b * n + slot] = in[u];
+  }
+}
+
+template <class V, int R, bool INV, bool HAD>
+__global__ void k_gpass(V* data, int64_t batch, int log2n, int logS, const V* __restrict__ tw) {
+  constexpr int LOGR = log2_of<R>::v;
+  const int64_t nsub = 1ll << (log2n - LOGR);
+  const int64_t total = batch * nsub;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u >> (log2n - LOGR);
+    pass_one<R, 31, INV, HAD>(data + (b << log2n), log2n, logS, log2n, tw, (int)(u & (nsub - 1)));
+  }
+}
+
+template <class V>
+__global__ void k_out(V* work, V* __restrict__ out, int64_t batch, int out_omega,
+                      const uint32_t* __restrict__ omega, int64_t m, int log2n) {
+  const int64_t n = 1ll << log2n;
+  const int64_t len = out_omega ? m : n;
+  const int64_t total = batch * len;
+  const double sc = 1.0 / sqrt((double)n);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u / len, j = u - b * len;
+    const V v = scale(work[b * n + (out_omega ? omega[j] : j)], sc);
+    if (out) out[u] = v;
+    else work[u] = v;  // dense, in place
+  }
+}
+
+// --------------------------------------------------------- kernel finish
+// c arrives in g64 from the adjoint transform of the Omega indicator scaled
+// by 1/sqrt(N) (= apply_adjoint(apply(e1)), kernel.cpp:33).
+__global__ void k_kernel_finish(DevOp op) {
+  const int64_t n = op.n;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (op.kind == FOURIER) {
+    // exact conjugate symmetry (kernel.cpp:35-45)
+    if (i == 0) {
+      op.g64[0].y = 0.0;
+      if (n % 2 == 0 && n > 1) op.g64[n / 2].y = 0.0;
+    } else if (2 * i < n) {
+      const double2 a = op.g64[i], b = op.g64[n - i];
+      const double2 avg = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      op.g64[i] = avg;
+      op.g64[n - i] = make_double2(avg.x, -avg.y);
+    }
+  } else if (i < n) {
+    // snap onto the integer lattice N*c (kernel.cpp:46-55)
+    const double k = round(op.g64[i].x * (double)n);
+    op.g64[i] = make_double2(k / (double)n, 0.0);
+    op.gr64[i] = k / (double)n;
+    if (op.glat) op.glat[i] = (int16_t)k;
+  }
+}
+
+__global__ void k_kernel_f32(DevOp op) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < op.n) op.g32[i] = make_float2((float)op.g64[i].x, (float)op.g64[i].y);
+}
+
+__global__ void k_twiddles(DevOp op) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < op.n) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)op.n, &s, &c);
+    op.tw64[k] = make_double2(c, s);
+    op.tw32[k] = make_float2((float)c, (float)s);
+  }
+}
+
+template <class V, bool INV, bool HAD>
+cudaError_t launch_tr_t(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  const int64_t n = op.n;
+  const size_t smem = (size_t)(n + (n >> LOGP)) * sizeof(V);
+  int threads = (int)std::min<int64_t>(512, std::max<int64_t>(32, n / RMAX));
+  threads = ((threads + 31) / 32) * 32;
+  auto k = k_transform<V, INV, HAD>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.batch, (int64_t)num_sms() * std::max(occ, 1)));
+  k<<<(int)grid, threads, smem, st>>>(op, (const V*)a.in, (V*)a.out, a.batch, a.in_omega,
+                                       a.out_omega, a.argmax_out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <class V, bool INV, bool HAD>
+cudaError_t launch_tr_global(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  if (!a.work) return cudaErrorInvalidValue;
+  V* work = (V*)a.work;
+  const int log2n = op.log2n;
+  const int64_t n = op.n;
+  const int grid = num_sms() * 8;
+  cudaError_t e;
+  if (a.in_omega) {
+    e = cudaMemsetAsync(work, 0, (size_t)a.batch * n * sizeof(V), st);
+    if (e != cudaSuccess) return e;
+  }
+  k_scatter_in<V, HAD><<<grid, 256, 0, st>>>((const V*)a.in, work, a.batch, a.in_omega,
+                                             op.omega, op.m, log2n);
+  ++g_launches;
+  const V* tw = nullptr;
+  if constexpr (!HAD) tw = (const V*)(sizeof(V) == 16 ? (const void*)op.tw64 : (const void*)op.tw32);
+  int s = 0;
+  for (; log2n - s >= LOGP; s += LOGP) {
+    k_gpass<V, 16, INV, HAD><<<grid, 256, 0, st>>>(work, a.batch, log2n, s, tw);
+    ++g_launches;
+  }
+  switch (log2n - s) {
+    case 1: k_gpass<V, 2, INV, HAD><<<grid, 256, 0, st>>>(work, a.batch, log2n, s, tw); ++g_launches; break;
+    case 2: k_gpass<V, 4, INV, HAD><<<grid, 256, 0, st>>>(work, a.batch, log2n, s, tw); ++g_launches; break;
+    case 3: k_gpass<V, 8, INV, HAD><<<grid, 256, 0, st>>>(work, a.batch, log2n, s, tw); ++g_launches; break;
+    default: break;
+  }
+  V* out = (V*)a.out;
+  k_out<V><<<grid, 256, 0, st>>>(work, (a.out_omega || out) ? out : nullptr, a.batch,
+                                 a.out_omega, op.omega, op.m, log2n);
+  ++g_launches;
+  if (a.argmax_out && !a.out_omega) {
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+    k_argmax<V><<<g2, 512, 0, st>>>(out ? out : work, n, a.batch, a.argmax_out);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+template <class V, bool HAD>
+cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
+  if (a.op->n > transform_max_n(a.dtype))
+    return a.inverse ? launch_tr_global<V, true, HAD>(a, st) : launch_tr_global<V, false, HAD>(a, st);
+  return a.inverse ? launch_tr_t<V, true, HAD>(a, st) : launch_tr_t<V, false, HAD>(a, st);
+}
+
+}  // namespace
+
+thread_local int g_launches = 0;
+
+int last_launch_count() { return g_launches; }
+
+int64_t transform_max_n(int dtype) {
+  const int64_t cap = (int64_t)smem_optin() - 2048;
+  int64_t n = 1;
+  while ((2 * n + ((2 * n) >> LOGP)) * elem_bytes(dtype) <= cap) n *= 2;
+  return n;
+}
+
+cudaError_t launch_transform(const TransformArgs& a, cudaStream_t st) {
+  g_launches = 0;
+  const bool had = a.op->kind == HADAMARD;
+  switch (a.dtype) {
+    case C128: return had ? launch_tr_v<double2, true>(a, st) : launch_tr_v<double2, false>(a, st);
+    case C64: return had ? launch_tr_v<float2, true>(a, st) : launch_tr_v<float2, false>(a, st);
+    case F64: return had ? launch_tr_v<double, true>(a, st) : cudaErrorInvalidValue;
+    case F32: return had ? launch_tr_v<float, true>(a, st) : cudaErrorInvalidValue;
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t st) {
+  g_launches = 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+  switch (a.dtype) {
+    case C128: k_argmax<double2><<<grid, 512, 0, st>>>((const double2*)a.h, a.n, a.batch, a.out); break;
+    case C64: k_argmax<float2><<<grid, 512, 0, st>>>((const float2*)a.h, a.n, a.batch, a.out); break;
+    case F64: k_argmax<double><<<grid, 512, 0, st>>>((const double*)a.h, a.n, a.batch, a.out); break;
+    case F32: k_argmax<float><<<grid, 512, 0, st>>>((const float*)a.h, a.n, a.batch, a.out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t st) {
+  const int64_t blocks = (op.n + 255) / 256;
+  k_kernel_finish<<<(unsigned)blocks, 256, 0, st>>>(op);
+  g_launches += 1;
+  if (op.g32) {
+    k_kernel_f32<<<(unsigned)blocks, 256, 0, st>>>(op);
+    g_launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_twiddles(const DevOp& op, cudaStream_t st) {
+  const int64_t blocks = (op.n + 255) / 256;
+  k_twiddles<<<(unsigned)blocks, 256, 0, st>>>(op);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace fmp
