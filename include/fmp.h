@@ -61,6 +61,9 @@ typedef struct fmp_ctx_s* fmp_ctx;
 typedef struct fmp_op_s* fmp_op;
 
 int fmp_version(void);
+/* calibrate the FMA pipe of the context's GPU: FMAs per second (fp64 when
+ * is_double, else fp32) — the roofline denominator of the accumulate path */
+int fmp_fma_peak(fmp_ctx ctx, int is_double, double* fma_per_s);
 const char* fmp_last_error(void);
 /* number of kernel launches the last call on this thread issued */
 int fmp_last_launch_count(void);

@@ -74,6 +74,7 @@ class OmpResult(C.Structure):
 
 
 _sig("fmp_version", C.c_int)
+_sig("fmp_fma_peak", C.c_int, _vp, C.c_int, C.POINTER(C.c_double))
 _sig("fmp_last_error", C.c_char_p)
 _sig("fmp_last_launch_count", C.c_int)
 _sig("fmp_ctx_create", C.c_int, C.c_int, C.POINTER(_vp))
@@ -171,6 +172,12 @@ class Context:
 
     def synchronize(self) -> None:
         _check(_lib.fmp_ctx_synchronize(self.handle))
+
+    def fma_peak(self, double: bool = True) -> float:
+        """Measured FMA-pipe throughput of this GPU (FMAs per second)."""
+        v = C.c_double(0)
+        _check(_lib.fmp_fma_peak(self.handle, int(double), C.byref(v)))
+        return v.value
 
     def close(self) -> None:
         if getattr(self, "handle", None):

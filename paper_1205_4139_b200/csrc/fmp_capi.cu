@@ -146,6 +146,14 @@ int copy_in(fmp_ctx_s* ctx, int slot, const void* host, size_t bytes, void** dev
 extern "C" {
 
 int fmp_version(void) { return 1; }
+
+int fmp_fma_peak(fmp_ctx ctx, int is_double, double* out) {
+  if (!ctx || !out) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CU(fmp::fma_peak(is_double, out));
+  return FMP_OK;
+}
 const char* fmp_last_error(void) { return g_err.c_str(); }
 int fmp_last_launch_count(void) { return g_launch_count; }
 

@@ -103,6 +103,8 @@ int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 int fast_update_grid(const DevOp& op, int dtype, int64_t batch);
 // largest n the smem-resident transform handles for this element size
 int64_t transform_max_n(int dtype);
+// FMA-pipe throughput (FMAs per second) measured by a calibration kernel
+cudaError_t fma_peak(int is_double, double* fma_per_s);
 // number of kernel launches issued by the last launch_* call on this thread
 int last_launch_count();
 

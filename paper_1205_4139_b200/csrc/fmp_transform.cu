@@ -269,3 +269,56 @@ cudaError_t launch_twiddles(const DevOp& op, cudaStream_t st) {
 }
 
 }  // namespace fmp
+
+// ------------------------------------------------ FMA-pipe calibration
+// Independent FMA chains (8 per thread) over a full-occupancy grid: the
+// roofline denominator for the accumulate path (measured on the box, since
+// MEASURED_PEAKS.json carries HBM and tensor peaks only).
+namespace {
+template <class T>
+__global__ void __launch_bounds__(256) k_fma_peak(T* out, int iters, T a, T b) {
+  T v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = (T)(threadIdx.x + j);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = v[j] * a + b;
+  }
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += v[j];
+  if (s == (T)-1.2345) out[threadIdx.x] = s;  // keep the chains live
+}
+}  // namespace
+
+namespace fmp {
+cudaError_t fma_peak(int is_double, double* fma_per_s) {
+  const int sms = num_sms();
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  void* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, 4096 * 8);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(a);
+    if (is_double)
+      k_fma_peak<double><<<blocks, threads>>>((double*)out, iters, 0.999999, 1e-7);
+    else
+      k_fma_peak<float><<<blocks, threads>>>((float*)out, iters, 0.9999f, 1e-4f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  *fma_per_s = (double)blocks * threads * iters * 8 / (best * 1e-3);
+  return e;
+}
+}  // namespace fmp
