@@ -135,39 +135,51 @@ __device__ __forceinline__ V mul_wconst(V v, int len, int j) {
   return cmul(v, w);
 }
 
-// R-point DFT in registers, input in bit-reversed order, output natural
-template <int R, bool INV, class V>
-__device__ __forceinline__ void dft_reg(V (&v)[R]) {
+// R-point DFT in registers, input in bit-reversed order, output natural.
+// Stages are template-recursive so every register index is a compile-time
+// constant (a runtime-indexed v[] would be placed in local memory).
+template <int R, bool INV, int LEN, class V>
+__device__ __forceinline__ void dft_stage(V (&v)[R]) {
+  if constexpr (LEN <= R) {
 #pragma unroll
-  for (int len = 2; len <= R; len <<= 1) {
+    for (int base = 0; base < R; base += LEN) {
 #pragma unroll
-    for (int base = 0; base < R; base += len) {
-#pragma unroll
-      for (int j = 0; j < len / 2; ++j) {
-        const V t = mul_wconst<INV>(v[base + j + len / 2], len, j);
+      for (int j = 0; j < LEN / 2; ++j) {
+        const V t = mul_wconst<INV>(v[base + j + LEN / 2], LEN, j);
         const V u = v[base + j];
         v[base + j] = add(u, t);
-        v[base + j + len / 2] = sub(u, t);
+        v[base + j + LEN / 2] = sub(u, t);
       }
     }
+    dft_stage<R, INV, LEN * 2>(v);
   }
 }
 
+template <int R, bool INV, class V>
+__device__ __forceinline__ void dft_reg(V (&v)[R]) {
+  dft_stage<R, INV, 2>(v);
+}
+
 // R-point Walsh-Hadamard in registers (natural order)
-template <int R, class V>
-__device__ __forceinline__ void wht_reg(V (&v)[R]) {
+template <int R, int HALF, class V>
+__device__ __forceinline__ void wht_stage(V (&v)[R]) {
+  if constexpr (HALF < R) {
 #pragma unroll
-  for (int half = 1; half < R; half <<= 1) {
+    for (int base = 0; base < R; base += 2 * HALF) {
 #pragma unroll
-    for (int base = 0; base < R; base += 2 * half) {
-#pragma unroll
-      for (int j = 0; j < half; ++j) {
-        const V a = v[base + j], b = v[base + j + half];
+      for (int j = 0; j < HALF; ++j) {
+        const V a = v[base + j], b = v[base + j + HALF];
         v[base + j] = add(a, b);
-        v[base + j + half] = sub(a, b);
+        v[base + j + HALF] = sub(a, b);
       }
     }
+    wht_stage<R, HALF * 2>(v);
   }
+}
+
+template <int R, class V>
+__device__ __forceinline__ void wht_reg(V (&v)[R]) {
+  wht_stage<R, 1>(v);
 }
 
 template <int LOGR>
@@ -188,12 +200,28 @@ __host__ __device__ constexpr int brev_small(int j) {
 template <int R> struct log2_of { static constexpr int v = R <= 1 ? 0 : 1 + log2_of<R / 2>::v; };
 template <> struct log2_of<1> { static constexpr int v = 0; };
 
+// Twiddle providers: tw(k) = exp(-2 pi i k / 2^log2tab) for k < 2^log2tab.
+template <class V>
+struct TwTable {  // full table (global memory, L1/L2 cached)
+  const V* __restrict__ p;
+  __device__ __forceinline__ V operator()(int k) const { return p[k]; }
+};
+template <class V>
+struct TwTwoLevel {  // W^k = lo[k mod 2^a] * hi[k >> a]; both tiny, in smem
+  const V* lo;
+  const V* hi;
+  int a;
+  __device__ __forceinline__ V operator()(int k) const {
+    return cmul(lo[k & ((1 << a) - 1)], hi[k >> a]);
+  }
+};
+
 // One radix-R sub-problem u of the pass over sub-blocks of span S = 2^logS
-// (see file comment).  Twiddles tw[k] = exp(-2 pi i k / 2^log2tab)
-// (conjugated when INV); the table may be longer than the vector.
-template <int R, int LOGP, bool INV, bool HAD, class V>
+// (see file comment); the twiddle table has 2^log2tab entries (it may be
+// longer than the vector).
+template <int R, int LOGP, bool INV, bool HAD, class V, class TW>
 __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2tab,
-                                         const V* __restrict__ tw, int u) {
+                                         const TW& tw, int u) {
   constexpr int LOGR = log2_of<R>::v;
   const int S = 1 << logS;
   const int o = u & (S - 1);
@@ -209,7 +237,7 @@ __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2ta
       const int step = o << (log2tab - logS - LOGR);
 #pragma unroll
       for (int j = 1; j < R; ++j) {
-        V w = tw[brev_small<R>(j) * step];
+        V w = tw(brev_small<R>(j) * step);
         if (INV) w.y = -w.y;
         v[j] = cmul(v[j], w);
       }
@@ -220,9 +248,8 @@ __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2ta
   for (int j = 0; j < R; ++j) buf[padx<LOGP>(base + j * S)] = v[j];
 }
 
-template <int R, int LOGP, bool INV, bool HAD, class V>
-__device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS,
-                                               const V* __restrict__ tw,
+template <int R, int LOGP, bool INV, bool HAD, class V, class TW>
+__device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS, const TW& tw,
                                                int tid, int nth) {
   constexpr int LOGR = log2_of<R>::v;
   const int nsub = 1 << (log2n - LOGR);
@@ -230,11 +257,11 @@ __device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS,
     pass_one<R, LOGP, INV, HAD>(buf, log2n, logS, log2n, tw, u);
 }
 
-// Whole in-place transform of one vector held by the calling block.
+// Whole in-place transform of one vector held by the calling block, radix
+// RMAX passes then one smaller remainder pass; padding period RMAX.
 // Ends with a __syncthreads().
-template <int RMAX, bool INV, bool HAD, class V>
-__device__ void block_transform(V* buf, int log2n, const V* __restrict__ tw,
-                                int tid, int nth) {
+template <int RMAX, bool INV, bool HAD, class V, class TW>
+__device__ void block_transform(V* buf, int log2n, const TW& tw, int tid, int nth) {
   constexpr int LOGP = log2_of<RMAX>::v;
   int s = 0;
   for (; log2n - s >= LOGP; s += LOGP) {
@@ -244,7 +271,10 @@ __device__ void block_transform(V* buf, int log2n, const V* __restrict__ tw,
   switch (log2n - s) {
     case 1: transform_pass<2, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
     case 2: transform_pass<4, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
-    case 3: transform_pass<8, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
+    case 3: if constexpr (RMAX > 8) {
+              transform_pass<8, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads();
+            }
+            break;
     default: break;
   }
 }
@@ -285,6 +315,23 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   double r = lane < nw ? red[lane] : 0.0;
   return warp_sum(r);
+}
+// three sums at once; `red` needs 96 doubles
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  __syncthreads();
+  if (lane == 0) {
+    red[w] = a;
+    red[32 + w] = b;
+    red[64 + w] = c;
+  }
+  __syncthreads();
+  a = warp_sum(lane < nw ? red[lane] : 0.0);
+  b = warp_sum(lane < nw ? red[32 + lane] : 0.0);
+  c = warp_sum(lane < nw ? red[64 + lane] : 0.0);
 }
 __device__ __forceinline__ unsigned block_min_u(unsigned v, unsigned* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;

@@ -81,30 +81,47 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
                                           const unsigned* lam, const V* xn, int t) {
   using T = typename scal<V>::T;
   const int mask = n - 1;
+  if (t <= 0) return;
+  // the atom list is read one step ahead so its smem latency overlaps the
+  // previous atom's kernel loads and FMAs
+  int l_nx = (int)lam[0];
+  V x_nx = xn[0];
   if constexpr (!HAD) {
-#pragma unroll 2
     for (int tau = 0; tau < t; ++tau) {
-      const int l = (int)lam[tau];
-      const V x = xn[tau];
+      const int l = l_nx;
+      const V x = x_nx;
+      if (tau + 1 < t) {
+        l_nx = (int)lam[tau + 1];
+        x_nx = xn[tau + 1];
+      }
       const int w0 = (i0 - l) & mask;
       if (w0 + 32 * RPT <= n) {
         const V* p = gF + w0 + lane;
+        V gv[RPT];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) msub(acc[r], x, p[32 * r]);
+        for (int r = 0; r < RPT; ++r) gv[r] = p[32 * r];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
       } else {
 #pragma unroll
         for (int r = 0; r < RPT; ++r) msub(acc[r], x, gF[(w0 + lane + 32 * r) & mask]);
       }
     }
   } else {
-#pragma unroll 2
     for (int tau = 0; tau < t; ++tau) {
-      const int l = (int)lam[tau];
-      const V x = xn[tau];
+      const int l = l_nx;
+      const V x = x_nx;
+      if (tau + 1 < t) {
+        l_nx = (int)lam[tau + 1];
+        x_nx = xn[tau + 1];
+      }
       const int base = (i0 ^ (l & ~(32 * RPT - 1))) + (lane ^ (l & 31));
       const int lr = (l >> 5) & (RPT - 1);
+      T gv[RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) msub(acc[r], x, (T)gH[base + 32 * (r ^ lr)]);
+      for (int r = 0; r < RPT; ++r) gv[r] = (T)gH[base + 32 * (r ^ lr)];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
     }
   }
 }

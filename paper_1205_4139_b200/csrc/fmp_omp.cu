@@ -1,9 +1,33 @@
 // Fused persistent OMP solver (solvers.cpp:296-411).
+//
+// One CTA owns one recovery problem at a time and pulls the next from a work
+// counter, so problems that halt early (config 4's noise tolerance) free their
+// SM at once.  Per problem, everything lives in shared memory:
+//
+//   buf  the transform buffer (n + n/8 slots); during fast iterations it holds
+//        h0 = Phi^H y, so the shifted-kernel accumulate reads only smem
+//   g    the correlation kernel c (Fourier: n complex; Hadamard: int16 lattice
+//        N*c), staged once per CTA and shared by every problem it solves
+//   W    the inverse Cholesky factor L^{-1} of the Gram matrix of the selected
+//        columns, column-major packed (global workspace when it does not fit)
+//   r    the residual (conventional iterations only)
+//
+// Iteration t (solvers.cpp:335-403): correlation h_t (t = 1 and conventional
+// rows: U^H scatter(r) by a radix-8 FFT/FWHT; fast rows: h0 - sum x g shifted),
+// band argmax (first index within 1e-9 of the max), stagnation stops, one Gram
+// row appended to W (entries are lookups c[(a-b) mod N] / c[a^b]), z = W b with
+// b = h0[Lambda], x = W^H z, then the residual: ||r||^2 = ||y||^2 - ||z||^2
+// while that identity is well away from the tolerance, else an explicit
+// r = y - Phi_Lambda x by one forward transform of the sparse estimate.
 #include "fmp_kcommon.cuh"
 
 namespace fmp {
 namespace {
-// -------------------------------------------------------------- OMP solver
+
+
+constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
+constexpr int OLOGP = 3;
+
 struct OmpK {
   DevOp op;
   const void* y;
@@ -11,7 +35,7 @@ struct OmpK {
   int64_t batch;
   int T;
   int64_t fast_until;
-  uint64_t* support;   // 1-based, batch x T
+  uint64_t* support;  // 1-based, batch x T
   double2* coeffs;
   uint64_t* size;
   uint64_t* iters;
@@ -26,33 +50,38 @@ struct OmpK {
   void* r_ws;
   int* queue;
   // shared-memory plan
-  int g_smem, r_smem, mag_in_buf;
-  int off_g, off_r, off_small;
+  int r_smem;
+  int off_g, off_r, off_w, off_tw, off_small;
+  int tw_a;       // two-level twiddle split
   double margin;  // relative slack on the residual identity
 };
 
-template <class V, bool HAD>
+template <bool HAD>
 __device__ __forceinline__ double2 gram(const DevOp& op, unsigned a, unsigned b) {
   // (Phi^H Phi)_{ab} = c[(a - b) mod N] (Fourier) or c[a XOR b] (Hadamard)
   if constexpr (HAD) return make_double2(op.gr64[a ^ b], 0.0);
   else return op.g64[(a - b) & (unsigned)(op.n - 1)];
 }
 
-template <class V, bool HAD, int RPT, bool GSM>
+// column-major packed lower triangle with capacity T: W(i, j), i >= j
+__device__ __forceinline__ int wofs(int T, int i, int j) {
+  return j * T - (j * (j - 1)) / 2 + (i - j);
+}
+
+template <class V, bool HAD, int RPT, bool GSM, bool WSM>
 __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ double red[32];
+  __shared__ double red[96];
   __shared__ unsigned redu[32];
   __shared__ int s_prob;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
             nw = nth >> 5;
-  const int nbuf = n + (n >> LOGP);
+  const int nbuf = n + (n >> OLOGP);
   const V zv = zero_of(V{});
-  const double sc = inv_sqrt_n(n);
+  const double sc = 1.0 / sqrt((double)n);
   const double xscale = HAD ? -1.0 / (double)n : -1.0;
-  const V* tw = twiddles<V>(op);
 
   V* buf = reinterpret_cast<V*>(sm);
   const V* gF = fourier_table<V>(op);
@@ -68,8 +97,21 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
       gH = s;
     }
   }
+  // two-level twiddles (Fourier): lo[k] = W^k, hi[k] = W^(k 2^a)
+  TwTwoLevel<V> tw{nullptr, nullptr, a.tw_a};
+  if constexpr (!HAD) {
+    V* lo = reinterpret_cast<V*>(sm + a.off_tw);
+    V* hi = lo + (1 << a.tw_a);
+    const V* full = twiddles<V>(op);
+    for (int k = tid; k < (1 << a.tw_a); k += nth) lo[k] = full[k];
+    for (int k = tid; k < (n >> a.tw_a); k += nth) hi[k] = full[k << a.tw_a];
+    tw.lo = lo;
+    tw.hi = hi;
+  }
   V* rs = a.r_smem ? reinterpret_cast<V*>(sm + a.off_r)
                    : reinterpret_cast<V*>(a.r_ws) + (size_t)blockIdx.x * m;
+  double2* W = WSM ? reinterpret_cast<double2*>(sm + a.off_w)
+                   : a.w_ws + (size_t)blockIdx.x * ((size_t)T * (T + 1) / 2);
   unsigned char* p = sm + a.off_small;
   double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   double2* s_z = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
@@ -78,11 +120,11 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)T + 15) / 16) * 16;
   unsigned* s_lam = reinterpret_cast<unsigned*>(p);
 
-  double2* W = a.w_ws + (size_t)blockIdx.x * ((size_t)T * (T + 1) / 2);
   V* h0w = reinterpret_cast<V*>(a.h0_ws) + (size_t)blockIdx.x * n;
-  double* msc = a.mag_in_buf ? reinterpret_cast<double*>(sm)
-                             : a.mag_ws + (size_t)blockIdx.x * n;
+  double* msc = a.mag_ws + (size_t)blockIdx.x * n;  // used only when a warp owns > 1 tile
   const double gamma = HAD ? op.gr64[0] : op.g64[0].x;  // c(1) = M/N
+  const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
+  const bool regs_only = ntiles > 0 && ntiles <= nw;  // every thread owns <= 1 tile
 
   for (;;) {
     __syncthreads();
@@ -100,8 +142,9 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
     double zz = 0.0;
     int s = 0, iters = 0, aborted = 0, tlast = 0;
     bool rn_explicit = true;
+    bool buf_h0 = false;  // buf currently holds h0 in padded layout
 
-    // explicit residual r = y - Phi_Lambda x via one forward transform of the
+    // explicit residual r = y - Phi_Lambda x by one forward transform of the
     // sparse estimate (replaces update_residual, solvers.cpp:180-192)
     auto residual_explicit = [&](int cnt) -> double {
       for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
@@ -109,16 +152,17 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
       for (int j = tid; j < cnt; j += nth) {
         V xv;
         from_c128(s_x[j], xv);
-        buf[in_slot<HAD>(s_lam[j], log2n)] = xv;
+        buf[padx<OLOGP>(HAD ? (int)s_lam[j] : (int)brev_n(s_lam[j], log2n))] = xv;
       }
       __syncthreads();
-      block_transform<RMAX, false, HAD>(buf, log2n, tw, tid, nth);
+      block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth);
       double r2 = 0.0;
       for (int j = tid; j < m; j += nth) {
-        const V rv = sub(y[j], scale(buf[padx<LOGP>((int)op.omega[j])], sc));
+        const V rv = sub(y[j], scale(buf[padx<OLOGP>((int)op.omega[j])], sc));
         rs[j] = rv;
         r2 += mag2(rv);
       }
+      buf_h0 = false;
       return sqrt(block_sum(r2, red));
     };
 
@@ -132,42 +176,56 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         V* hrow = a.hist ? reinterpret_cast<V*>(a.hist) + ((size_t)prob * T + (t - 1)) * n
                          : nullptr;
         double best = 0.0;
+        double m2[RPT];
         if (!fast_row) {
           // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
           const V* r = t == 1 ? y : rs;
           for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
           __syncthreads();
-          for (int j = tid; j < m; j += nth) buf[in_slot<HAD>(op.omega[j], log2n)] = r[j];
+          for (int j = tid; j < m; j += nth)
+            buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
           __syncthreads();
-          block_transform<RMAX, true, HAD>(buf, log2n, tw, tid, nth);
+          block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
+          for (int i = tid; i < nbuf; i += nth) buf[i] = scale(buf[i], sc);
+          __syncthreads();
           for (int k = tid; k < n; k += nth) {
-            const V v = scale(buf[padx<LOGP>(k)], sc);
+            const V v = buf[padx<OLOGP>(k)];
             if (t == 1) h0w[k] = v;
             if (hrow) hrow[k] = v;
             best = fmax(best, mag2(v));
           }
+          buf_h0 = t == 1;
         } else {
           // fast correlation (kernel.cpp:209-303) from h0 and the staged c
-          if (n >= 32 * RPT) {
-            const int ntiles = n / (32 * RPT);
+          if (!buf_h0) {
+            __syncthreads();
+            for (int k = tid; k < n; k += nth) buf[padx<OLOGP>(k)] = h0w[k];
+            buf_h0 = true;
+            __syncthreads();
+          }
+          if (ntiles) {
             for (int tile = warp; tile < ntiles; tile += nw) {
               const int i0 = tile * 32 * RPT;
               V acc[RPT];
 #pragma unroll
-              for (int r = 0; r < RPT; ++r) acc[r] = h0w[i0 + lane + 32 * r];
+              for (int r = 0; r < RPT; ++r) acc[r] = buf[padx<OLOGP>(i0 + lane + 32 * r)];
               fast_tile<V, HAD, RPT>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
                 const int i = i0 + lane + 32 * r;
-                const double mm = mag2(acc[r]);
-                msc[i] = mm;
-                best = fmax(best, mm);
+                m2[r] = mag2(acc[r]);
+                if (!regs_only) msc[i] = m2[r];
+                best = fmax(best, m2[r]);
                 if (hrow) hrow[i] = acc[r];
               }
             }
+            if (regs_only && warp >= ntiles) {
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) m2[r] = -1.0;
+            }
           } else {
             for (int i = tid; i < n; i += nth) {
-              V acc = h0w[i];
+              V acc = buf[padx<OLOGP>(i)];
               fast_point<V, HAD>(acc, i, n, gF, gH, s_lam, s_xn, s);
               const double mm = mag2(acc);
               msc[i] = mm;
@@ -183,7 +241,11 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         unsigned first = 0xffffffffu;
         if (!fast_row) {
           for (int k = tid; k < n; k += nth)
-            if (mag2(scale(buf[padx<LOGP>(k)], sc)) >= cut) { first = (unsigned)k; break; }
+            if (mag2(buf[padx<OLOGP>(k)]) >= cut) { first = (unsigned)k; break; }
+        } else if (regs_only) {
+#pragma unroll
+          for (int r = RPT - 1; r >= 0; --r)
+            if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
         } else {
           for (int k = tid; k < n; k += nth)
             if (msc[k] >= cut) { first = (unsigned)k; break; }
@@ -193,21 +255,18 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         for (int j = tid; j < s; j += nth) dup |= s_lam[j] == pick;
         if (__syncthreads_or(dup)) break;
 
-        // ---- least squares: append one Gram row to the inverse Cholesky
-        // factor W = L^{-1} (G = L L^H), z = W b, x = W^H z, b = h0[Lambda]
-        for (int j = tid; j < s; j += nth) s_a[j] = gram<V, HAD>(op, s_lam[j], pick);
+        // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H)
+        for (int j = tid; j < s; j += nth) s_a[j] = gram<HAD>(op, s_lam[j], pick);
         __syncthreads();
-        for (int i = warp; i < s; i += nw) {
-          const double2* Wi = W + (size_t)i * (i + 1) / 2;
+        // l = W a: thread i sums row i over the columns (contiguous per j)
+        for (int i = tid; i < s; i += nth) {
           double ar = 0.0, ai = 0.0;
-          for (int j = lane; j <= i; j += 32) {
-            const double2 w = Wi[j], v = s_a[j];
-            ar += w.x * v.x - w.y * v.y;
-            ai += w.x * v.y + w.y * v.x;
+          for (int j = 0; j <= i; ++j) {
+            const double2 w = W[wofs(T, i, j)], v = s_a[j];
+            ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
+            ai = fma(w.x, v.y, fma(w.y, v.x, ai));
           }
-          ar = warp_sum(ar);
-          ai = warp_sum(ai);
-          if (lane == 0) s_l[i] = make_double2(ar, ai);
+          s_l[i] = make_double2(ar, ai);
         }
         __syncthreads();
         double ll = 0.0, lzr = 0.0, lzi = 0.0;
@@ -217,43 +276,48 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           lzr += l.x * zc.x + l.y * zc.y;  // conj(l) z
           lzi += l.x * zc.y - l.y * zc.x;
         }
-        ll = block_sum(ll, red);
-        lzr = block_sum(lzr, red);
-        lzi = block_sum(lzi, red);
+        block_sum3(ll, lzr, lzi, red);
         const double d2 = gamma - ll;
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
         if (!(d2 > 1e-12 * gamma)) { aborted = 1; break; }
         const double d = sqrt(d2);
-        const double2 bnew = to_c128(h0w[pick]);
+        const double2 bnew = to_c128(buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
         const double2 znew = make_double2((bnew.x - lzr) / d, (bnew.y - lzi) / d);
-        double2* Wn = W + (size_t)s * (s + 1) / 2;
-        for (int j = tid; j < s; j += nth) {
+        // new row s of W: w_j = -(1/d) sum_{i=j}^{s-1} conj(l_i) W_ij; w_s = 1/d
+        for (int j = warp; j < s; j += nw) {
           double ar = 0.0, ai = 0.0;
-          for (int i = j; i < s; ++i) {
-            const double2 l = s_l[i], w = W[(size_t)i * (i + 1) / 2 + j];
-            ar += l.x * w.x + l.y * w.y;  // conj(l) w
+          for (int i = j + lane; i < s; i += 32) {
+            const double2 l = s_l[i], w = W[wofs(T, i, j)];
+            ar += l.x * w.x + l.y * w.y;
             ai += l.x * w.y - l.y * w.x;
           }
-          Wn[j] = make_double2(-ar / d, -ai / d);
+          ar = warp_sum(ar);
+          ai = warp_sum(ai);
+          if (lane == 0) W[wofs(T, s, j)] = make_double2(-ar / d, -ai / d);
         }
         if (tid == 0) {
-          Wn[s] = make_double2(1.0 / d, 0.0);
+          W[wofs(T, s, s)] = make_double2(1.0 / d, 0.0);
           s_z[s] = znew;
           s_lam[s] = pick;
         }
         zz += znew.x * znew.x + znew.y * znew.y;
         ++s;
         __syncthreads();
-        for (int j = tid; j < s; j += nth) {
+        // x = W^H z: x_j = sum_{i >= j} conj(W_ij) z_i, one warp per column
+        for (int j = warp; j < s; j += nw) {
           double ar = 0.0, ai = 0.0;
-          for (int i = j; i < s; ++i) {
-            const double2 w = W[(size_t)i * (i + 1) / 2 + j], zc = s_z[i];
-            ar += w.x * zc.x + w.y * zc.y;  // conj(w) z
+          for (int i = j + lane; i < s; i += 32) {
+            const double2 w = W[wofs(T, i, j)], zc = s_z[i];
+            ar += w.x * zc.x + w.y * zc.y;
             ai += w.x * zc.y - w.y * zc.x;
           }
-          s_x[j] = make_double2(ar, ai);
-          from_c128(make_double2(ar * xscale, ai * xscale), s_xn[j]);
+          ar = warp_sum(ar);
+          ai = warp_sum(ai);
+          if (lane == 0) {
+            s_x[j] = make_double2(ar, ai);
+            from_c128(make_double2(ar * xscale, ai * xscale), s_xn[j]);
+          }
         }
         __syncthreads();
         iters = t;
@@ -291,9 +355,9 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
 }
 
 struct OmpPlan {
-  size_t buf, g, r, small, total;
-  bool gsm, rsm, mag_in_buf;
-  int off_g, off_r, off_small;
+  size_t total;
+  bool gsm, rsm, wsm;
+  int off_g, off_r, off_w, off_tw, off_small, tw_a;
 };
 
 template <class V, bool HAD>
@@ -301,25 +365,36 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   OmpPlan p{};
   const int64_t n = op.n, m = op.m;
   auto al = [](size_t b) { return ((b + 15) / 16) * 16; };
-  p.buf = al((size_t)(n + (n >> LOGP)) * sizeof(V));
-  p.g = al(HAD ? (size_t)n * 2 : (size_t)n * sizeof(V));
-  p.r = al((size_t)m * sizeof(V));
-  p.small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T);
+  const size_t buf = al((size_t)(n + (n >> OLOGP)) * sizeof(V));
+  const size_t g = al(HAD ? (size_t)n * 2 : (size_t)n * sizeof(V));
+  const size_t r = al((size_t)m * sizeof(V));
+  const size_t w = al((size_t)T * (T + 1) / 2 * 16);
+  p.tw_a = (op.log2n + 1) / 2;
+  const size_t tw = HAD ? 0 : al(((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) * sizeof(V);
+  const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T);
   const size_t cap = (size_t)smem_optin() - 2048;
-  size_t tot = p.buf + p.small;
-  p.gsm = !(HAD && !op.glat) && tot + p.g <= cap;
-  if (p.gsm) tot += p.g;
-  p.rsm = tot + p.r <= cap;
-  if (p.rsm) tot += p.r;
+  size_t tot = buf + tw + small;
+  p.wsm = tot + w <= cap;  // W first: the least-squares phase is latency bound
+  if (p.wsm) tot += w;
+  p.gsm = !(HAD && !op.glat) && tot + g <= cap;
+  if (p.gsm) tot += g;
+  p.rsm = tot + r <= cap;
+  if (p.rsm) tot += r;
   p.total = tot;
-  p.mag_in_buf = sizeof(V) >= 8;
-  size_t off = p.buf;
-  p.off_g = (int)off;
-  if (p.gsm) off += p.g;
-  p.off_r = (int)off;
-  if (p.rsm) off += p.r;
+  size_t off = buf;
+  p.off_tw = (int)off; off += tw;
+  p.off_w = (int)off; if (p.wsm) off += w;
+  p.off_g = (int)off; if (p.gsm) off += g;
+  p.off_r = (int)off; if (p.rsm) off += r;
   p.off_small = (int)off;
   return p;
+}
+
+template <class V, bool HAD, int RPT, bool GSM, bool WSM>
+void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
+  auto f = k_omp<V, HAD, RPT, GSM, WSM>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  f<<<grid, OMP_THREADS, smem, st>>>(k);
 }
 
 template <class V, bool HAD, int RPT>
@@ -348,22 +423,21 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.mag_ws = a.mag_ws;
   k.r_ws = a.r_ws;
   k.queue = a.queue;
-  k.g_smem = p.gsm;
   k.r_smem = p.rsm;
-  k.mag_in_buf = p.mag_in_buf;
   k.off_g = p.off_g;
   k.off_r = p.off_r;
+  k.off_w = p.off_w;
+  k.off_tw = p.off_tw;
   k.off_small = p.off_small;
+  k.tw_a = p.tw_a;
   k.margin = is_double(a.dtype) ? 1e-10 : 1e-5;
   const int grid = std::max(1, a.grid);
   if (p.gsm) {
-    auto f = k_omp<V, HAD, RPT, true>;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.total);
-    f<<<grid, OMP_THREADS, p.total, st>>>(k);
+    if (p.wsm) launch_k<V, HAD, RPT, true, true>(k, grid, p.total, st);
+    else launch_k<V, HAD, RPT, true, false>(k, grid, p.total, st);
   } else {
-    auto f = k_omp<V, HAD, RPT, false>;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.total);
-    f<<<grid, OMP_THREADS, p.total, st>>>(k);
+    if (p.wsm) launch_k<V, HAD, RPT, false, true>(k, grid, p.total, st);
+    else launch_k<V, HAD, RPT, false, false>(k, grid, p.total, st);
   }
   ++g_launches;
   return cudaGetLastError();

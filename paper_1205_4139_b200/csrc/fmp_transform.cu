@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(512) k_transform(DevOp op, const V* __restrict
       for (int k = tid; k < n; k += nth) buf[in_slot<HAD>((unsigned)k, log2n)] = v[k];
     }
     __syncthreads();
-    block_transform<RMAX, INV, HAD>(buf, log2n, tw, tid, nth);
+    block_transform<RMAX, INV, HAD>(buf, log2n, TwTable<V>{tw}, tid, nth);
     if (out_omega) {
       V* o = out + b * m;
       for (int j = tid; j < m; j += nth) o[j] = scale(buf[padx<LOGP>((int)op.omega[j])], sc);
@@ -85,7 +85,8 @@ __global__ void k_gpass(V* data, int64_t batch, int log2n, int logS, const V* __
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = u >> (log2n - LOGR);
-    pass_one<R, 31, INV, HAD>(data + (b << log2n), log2n, logS, log2n, tw, (int)(u & (nsub - 1)));
+    pass_one<R, 31, INV, HAD>(data + (b << log2n), log2n, logS, log2n, TwTable<V>{tw},
+                              (int)(u & (nsub - 1)));
   }
 }
 
