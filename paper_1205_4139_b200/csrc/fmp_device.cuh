@@ -202,17 +202,22 @@ template <> struct log2_of<1> { static constexpr int v = 0; };
 
 // Twiddle providers: tw(k) = exp(-2 pi i k / 2^log2tab) for k < 2^log2tab.
 template <class V>
-struct TwTable {  // full table (global memory, L1/L2 cached)
+struct TwTable {  // full table (global memory, L1/L2 cached); direct lookups
+  static constexpr bool kPowers = false;
   const V* __restrict__ p;
   __device__ __forceinline__ V operator()(int k) const { return p[k]; }
 };
 template <class V>
 struct TwTwoLevel {  // W^k = lo[k mod 2^a] * hi[k >> a]; both tiny, in smem
-  const V* lo;
+  // a pass needs W^(rho step) for rho < R: one lookup, then products
+  // (at most 4 roundings deep), which keeps smem traffic to the data itself
+  static constexpr bool kPowers = true;
+  const V* lo;  // padded: entry i at i + i/8 (pass indices are strided by 8)
   const V* hi;
   int a;
+  __device__ __forceinline__ static int pad(int i) { return i + (i >> 3); }
   __device__ __forceinline__ V operator()(int k) const {
-    return cmul(lo[k & ((1 << a) - 1)], hi[k >> a]);
+    return cmul(lo[pad(k & ((1 << a) - 1))], hi[pad(k >> a)]);
   }
 };
 
@@ -235,11 +240,22 @@ __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2ta
     if (logS > 0) {
       // twiddle index brev(j) * o * 2^log2tab / (R S)
       const int step = o << (log2tab - logS - LOGR);
+      if constexpr (TW::kPowers) {
+        V w[R];
+        w[1] = tw(step);
+        if (INV) w[1].y = -w[1].y;
 #pragma unroll
-      for (int j = 1; j < R; ++j) {
-        V w = tw(brev_small<R>(j) * step);
-        if (INV) w.y = -w.y;
-        v[j] = cmul(v[j], w);
+        for (int q = 2; q < R; ++q)
+          w[q] = (q & 1) ? cmul(w[q - 1], w[1]) : cmul(w[q / 2], w[q / 2]);
+#pragma unroll
+        for (int j = 1; j < R; ++j) v[j] = cmul(v[j], w[brev_small<R>(j)]);
+      } else {
+#pragma unroll
+        for (int j = 1; j < R; ++j) {
+          V w = tw(brev_small<R>(j) * step);
+          if (INV) w.y = -w.y;
+          v[j] = cmul(v[j], w);
+        }
       }
     }
     dft_reg<R, INV>(v);

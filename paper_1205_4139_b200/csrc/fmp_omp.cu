@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   TwTwoLevel<V> tw{nullptr, nullptr, a.tw_a};
   if constexpr (!HAD) {
     V* lo = reinterpret_cast<V*>(sm + a.off_tw);
-    V* hi = lo + (1 << a.tw_a);
+    V* hi = lo + TwTwoLevel<V>::pad(1 << a.tw_a) + 1;
     const V* full = twiddles<V>(op);
-    for (int k = tid; k < (1 << a.tw_a); k += nth) lo[k] = full[k];
-    for (int k = tid; k < (n >> a.tw_a); k += nth) hi[k] = full[k << a.tw_a];
+    for (int k = tid; k < (1 << a.tw_a); k += nth) lo[TwTwoLevel<V>::pad(k)] = full[k];
+    for (int k = tid; k < (n >> a.tw_a); k += nth) hi[TwTwoLevel<V>::pad(k)] = full[k << a.tw_a];
     tw.lo = lo;
     tw.hi = hi;
   }
@@ -118,11 +118,19 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   double2* s_a = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   double2* s_l = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)T + 15) / 16) * 16;
-  unsigned* s_lam = reinterpret_cast<unsigned*>(p);
+  unsigned* s_lam = reinterpret_cast<unsigned*>(p); p += ((4 * (size_t)T + 15) / 16) * 16;
+  unsigned* s_sel = reinterpret_cast<unsigned*>(p);  // n bits: atoms selected so far
 
   V* h0w = reinterpret_cast<V*>(a.h0_ws) + (size_t)blockIdx.x * n;
   double* msc = a.mag_ws + (size_t)blockIdx.x * n;  // used only when a warp owns > 1 tile
   const double gamma = HAD ? op.gr64[0] : op.g64[0].x;  // c(1) = M/N
+  // Gram entry (Phi^H Phi)_{ab}: from the staged kernel when it is exact fp64
+  // (c128 table, or the Hadamard integer lattice), else the fp64 table
+  auto gram_of = [&](unsigned ga, unsigned gb) -> double2 {
+    if constexpr (GSM && HAD) return make_double2((double)gH[ga ^ gb] / (double)n, 0.0);
+    else if constexpr (GSM && sizeof(V) == 16) return to_c128(gF[(ga - gb) & (unsigned)(n - 1)]);
+    else return gram<HAD>(op, ga, gb);
+  };
   const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
   const bool regs_only = ntiles > 0 && ntiles <= nw;  // every thread owns <= 1 tile
 
@@ -135,6 +143,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
     const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
     const double tol = a.tol[prob];
 
+    for (int i = tid; i < (n + 31) / 32; i += nth) s_sel[i] = 0u;
     double yy = 0.0;
     for (int j = tid; j < m; j += nth) yy += mag2(y[j]);
     yy = block_sum(yy, red);
@@ -186,10 +195,14 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
             buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
           __syncthreads();
           block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
-          for (int i = tid; i < nbuf; i += nth) buf[i] = scale(buf[i], sc);
-          __syncthreads();
+          if (t == 1) {
+            // h0 = Phi^H y stays in buf (scaled, padded) for the fast rows
+            for (int i = tid; i < nbuf; i += nth) buf[i] = scale(buf[i], sc);
+            __syncthreads();
+          }
+          const double scv = t == 1 ? 1.0 : sc;
           for (int k = tid; k < n; k += nth) {
-            const V v = buf[padx<OLOGP>(k)];
+            const V v = scale(buf[padx<OLOGP>(k)], scv);
             if (t == 1) h0w[k] = v;
             if (hrow) hrow[k] = v;
             best = fmax(best, mag2(v));
@@ -240,8 +253,9 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         const double cut = best * (1.0 - kTieBandRel);
         unsigned first = 0xffffffffu;
         if (!fast_row) {
+          const double scv = t == 1 ? 1.0 : sc;
           for (int k = tid; k < n; k += nth)
-            if (mag2(buf[padx<OLOGP>(k)]) >= cut) { first = (unsigned)k; break; }
+            if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
         } else if (regs_only) {
 #pragma unroll
           for (int r = RPT - 1; r >= 0; --r)
@@ -251,24 +265,20 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
             if (msc[k] >= cut) { first = (unsigned)k; break; }
         }
         const unsigned pick = block_min_u(first, redu);
-        int dup = 0;
-        for (int j = tid; j < s; j += nth) dup |= s_lam[j] == pick;
-        if (__syncthreads_or(dup)) break;
+        // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
+        if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
 
-        // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H)
-        for (int j = tid; j < s; j += nth) s_a[j] = gram<HAD>(op, s_lam[j], pick);
-        __syncthreads();
-        // l = W a: thread i sums row i over the columns (contiguous per j)
+        // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H).
+        // l = W a with a_j = G(lambda_j, pick) looked up in c; thread i owns row i
         for (int i = tid; i < s; i += nth) {
           double ar = 0.0, ai = 0.0;
           for (int j = 0; j <= i; ++j) {
-            const double2 w = W[wofs(T, i, j)], v = s_a[j];
+            const double2 w = W[wofs(T, i, j)], v = gram_of(s_lam[j], pick);
             ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
             ai = fma(w.x, v.y, fma(w.y, v.x, ai));
           }
           s_l[i] = make_double2(ar, ai);
         }
-        __syncthreads();
         double ll = 0.0, lzr = 0.0, lzi = 0.0;
         for (int i = tid; i < s; i += nth) {
           const double2 l = s_l[i], zc = s_z[i];
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           lzr += l.x * zc.x + l.y * zc.y;  // conj(l) z
           lzi += l.x * zc.y - l.y * zc.x;
         }
-        block_sum3(ll, lzr, lzi, red);
+        block_sum3(ll, lzr, lzi, red);  // also publishes s_l
         const double d2 = gamma - ll;
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
@@ -284,41 +294,42 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         const double d = sqrt(d2);
         const double2 bnew = to_c128(buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
         const double2 znew = make_double2((bnew.x - lzr) / d, (bnew.y - lzi) / d);
-        // new row s of W: w_j = -(1/d) sum_{i=j}^{s-1} conj(l_i) W_ij; w_s = 1/d
+        // one pass per column j < s (a warp each) yields both the new row of W,
+        // W_sj = -(1/d) sum_{i=j}^{s-1} conj(l_i) W_ij, and the coefficient
+        // x_j = sum_{i=j}^{s-1} conj(W_ij) z_i + conj(W_sj) z_s   (x = W^H z)
         for (int j = warp; j < s; j += nw) {
-          double ar = 0.0, ai = 0.0;
+          double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
           for (int i = j + lane; i < s; i += 32) {
-            const double2 l = s_l[i], w = W[wofs(T, i, j)];
-            ar += l.x * w.x + l.y * w.y;
+            const double2 l = s_l[i], w = W[wofs(T, i, j)], zc = s_z[i];
+            ar += l.x * w.x + l.y * w.y;  // conj(l) w
             ai += l.x * w.y - l.y * w.x;
+            br += w.x * zc.x + w.y * zc.y;  // conj(w) z
+            bi += w.x * zc.y - w.y * zc.x;
           }
           ar = warp_sum(ar);
           ai = warp_sum(ai);
-          if (lane == 0) W[wofs(T, s, j)] = make_double2(-ar / d, -ai / d);
+          br = warp_sum(br);
+          bi = warp_sum(bi);
+          if (lane == 0) {
+            const double2 wn = make_double2(-ar / d, -ai / d);
+            W[wofs(T, s, j)] = wn;
+            const double xr = br + wn.x * znew.x + wn.y * znew.y;
+            const double xi = bi + wn.x * znew.y - wn.y * znew.x;
+            s_x[j] = make_double2(xr, xi);
+            from_c128(make_double2(xr * xscale, xi * xscale), s_xn[j]);
+          }
         }
         if (tid == 0) {
           W[wofs(T, s, s)] = make_double2(1.0 / d, 0.0);
           s_z[s] = znew;
           s_lam[s] = pick;
+          s_sel[pick >> 5] |= 1u << (pick & 31);
+          const double2 xs = make_double2(znew.x / d, znew.y / d);
+          s_x[s] = xs;
+          from_c128(make_double2(xs.x * xscale, xs.y * xscale), s_xn[s]);
         }
         zz += znew.x * znew.x + znew.y * znew.y;
         ++s;
-        __syncthreads();
-        // x = W^H z: x_j = sum_{i >= j} conj(W_ij) z_i, one warp per column
-        for (int j = warp; j < s; j += nw) {
-          double ar = 0.0, ai = 0.0;
-          for (int i = j + lane; i < s; i += 32) {
-            const double2 w = W[wofs(T, i, j)], zc = s_z[i];
-            ar += w.x * zc.x + w.y * zc.y;
-            ai += w.x * zc.y - w.y * zc.x;
-          }
-          ar = warp_sum(ar);
-          ai = warp_sum(ai);
-          if (lane == 0) {
-            s_x[j] = make_double2(ar, ai);
-            from_c128(make_double2(ar * xscale, ai * xscale), s_xn[j]);
-          }
-        }
         __syncthreads();
         iters = t;
 
@@ -370,8 +381,9 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   const size_t r = al((size_t)m * sizeof(V));
   const size_t w = al((size_t)T * (T + 1) / 2 * 16);
   p.tw_a = (op.log2n + 1) / 2;
-  const size_t tw = HAD ? 0 : al(((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) * sizeof(V);
-  const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T);
+  const size_t tw = HAD ? 0 : al(2 * (((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) + 4) * sizeof(V);
+  const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
+                       al(4 * (size_t)((n + 31) / 32));
   const size_t cap = (size_t)smem_optin() - 2048;
   size_t tot = buf + tw + small;
   p.wsm = tot + w <= cap;  // W first: the least-squares phase is latency bound
