@@ -241,10 +241,29 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   };
   std::vector<uint32_t> om(m);
   for (uint64_t i = 0; i < m; ++i) om[i] = (uint32_t)(r[i] - 1);
+  // transform slot of each row (bit-reversed for the Fourier DIT), sorted
+  std::vector<std::pair<uint32_t, uint32_t>> slots(m);
+  for (uint64_t i = 0; i < m; ++i) {
+    uint32_t p = om[i];
+    if (kind == FMP_FOURIER) {
+      uint32_t q = 0;
+      for (int b = 0; b < d.log2n; ++b) q |= ((p >> b) & 1u) << (d.log2n - 1 - b);
+      p = q;
+    }
+    slots[i] = {p, (uint32_t)i};
+  }
+  std::sort(slots.begin(), slots.end());
+  std::vector<uint32_t> spos(m), srow(m);
+  for (uint64_t i = 0; i < m; ++i) {
+    spos[i] = slots[i].first;
+    srow[i] = slots[i].second;
+  }
   cudaError_t e = cudaSuccess;
 #define OPALLOC(p, bytes) \
   if ((e = cudaMalloc(&p, (bytes))) != cudaSuccess) return cleanup(fail(FMP_ENOMEM, "operator alloc: %s", cudaGetErrorString(e)))
   OPALLOC(d.omega, m * 4);
+  OPALLOC(d.scat_pos, m * 4);
+  OPALLOC(d.scat_row, m * 4);
   OPALLOC(d.g64, n * 16);
   if (kind == FMP_FOURIER) {
     OPALLOC(d.tw64, n * 16);
@@ -257,7 +276,9 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
 #undef OPALLOC
   cudaStream_t st = ctx->cur;
   int launches = 0;
-  if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+  if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d.scat_pos, spos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d.scat_row, srow.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return cleanup(fail(FMP_ECUDA, "omega copy: %s", cudaGetErrorString(e)));
   if (kind == FMP_FOURIER) {
     if ((e = fmp::launch_twiddles(d, st)) != cudaSuccess)
@@ -290,7 +311,7 @@ int fmp_operator_destroy(fmp_op op) {
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->cur);
   DevOp& d = op->d;
-  for (void* p : {(void*)d.omega, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
+  for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
                   (void*)d.gr64, (void*)d.glat})
     if (p) cudaFree(p);
   delete op;

@@ -266,29 +266,33 @@ __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2ta
 
 template <int R, int LOGP, bool INV, bool HAD, class V, class TW>
 __device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS, const TW& tw,
-                                               int tid, int nth) {
+                                               int tid, int nth, int log2tab) {
   constexpr int LOGR = log2_of<R>::v;
   const int nsub = 1 << (log2n - LOGR);
   for (int u = tid; u < nsub; u += nth)
-    pass_one<R, LOGP, INV, HAD>(buf, log2n, logS, log2n, tw, u);
+    pass_one<R, LOGP, INV, HAD>(buf, log2n, logS, log2tab, tw, u);
 }
 
 // Whole in-place transform of one vector held by the calling block, radix
 // RMAX passes then one smaller remainder pass; padding period RMAX.
 // Ends with a __syncthreads().
+// log2tab: size of the twiddle table (defaults to the vector); a block that
+// runs the first stages of a longer transform passes the full length.
 template <int RMAX, bool INV, bool HAD, class V, class TW>
-__device__ void block_transform(V* buf, int log2n, const TW& tw, int tid, int nth) {
+__device__ void block_transform(V* buf, int log2n, const TW& tw, int tid, int nth,
+                                int log2tab = -1) {
   constexpr int LOGP = log2_of<RMAX>::v;
+  if (log2tab < 0) log2tab = log2n;
   int s = 0;
   for (; log2n - s >= LOGP; s += LOGP) {
-    transform_pass<RMAX, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth);
+    transform_pass<RMAX, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth, log2tab);
     __syncthreads();
   }
   switch (log2n - s) {
-    case 1: transform_pass<2, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
-    case 2: transform_pass<4, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads(); break;
+    case 1: transform_pass<2, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth, log2tab); __syncthreads(); break;
+    case 2: transform_pass<4, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth, log2tab); __syncthreads(); break;
     case 3: if constexpr (RMAX > 8) {
-              transform_pass<8, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth); __syncthreads();
+              transform_pass<8, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth, log2tab); __syncthreads();
             }
             break;
     default: break;

@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
             nw = nth >> 5;
   // staged kernel table, then the atom chunk (lambda, -x or -x/N)
   const V* gF = fourier_table<V>(op);
-  const int16_t* gH = op.glat;
+  const uint16_t* gH = op.glat;
   size_t goff = 0;
   if constexpr (GSM) {
     if constexpr (!HAD) {
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
       gF = s;
       goff = (size_t)n * sizeof(V);
     } else {
-      int16_t* s = reinterpret_cast<int16_t*>(smem_raw);
+      uint16_t* s = reinterpret_cast<uint16_t*>(smem_raw);
       const int* src = reinterpret_cast<const int*>(op.glat);
       int* dst = reinterpret_cast<int*>(s);
       for (int i = tid; i < n / 2; i += nth) dst[i] = src[i];

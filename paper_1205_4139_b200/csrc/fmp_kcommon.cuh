@@ -74,10 +74,20 @@ __device__ __forceinline__ int in_slot(unsigned p, int log2n) {
 // Fourier: source (i - lambda) mod n (kernel.cpp:247-255, map_index
 // kernel.cpp:111-118); Hadamard: i XOR lambda on the integer lattice N*c
 // (kernel.cpp:227-238), xn = -x/N so that xn * k == -x * c exactly.
+// Exact conversion of a biased lattice entry u = k + 32768 to k in T without
+// the (slow, XU-pipe) integer conversion: 2^52 + u (2^23 + u for float) is
+// assembled from its bit pattern and the bias subtracted, both exact.
+__device__ __forceinline__ void lat_to(unsigned u, double& o) {
+  o = __hiloint2double(0x43300000, (int)u) - 4503599627403264.0;  // 2^52 + 2^15
+}
+__device__ __forceinline__ void lat_to(unsigned u, float& o) {
+  o = __int_as_float(0x4B000000 | (int)u) - 8421376.0f;  // 2^23 + 2^15
+}
+
 template <class V, bool HAD, int RPT>
 __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n,
                                           const V* __restrict__ gF,
-                                          const int16_t* __restrict__ gH,
+                                          const uint16_t* __restrict__ gH,
                                           const unsigned* lam, const V* xn, int t) {
   using T = typename scal<V>::T;
   const int mask = n - 1;
@@ -119,7 +129,7 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
       const int lr = (l >> 5) & (RPT - 1);
       T gv[RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) gv[r] = (T)gH[base + 32 * (r ^ lr)];
+      for (int r = 0; r < RPT; ++r) lat_to((unsigned)gH[base + 32 * (r ^ lr)], gv[r]);
 #pragma unroll
       for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
     }
@@ -129,13 +139,17 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
 // single output (small n): h0 value in acc
 template <class V, bool HAD>
 __device__ __forceinline__ void fast_point(V& acc, int i, int n, const V* __restrict__ gF,
-                                           const int16_t* __restrict__ gH,
+                                           const uint16_t* __restrict__ gH,
                                            const unsigned* lam, const V* xn, int t) {
   using T = typename scal<V>::T;
   for (int tau = 0; tau < t; ++tau) {
     const int l = (int)lam[tau];
     if constexpr (!HAD) msub(acc, xn[tau], gF[(i - l) & (n - 1)]);
-    else msub(acc, xn[tau], (T)gH[i ^ l]);
+    else {
+      T gv;
+      lat_to((unsigned)gH[i ^ l], gv);
+      msub(acc, xn[tau], gv);
+    }
   }
 }
 

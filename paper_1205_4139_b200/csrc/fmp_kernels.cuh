@@ -27,7 +27,11 @@ struct DevOp {
   double2* g64 = nullptr;     // c, n entries, fp64 (Fourier: exact conj symmetry)
   float2* g32 = nullptr;      // c rounded to c64 (Fourier)
   double* gr64 = nullptr;     // c real part (Hadamard), exact k/N
-  int16_t* glat = nullptr;    // Hadamard lattice N*c (|N c| <= M); null if M > 32767
+  uint16_t* glat = nullptr;   // Hadamard lattice N*c + 32768 (|N c| <= M); null if M > 32767
+  // Omega scatter sorted by transform slot (slot = brev(row) Fourier, row
+  // Hadamard): the large-n transform's blocks find their rows by bisection
+  uint32_t* scat_pos = nullptr;  // m, ascending slots
+  uint32_t* scat_row = nullptr;  // m, index into the m-vector for each slot
 };
 
 struct TransformArgs {

@@ -85,14 +85,14 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
 
   V* buf = reinterpret_cast<V*>(sm);
   const V* gF = fourier_table<V>(op);
-  const int16_t* gH = op.glat;
+  const uint16_t* gH = op.glat;
   if constexpr (GSM) {
     if constexpr (!HAD) {
       V* s = reinterpret_cast<V*>(sm + a.off_g);
       for (int i = tid; i < n; i += nth) s[i] = gF[i];
       gF = s;
     } else {
-      int16_t* s = reinterpret_cast<int16_t*>(sm + a.off_g);
+      uint16_t* s = reinterpret_cast<uint16_t*>(sm + a.off_g);
       for (int i = tid; i < n; i += nth) s[i] = op.glat[i];
       gH = s;
     }
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   // Gram entry (Phi^H Phi)_{ab}: from the staged kernel when it is exact fp64
   // (c128 table, or the Hadamard integer lattice), else the fp64 table
   auto gram_of = [&](unsigned ga, unsigned gb) -> double2 {
-    if constexpr (GSM && HAD) return make_double2((double)gH[ga ^ gb] / (double)n, 0.0);
+    if constexpr (GSM && HAD) return make_double2((double)((int)gH[ga ^ gb] - 32768) / (double)n, 0.0);
     else if constexpr (GSM && sizeof(V) == 16) return to_c128(gF[(ga - gb) & (unsigned)(n - 1)]);
     else return gram<HAD>(op, ga, gb);
   };

@@ -92,11 +92,11 @@ __global__ void k_gpass(V* data, int64_t batch, int log2n, int logS, const V* __
 
 template <class V>
 __global__ void k_out(V* work, V* __restrict__ out, int64_t batch, int out_omega,
-                      const uint32_t* __restrict__ omega, int64_t m, int log2n) {
+                      const uint32_t* __restrict__ omega, int64_t m, int log2n, int scaled) {
   const int64_t n = 1ll << log2n;
   const int64_t len = out_omega ? m : n;
   const int64_t total = batch * len;
-  const double sc = 1.0 / sqrt((double)n);
+  const double sc = scaled ? 1.0 : 1.0 / sqrt((double)n);
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = u / len, j = u - b * len;
@@ -128,7 +128,7 @@ __global__ void k_kernel_finish(DevOp op) {
     const double k = round(op.g64[i].x * (double)n);
     op.g64[i] = make_double2(k / (double)n, 0.0);
     op.gr64[i] = k / (double)n;
-    if (op.glat) op.glat[i] = (int16_t)k;
+    if (op.glat) op.glat[i] = (uint16_t)((int)k + 32768);
   }
 }
 
@@ -165,6 +165,157 @@ cudaError_t launch_tr_t(const TransformArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------ cluster transform path
+// n beyond one CTA: a thread-block cluster of K CTAs owns one vector.
+// Phase A: CTA c runs the first log2(n/K) stages on its contiguous block in
+// shared memory (these stages never leave the block) and writes it back.
+// A cluster barrier (release/acquire) hands the L2-resident intermediate over.
+// Phase B: the last log2(K) stages are a radix-K pass of span n/K; CTA c owns
+// 1/K of the offsets and finishes them in registers, in place.  HBM traffic
+// is the input plus one output write (the intermediate stays in L2).
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <class V, bool INV, bool HAD, int K>
+__global__ void __launch_bounds__(256) k_transform_cluster(DevOp op, const V* __restrict__ in,
+                                                           V* dst, int64_t batch, int in_omega) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* buf = reinterpret_cast<V*>(smem_raw);
+  constexpr int LOGK = log2_of<K>::v;
+  const int log2n = op.log2n, n = (int)op.n, m = (int)op.m;
+  const int log2b = log2n - LOGK, B = 1 << log2b;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const unsigned c = cluster_rank();
+  const int64_t cid = blockIdx.x / K, ncl = gridDim.x / K;
+  const V* tw = twiddles<V>(op);
+  const double sc = 1.0 / sqrt((double)n);
+  const V z = zero_of(V{});
+  const int lo_slot = (int)c * B;
+  // this block's Omega rows: bisection in the slot-sorted scatter
+  int k0 = 0, k1 = 0;
+  if (in_omega) {
+    int lo = 0, hi = m;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)op.scat_pos[mid] < lo_slot) lo = mid + 1; else hi = mid; }
+    k0 = lo;
+    hi = m;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)op.scat_pos[mid] < lo_slot + B) lo = mid + 1; else hi = mid; }
+    k1 = lo;
+  }
+  for (int64_t b = cid; b < batch; b += ncl) {
+    V* vec = dst + b * n;
+    // ---- phase A
+    if (in_omega) {
+      for (int i = tid; i < B + (B >> LOGP); i += nth) buf[i] = z;
+      __syncthreads();
+      const V* r = in + b * m;
+      for (int k = k0 + tid; k < k1; k += nth)
+        buf[padx<LOGP>((int)op.scat_pos[k] - lo_slot)] = r[op.scat_row[k]];
+    } else {
+      const V* v = in + b * n;
+      for (int i = tid; i < B; i += nth) {
+        const unsigned p = (unsigned)(lo_slot + i);
+        buf[padx<LOGP>(i)] = v[HAD ? p : brev_n(p, log2n)];
+      }
+    }
+    __syncthreads();
+    block_transform<RMAX, INV, HAD>(buf, log2b, TwTable<V>{tw}, tid, nth, log2n);
+    for (int i = tid; i < B; i += nth) vec[lo_slot + i] = buf[padx<LOGP>(i)];
+    cluster_sync_all();
+    // ---- phase B: offsets o in [c B/K, (c+1) B/K), elements o + j B
+    const int o0 = (int)c * (B / K);
+    for (int o = o0 + tid; o < o0 + B / K; o += nth) {
+      V v[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) v[j] = __ldcg(vec + o + j * B);
+      if constexpr (HAD) {
+        wht_reg<K>(v);
+      } else {
+#pragma unroll
+        for (int j = 1; j < K; ++j) {
+          V w = tw[brev_small<K>(j) * o];
+          if (INV) w.y = -w.y;
+          v[j] = cmul(v[j], w);
+        }
+        dft_reg<K, INV>(v);
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) __stcg(vec + o + j * B, scale(v[j], sc));
+    }
+    __syncthreads();
+  }
+}
+
+template <class V, bool INV, bool HAD, int K>
+cudaError_t launch_tr_cluster_k(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  const int64_t B = op.n / K;
+  const size_t smem = (size_t)(B + (B >> LOGP)) * sizeof(V);
+  auto kern = k_transform_cluster<V, INV, HAD, K>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (K > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  V* dst = a.out_omega ? (V*)a.work : (V*)a.out;
+  if (!dst) dst = (V*)a.work;
+  if (!dst) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  cfg.gridDim = dim3(K);
+  cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+  if (ncl <= 0) ncl = std::max(1, num_sms() / K);
+  ncl = (int)std::min<int64_t>(ncl, a.batch);
+  cfg.gridDim = dim3(ncl * K);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, op, (const V*)a.in, dst, a.batch, a.in_omega);
+  if (e != cudaSuccess) return e;
+  ++g_launches;
+  const int grid = num_sms() * 8;
+  if (a.out_omega) {
+    k_out<V><<<grid, 256, 0, st>>>(dst, (V*)a.out, a.batch, 1, op.omega, op.m, op.log2n, 1);
+    ++g_launches;
+  }
+  if (a.argmax_out && !a.out_omega) {
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+    k_argmax<V><<<g2, 512, 0, st>>>(dst, op.n, a.batch, a.argmax_out);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+// cluster size for a vector of n elements: blocks of at most 32 KB, so that
+// several clusters are resident per SM group and hide each other's barriers
+template <class V>
+int cluster_k(int64_t n, int dtype) {
+  int64_t k = 2;
+  while (k <= 16 && (n / k) * (int64_t)sizeof(V) > 64 * 1024) k *= 2;
+  if (k > 16 || n / k > transform_max_n(dtype)) return 0;
+  return (int)k;
+}
+
+template <class V, bool INV, bool HAD>
+cudaError_t launch_tr_cluster(const TransformArgs& a, cudaStream_t st, int k) {
+  switch (k) {
+    case 2: return launch_tr_cluster_k<V, INV, HAD, 2>(a, st);
+    case 4: return launch_tr_cluster_k<V, INV, HAD, 4>(a, st);
+    case 8: return launch_tr_cluster_k<V, INV, HAD, 8>(a, st);
+    case 16: return launch_tr_cluster_k<V, INV, HAD, 16>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <class V, bool INV, bool HAD>
 cudaError_t launch_tr_global(const TransformArgs& a, cudaStream_t st) {
   const DevOp& op = *a.op;
@@ -196,7 +347,7 @@ cudaError_t launch_tr_global(const TransformArgs& a, cudaStream_t st) {
   }
   V* out = (V*)a.out;
   k_out<V><<<grid, 256, 0, st>>>(work, (a.out_omega || out) ? out : nullptr, a.batch,
-                                 a.out_omega, op.omega, op.m, log2n);
+                                 a.out_omega, op.omega, op.m, log2n, 0);
   ++g_launches;
   if (a.argmax_out && !a.out_omega) {
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
@@ -208,8 +359,13 @@ cudaError_t launch_tr_global(const TransformArgs& a, cudaStream_t st) {
 
 template <class V, bool HAD>
 cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
-  if (a.op->n > transform_max_n(a.dtype))
+  if (a.op->n > transform_max_n(a.dtype)) {
+    const int k = a.op->scat_pos ? cluster_k<V>(a.op->n, a.dtype) : 0;
+    if (k)
+      return a.inverse ? launch_tr_cluster<V, true, HAD>(a, st, k)
+                       : launch_tr_cluster<V, false, HAD>(a, st, k);
     return a.inverse ? launch_tr_global<V, true, HAD>(a, st) : launch_tr_global<V, false, HAD>(a, st);
+  }
   return a.inverse ? launch_tr_t<V, true, HAD>(a, st) : launch_tr_t<V, false, HAD>(a, st);
 }
 
