@@ -54,7 +54,8 @@ enum fmp_mode {
   FMP_MODE_CONVENTIONAL = 0,
   FMP_MODE_FAST = 1,
   FMP_MODE_ADAPTIVE = 2,
-  FMP_MODE_CUSTOM = 3
+  FMP_MODE_CUSTOM = 3,
+  FMP_MODE_GPU = 4     /* Adaptive with the B200-calibrated switch point */
 };
 
 typedef struct fmp_ctx_s* fmp_ctx;
@@ -93,6 +94,9 @@ int fmp_operator_kernel(fmp_op op, double* c_out, double* values_out,
                         uint32_t* value_index_out, uint64_t* nvalues);
 /* crossover_iteration (cost_model.hpp:76): the Adaptive switch point */
 uint64_t fmp_crossover_iteration(int kind, uint64_t n);
+/* the same switch point measured for this GPU path (FMP_MODE_GPU): fast
+ * updates while t <= this, transforms afterwards */
+uint64_t fmp_gpu_crossover(int kind, uint64_t n);
 
 /* ------------------------------------------------------ transforms (batched) */
 /* SensingOperator::apply, Phi x (sensing.cpp:93-100): x batch x n -> y batch x m */

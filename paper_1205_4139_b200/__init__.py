@@ -48,7 +48,7 @@ C128, C64, F64, F32 = 0, 1, 2, 3
 DTYPES = {np.dtype(np.complex128): C128, np.dtype(np.complex64): C64,
           np.dtype(np.float64): F64, np.dtype(np.float32): F32}
 NP_OF = {C128: np.complex128, C64: np.complex64, F64: np.float64, F32: np.float32}
-MODES = {"conventional": 0, "fast": 1, "adaptive": 2, "custom": 3}
+MODES = {"conventional": 0, "fast": 1, "adaptive": 2, "custom": 3, "gpu": 4}
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
@@ -87,6 +87,7 @@ _sig("fmp_operator_destroy", C.c_int, _vp)
 _sig("fmp_operator_info", C.c_int, _vp, C.POINTER(C.c_int), C.POINTER(_u64), C.POINTER(_u64))
 _sig("fmp_operator_kernel", C.c_int, _vp, _vp, _vp, _vp, C.POINTER(_u64))
 _sig("fmp_crossover_iteration", _u64, C.c_int, _u64)
+_sig("fmp_gpu_crossover", _u64, C.c_int, _u64)
 _sig("fmp_apply", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
 _sig("fmp_apply_dev", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
 _sig("fmp_apply_adjoint", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
@@ -204,6 +205,12 @@ def default_context(device: int = 0) -> Context:
 def crossover_iteration(kind, n: int) -> int:
     kind = KINDS.get(kind, kind)
     return int(_lib.fmp_crossover_iteration(kind, n))
+
+
+def gpu_crossover(kind, n: int) -> int:
+    """Switch point of the GPU-calibrated Adaptive mode ("gpu")."""
+    kind = KINDS.get(kind, kind)
+    return int(_lib.fmp_gpu_crossover(kind, n))
 
 
 def make_row_selection(n: int, m: int, seed: int) -> np.ndarray:
@@ -543,6 +550,6 @@ def apply_adjoint_dev(op: SensingOperator, r, h_out=None, argmax_out=None,
 __all__ = [
     "Context", "SensingOperator", "CorrelationKernel", "compute_kernel", "fast_update",
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
-    "omp_solve_batch", "crossover_iteration", "make_row_selection", "make_batch", "derive_seed",
+    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
 ]

@@ -22,8 +22,8 @@ LIB = os.path.join(PKG, "libfmp_cuda.so")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["fmp_omp.cu", "fmp_fast_update.cu", "fmp_transform.cu", "fmp_capi.cu", "fmp_host_gen.cpp"]
-HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh"]
+SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_fast_update.cu", "fmp_transform.cu", "fmp_capi.cu", "fmp_host_gen.cpp"]
+HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh"]
 
 
 def _newest_dep() -> float:
@@ -47,7 +47,7 @@ def _compile(src: str, force: bool) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
+    with cf.ThreadPoolExecutor(min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]

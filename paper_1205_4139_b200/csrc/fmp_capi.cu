@@ -72,7 +72,7 @@ struct Workspace {
 };
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
-            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX };
+            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF };
 
 }  // namespace
 
@@ -162,6 +162,15 @@ uint64_t fmp_crossover_iteration(int kind, uint64_t n) {
   if (!pow2(n)) return 0;
   const uint64_t logn = (uint64_t)ilog2(n);
   return kind == FMP_FOURIER ? (5 * logn) / 6 + 1 : logn + 1;
+}
+
+uint64_t fmp_gpu_crossover(int kind, uint64_t n) {
+  // measured on B200 (bench.py --mode custom:T sweeps): the
+  // fused kernel's transform iteration costs about as much as 8 log2(N) / 3
+  // fast-update atoms for Fourier; the Hadamard FWHT needs no twiddles
+  if (!pow2(n)) return 0;
+  const uint64_t logn = (uint64_t)ilog2(n);
+  return kind == FMP_FOURIER ? (8 * logn) / 3 : 2 * logn;
 }
 
 int fmp_ctx_create(int device, fmp_ctx* out) {
@@ -533,7 +542,7 @@ static int omp_validate(fmp_op op, int dtype, const fmp_omp_config* cfg) {
   if (cfg->max_iterations < 1) return fail(FMP_EINVAL, "omp_solve: max_iterations must be >= 1");
   if (!cfg->tolerances && !(cfg->tolerance >= 0.0))
     return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
-  if (cfg->mode < 0 || cfg->mode > 3) return fail(FMP_EINVAL, "unknown correlation mode");
+  if (cfg->mode < 0 || cfg->mode > 4) return fail(FMP_EINVAL, "unknown correlation mode");
   if (cfg->max_iterations > 4096) return fail(FMP_EUNSUPPORTED, "max_iterations > 4096");
   if (op->d.kind == fmp::HADAMARD && !op->d.glat)
     return fail(FMP_EUNSUPPORTED, "hadamard solve needs m <= 32767 (int16 lattice)");
@@ -545,6 +554,7 @@ static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg) {
     case FMP_MODE_CONVENTIONAL: return 0;
     case FMP_MODE_FAST: return std::numeric_limits<int64_t>::max();
     case FMP_MODE_ADAPTIVE: return (int64_t)fmp_crossover_iteration(op->d.kind, (uint64_t)op->d.n);
+    case FMP_MODE_GPU: return (int64_t)fmp_gpu_crossover(op->d.kind, (uint64_t)op->d.n);
     default: return (int64_t)std::min<uint64_t>(cfg->fast_until, (uint64_t)INT64_MAX);
   }
 }
@@ -586,6 +596,11 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   void* r;
   ALLOC(r, S_R, (size_t)a.grid * m * eb);
   a.r_ws = r;
+  if (n > fmp::transform_max_n(dtype) / 2) {
+    void* bw;
+    ALLOC(bw, S_BUF, (size_t)a.grid * (n + n / 8) * eb);
+    a.buf_ws = bw;
+  }
   int* q;
   ALLOC(q, S_Q, 64);
   a.queue = q;

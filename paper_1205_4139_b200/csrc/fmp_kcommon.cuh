@@ -84,7 +84,26 @@ __device__ __forceinline__ void lat_to(unsigned u, float& o) {
   o = __int_as_float(0x4B000000 | (int)u) - 8421376.0f;  // 2^23 + 2^15
 }
 
-template <class V, bool HAD, int RPT>
+// acc -= x * conj(g) with xn = -x
+__device__ __forceinline__ void msub_conj(double2& acc, double2 xn, double2 g) {
+  acc.x = fma(xn.x, g.x, acc.x);
+  acc.x = fma(xn.y, g.y, acc.x);
+  acc.y = fma(xn.y, g.x, acc.y);
+  acc.y = fma(-xn.x, g.y, acc.y);
+}
+__device__ __forceinline__ void msub_conj(float2& acc, float2 xn, float2 g) {
+  acc.x = fmaf(xn.x, g.x, acc.x);
+  acc.x = fmaf(xn.y, g.y, acc.x);
+  acc.y = fmaf(xn.y, g.x, acc.y);
+  acc.y = fmaf(-xn.x, g.y, acc.y);
+}
+template <class V>
+__device__ __forceinline__ void msub_conj(V&, V, V) {}
+
+// HALFG: the Fourier kernel is stored as its conjugate-symmetric half,
+// c[0..n/2] (c[n-j] = conj(c[j]), kernel.cpp:35-45); windows that stay on one
+// side of n/2 read it forwards (lower) or mirrored and conjugated (upper).
+template <class V, bool HAD, int RPT, bool HALFG = false>
 __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n,
                                           const V* __restrict__ gF,
                                           const uint16_t* __restrict__ gH,
@@ -105,16 +124,42 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
         x_nx = xn[tau + 1];
       }
       const int w0 = (i0 - l) & mask;
-      if (w0 + 32 * RPT <= n) {
-        const V* p = gF + w0 + lane;
-        V gv[RPT];
+      if constexpr (!HALFG) {
+        if (w0 + 32 * RPT <= n) {
+          const V* p = gF + w0 + lane;
+          V gv[RPT];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) gv[r] = p[32 * r];
+          for (int r = 0; r < RPT; ++r) gv[r] = p[32 * r];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
+          for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) msub(acc[r], x, gF[(w0 + lane + 32 * r) & mask]);
+        }
       } else {
+        const int half = n >> 1;
+        if (w0 + 32 * RPT <= half + 1) {
+          const V* p = gF + w0 + lane;
+          V gv[RPT];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) msub(acc[r], x, gF[(w0 + lane + 32 * r) & mask]);
+          for (int r = 0; r < RPT; ++r) gv[r] = p[32 * r];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
+        } else if (w0 > half && w0 + 32 * RPT <= n) {
+          const V* p = gF + (n - w0 - lane);
+          V gv[RPT];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) gv[r] = p[-32 * r];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) msub_conj(acc[r], x, gv[r]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int j = (w0 + lane + 32 * r) & mask;
+            if (j <= half) msub(acc[r], x, gF[j]);
+            else msub_conj(acc[r], x, gF[n - j]);
+          }
+        }
       }
     }
   } else {
@@ -137,14 +182,18 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
 }
 
 // single output (small n): h0 value in acc
-template <class V, bool HAD>
+template <class V, bool HAD, bool HALFG = false>
 __device__ __forceinline__ void fast_point(V& acc, int i, int n, const V* __restrict__ gF,
                                            const uint16_t* __restrict__ gH,
                                            const unsigned* lam, const V* xn, int t) {
   using T = typename scal<V>::T;
   for (int tau = 0; tau < t; ++tau) {
     const int l = (int)lam[tau];
-    if constexpr (!HAD) msub(acc, xn[tau], gF[(i - l) & (n - 1)]);
+    if constexpr (!HAD) {
+      const int j = (i - l) & (n - 1);
+      if (!HALFG || j <= (n >> 1)) msub(acc, xn[tau], gF[j]);
+      else msub_conj(acc, xn[tau], gF[n - j]);
+    }
     else {
       T gv;
       lat_to((unsigned)gH[i ^ l], gv);

@@ -1,0 +1,8 @@
+// Fused OMP solver instantiations for c128 data.
+#include "fmp_omp_impl.cuh"
+
+namespace fmp {
+cudaError_t launch_omp_c128(const OmpArgs& a, cudaStream_t st) {
+  return a.op->kind == HADAMARD ? launch_omp_v<double2, true>(a, st) : launch_omp_v<double2, false>(a, st);
+}
+}  // namespace fmp

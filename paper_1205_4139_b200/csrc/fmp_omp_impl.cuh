@@ -1,0 +1,493 @@
+// Fused persistent OMP solver (solvers.cpp:296-411).
+//
+// One CTA owns one recovery problem at a time and pulls the next from a work
+// counter, so problems that halt early (config 4's noise tolerance) free their
+// SM at once.  Per problem, everything lives in shared memory:
+//
+//   buf  the transform buffer (n + n/8 slots); during fast iterations it holds
+//        h0 = Phi^H y, so the shifted-kernel accumulate reads only smem
+//   g    the correlation kernel c (Fourier: n complex; Hadamard: int16 lattice
+//        N*c), staged once per CTA and shared by every problem it solves
+//   W    the inverse Cholesky factor L^{-1} of the Gram matrix of the selected
+//        columns, column-major packed (global workspace when it does not fit)
+//   r    the residual (conventional iterations only)
+//
+// Iteration t (solvers.cpp:335-403): correlation h_t (t = 1 and conventional
+// rows: U^H scatter(r) by a radix-8 FFT/FWHT; fast rows: h0 - sum x g shifted),
+// band argmax (first index within 1e-9 of the max), stagnation stops, one Gram
+// row appended to W (entries are lookups c[(a-b) mod N] / c[a^b]), z = W b with
+// b = h0[Lambda], x = W^H z, then the residual: ||r||^2 = ||y||^2 - ||z||^2
+// while that identity is well away from the tolerance, else an explicit
+// r = y - Phi_Lambda x by one forward transform of the sparse estimate.
+#pragma once
+#include "fmp_kcommon.cuh"
+
+namespace fmp {
+namespace {
+
+
+constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
+constexpr int OLOGP = 3;
+
+struct OmpK {
+  DevOp op;
+  const void* y;
+  const double* tol;
+  int64_t batch;
+  int T;
+  int64_t fast_until;
+  uint64_t* support;  // 1-based, batch x T
+  double2* coeffs;
+  uint64_t* size;
+  uint64_t* iters;
+  uint64_t* hlen;
+  double* resid;
+  int32_t* aborted;
+  uint8_t* modes;
+  void* hist;
+  double2* w_ws;
+  void* h0_ws;
+  double* mag_ws;
+  void* r_ws;
+  int* queue;
+  // shared-memory plan
+  void* buf_ws;  // grid x (n + n/8) when the buffer lives in global memory
+  int r_smem, w_smem;
+  int off_g, off_r, off_w, off_tw, off_small;
+  int tw_a;       // two-level twiddle split
+  double margin;  // relative slack on the residual identity
+};
+
+template <bool HAD>
+__device__ __forceinline__ double2 gram(const DevOp& op, unsigned a, unsigned b) {
+  // (Phi^H Phi)_{ab} = c[(a - b) mod N] (Fourier) or c[a XOR b] (Hadamard)
+  if constexpr (HAD) return make_double2(op.gr64[a ^ b], 0.0);
+  else return op.g64[(a - b) & (unsigned)(op.n - 1)];
+}
+
+// column-major packed lower triangle with capacity T: W(i, j), i >= j
+__device__ __forceinline__ int wofs(int T, int i, int j) {
+  return j * T - (j * (j - 1)) / 2 + (i - j);
+}
+
+// GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
+// Fourier only); BUFG: transform buffer in global memory (n beyond smem)
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
+__global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ double red[96];
+  __shared__ unsigned redu[32];
+  __shared__ int s_prob;
+  const DevOp& op = a.op;
+  const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
+            nw = nth >> 5;
+  const int nbuf = n + (n >> OLOGP);
+  const V zv = zero_of(V{});
+  const double sc = 1.0 / sqrt((double)n);
+  const double xscale = HAD ? -1.0 / (double)n : -1.0;
+
+  V* buf = BUFG ? reinterpret_cast<V*>(a.buf_ws) + (size_t)blockIdx.x * nbuf
+                : reinterpret_cast<V*>(sm);
+  const V* gF = fourier_table<V>(op);
+  const uint16_t* gH = op.glat;
+  if constexpr (GMODE > 0) {
+    if constexpr (!HAD) {
+      V* s = reinterpret_cast<V*>(sm + a.off_g);
+      const int cnt = GMODE == 2 ? n / 2 + 1 : n;
+      for (int i = tid; i < cnt; i += nth) s[i] = gF[i];
+      gF = s;
+    } else {
+      uint16_t* s = reinterpret_cast<uint16_t*>(sm + a.off_g);
+      for (int i = tid; i < n; i += nth) s[i] = op.glat[i];
+      gH = s;
+    }
+  }
+  // two-level twiddles (Fourier): lo[k] = W^k, hi[k] = W^(k 2^a)
+  TwTwoLevel<V> tw{nullptr, nullptr, a.tw_a};
+  if constexpr (!HAD) {
+    V* lo = reinterpret_cast<V*>(sm + a.off_tw);
+    V* hi = lo + TwTwoLevel<V>::pad(1 << a.tw_a) + 1;
+    const V* full = twiddles<V>(op);
+    for (int k = tid; k < (1 << a.tw_a); k += nth) lo[TwTwoLevel<V>::pad(k)] = full[k];
+    for (int k = tid; k < (n >> a.tw_a); k += nth) hi[TwTwoLevel<V>::pad(k)] = full[k << a.tw_a];
+    tw.lo = lo;
+    tw.hi = hi;
+  }
+  V* rs = a.r_smem ? reinterpret_cast<V*>(sm + a.off_r)
+                   : reinterpret_cast<V*>(a.r_ws) + (size_t)blockIdx.x * m;
+  double2* W = a.w_smem ? reinterpret_cast<double2*>(sm + a.off_w)
+                       : a.w_ws + (size_t)blockIdx.x * ((size_t)T * (T + 1) / 2);
+  unsigned char* p = sm + a.off_small;
+  double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
+  double2* s_z = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
+  double2* s_a = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
+  double2* s_l = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
+  V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)T + 15) / 16) * 16;
+  unsigned* s_lam = reinterpret_cast<unsigned*>(p); p += ((4 * (size_t)T + 15) / 16) * 16;
+  unsigned* s_sel = reinterpret_cast<unsigned*>(p);  // n bits: atoms selected so far
+
+  V* h0w = reinterpret_cast<V*>(a.h0_ws) + (size_t)blockIdx.x * n;
+  double* msc = a.mag_ws + (size_t)blockIdx.x * n;  // used only when a warp owns > 1 tile
+  const double gamma = HAD ? op.gr64[0] : op.g64[0].x;  // c(1) = M/N
+  // Gram entry (Phi^H Phi)_{ab}: from the staged kernel when it is exact fp64
+  // (c128 table, or the Hadamard integer lattice), else the fp64 table
+  auto gram_of = [&](unsigned ga, unsigned gb) -> double2 {
+    if constexpr (GMODE > 0 && HAD) {
+      return make_double2((double)((int)gH[ga ^ gb] - 32768) / (double)n, 0.0);
+    } else if constexpr (GMODE == 1 && sizeof(V) == 16) {
+      return to_c128(gF[(ga - gb) & (unsigned)(n - 1)]);
+    } else if constexpr (GMODE == 2 && sizeof(V) == 16) {
+      const unsigned j = (ga - gb) & (unsigned)(n - 1);
+      return j <= (unsigned)(n >> 1) ? to_c128(gF[j]) : to_c128(conj(gF[n - j]));
+    } else {
+      return gram<HAD>(op, ga, gb);
+    }
+  };
+  const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
+  const bool regs_only = ntiles > 0 && ntiles <= nw;  // every thread owns <= 1 tile
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_prob = atomicAdd(a.queue, 1);
+    __syncthreads();
+    const int64_t prob = s_prob;
+    if (prob >= a.batch) break;
+    const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
+    const double tol = a.tol[prob];
+
+    for (int i = tid; i < (n + 31) / 32; i += nth) s_sel[i] = 0u;
+    double yy = 0.0;
+    for (int j = tid; j < m; j += nth) yy += mag2(y[j]);
+    yy = block_sum(yy, red);
+    double rn = sqrt(yy);
+    double zz = 0.0;
+    int s = 0, iters = 0, aborted = 0, tlast = 0;
+    bool rn_explicit = true;
+    bool buf_h0 = false;  // buf currently holds h0 in padded layout
+
+    // explicit residual r = y - Phi_Lambda x by one forward transform of the
+    // sparse estimate (replaces update_residual, solvers.cpp:180-192)
+    auto residual_explicit = [&](int cnt) -> double {
+      for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
+      __syncthreads();
+      for (int j = tid; j < cnt; j += nth) {
+        V xv;
+        from_c128(s_x[j], xv);
+        buf[padx<OLOGP>(HAD ? (int)s_lam[j] : (int)brev_n(s_lam[j], log2n))] = xv;
+      }
+      __syncthreads();
+      block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth);
+      double r2 = 0.0;
+      for (int j = tid; j < m; j += nth) {
+        const V rv = sub(y[j], scale(buf[padx<OLOGP>((int)op.omega[j])], sc));
+        rs[j] = rv;
+        r2 += mag2(rv);
+      }
+      buf_h0 = false;
+      return sqrt(block_sum(r2, red));
+    };
+
+    if (!(rn <= tol)) {
+      for (int t = 1; t <= T; ++t) {
+        const bool fast_row = t >= 2 && (int64_t)t <= a.fast_until;
+        tlast = t;
+        // booked like the reference's cost rows: t = 1 counts under the plan
+        // (solvers.cpp:336-340) although it always runs the transform
+        if (a.modes && tid == 0) a.modes[prob * T + (t - 1)] = (int64_t)t <= a.fast_until ? 1 : 0;
+        V* hrow = a.hist ? reinterpret_cast<V*>(a.hist) + ((size_t)prob * T + (t - 1)) * n
+                         : nullptr;
+        double best = 0.0;
+        double m2[RPT];
+        if (!fast_row) {
+          // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
+          const V* r = t == 1 ? y : rs;
+          for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
+          __syncthreads();
+          for (int j = tid; j < m; j += nth)
+            buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
+          __syncthreads();
+          block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
+          if (t == 1) {
+            // h0 = Phi^H y stays in buf (scaled, padded) for the fast rows
+            for (int i = tid; i < nbuf; i += nth) buf[i] = scale(buf[i], sc);
+            __syncthreads();
+          }
+          const double scv = t == 1 ? 1.0 : sc;
+          for (int k = tid; k < n; k += nth) {
+            const V v = scale(buf[padx<OLOGP>(k)], scv);
+            if (t == 1) h0w[k] = v;
+            if (hrow) hrow[k] = v;
+            best = fmax(best, mag2(v));
+          }
+          buf_h0 = t == 1;
+        } else {
+          // fast correlation (kernel.cpp:209-303) from h0 and the staged c
+          if (!buf_h0) {
+            __syncthreads();
+            for (int k = tid; k < n; k += nth) buf[padx<OLOGP>(k)] = h0w[k];
+            buf_h0 = true;
+            __syncthreads();
+          }
+          if (ntiles) {
+            for (int tile = warp; tile < ntiles; tile += nw) {
+              const int i0 = tile * 32 * RPT;
+              V acc[RPT];
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) acc[r] = buf[padx<OLOGP>(i0 + lane + 32 * r)];
+              fast_tile<V, HAD, RPT, GMODE == 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) {
+                const int i = i0 + lane + 32 * r;
+                m2[r] = mag2(acc[r]);
+                if (!regs_only) msc[i] = m2[r];
+                best = fmax(best, m2[r]);
+                if (hrow) hrow[i] = acc[r];
+              }
+            }
+            if (regs_only && warp >= ntiles) {
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) m2[r] = -1.0;
+            }
+          } else {
+            for (int i = tid; i < n; i += nth) {
+              V acc = buf[padx<OLOGP>(i)];
+              fast_point<V, HAD, GMODE == 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
+              const double mm = mag2(acc);
+              msc[i] = mm;
+              best = fmax(best, mm);
+              if (hrow) hrow[i] = acc;
+            }
+          }
+        }
+        // identification with the tie band (solvers.cpp:90-101, :362-367)
+        best = block_max(best, red);
+        if (best == 0.0) break;
+        const double cut = best * (1.0 - kTieBandRel);
+        unsigned first = 0xffffffffu;
+        if (!fast_row) {
+          const double scv = t == 1 ? 1.0 : sc;
+          for (int k = tid; k < n; k += nth)
+            if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
+        } else if (regs_only) {
+#pragma unroll
+          for (int r = RPT - 1; r >= 0; --r)
+            if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
+        } else {
+          for (int k = tid; k < n; k += nth)
+            if (msc[k] >= cut) { first = (unsigned)k; break; }
+        }
+        const unsigned pick = block_min_u(first, redu);
+        // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
+        if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
+
+        // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H).
+        // l = W a with a_j = G(lambda_j, pick) looked up in c; thread i owns row i
+        for (int i = tid; i < s; i += nth) {
+          double ar = 0.0, ai = 0.0;
+          for (int j = 0; j <= i; ++j) {
+            const double2 w = W[wofs(T, i, j)], v = gram_of(s_lam[j], pick);
+            ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
+            ai = fma(w.x, v.y, fma(w.y, v.x, ai));
+          }
+          s_l[i] = make_double2(ar, ai);
+        }
+        double ll = 0.0, lzr = 0.0, lzi = 0.0;
+        for (int i = tid; i < s; i += nth) {
+          const double2 l = s_l[i], zc = s_z[i];
+          ll += l.x * l.x + l.y * l.y;
+          lzr += l.x * zc.x + l.y * zc.y;  // conj(l) z
+          lzi += l.x * zc.y - l.y * zc.x;
+        }
+        block_sum3(ll, lzr, lzi, red);  // also publishes s_l
+        const double d2 = gamma - ll;
+        // pivot floor as the reference's normal-equations path
+        // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
+        if (!(d2 > 1e-12 * gamma)) { aborted = 1; break; }
+        const double d = sqrt(d2);
+        const double2 bnew = to_c128(buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
+        const double2 znew = make_double2((bnew.x - lzr) / d, (bnew.y - lzi) / d);
+        // one pass per column j < s (a warp each) yields both the new row of W,
+        // W_sj = -(1/d) sum_{i=j}^{s-1} conj(l_i) W_ij, and the coefficient
+        // x_j = sum_{i=j}^{s-1} conj(W_ij) z_i + conj(W_sj) z_s   (x = W^H z)
+        for (int j = warp; j < s; j += nw) {
+          double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+          for (int i = j + lane; i < s; i += 32) {
+            const double2 l = s_l[i], w = W[wofs(T, i, j)], zc = s_z[i];
+            ar += l.x * w.x + l.y * w.y;  // conj(l) w
+            ai += l.x * w.y - l.y * w.x;
+            br += w.x * zc.x + w.y * zc.y;  // conj(w) z
+            bi += w.x * zc.y - w.y * zc.x;
+          }
+          ar = warp_sum(ar);
+          ai = warp_sum(ai);
+          br = warp_sum(br);
+          bi = warp_sum(bi);
+          if (lane == 0) {
+            const double2 wn = make_double2(-ar / d, -ai / d);
+            W[wofs(T, s, j)] = wn;
+            const double xr = br + wn.x * znew.x + wn.y * znew.y;
+            const double xi = bi + wn.x * znew.y - wn.y * znew.x;
+            s_x[j] = make_double2(xr, xi);
+            from_c128(make_double2(xr * xscale, xi * xscale), s_xn[j]);
+          }
+        }
+        if (tid == 0) {
+          W[wofs(T, s, s)] = make_double2(1.0 / d, 0.0);
+          s_z[s] = znew;
+          s_lam[s] = pick;
+          s_sel[pick >> 5] |= 1u << (pick & 31);
+          const double2 xs = make_double2(znew.x / d, znew.y / d);
+          s_x[s] = xs;
+          from_c128(make_double2(xs.x * xscale, xs.y * xscale), s_xn[s]);
+        }
+        zz += znew.x * znew.x + znew.y * znew.y;
+        ++s;
+        __syncthreads();
+        iters = t;
+
+        // ---- residual and halting (solvers.cpp:388-402)
+        const bool next_conv = t < T && !((int64_t)(t + 1) <= a.fast_until);
+        const double r2id = yy - zz;  // ||y||^2 - ||P y||^2
+        const bool near = !(r2id > tol * tol + a.margin * yy);
+        if (next_conv || near) {
+          rn = residual_explicit(s);
+          rn_explicit = true;
+        } else {
+          rn = sqrt(fmax(r2id, 0.0));
+          rn_explicit = false;
+        }
+        if (rn_explicit && rn <= tol) break;
+      }
+      if (!rn_explicit) rn = residual_explicit(s);
+    }
+    // ---- results (RecoveryResult, solvers.hpp:53-64)
+    uint64_t* sup = a.support + prob * T;
+    double2* co = a.coeffs + prob * T;
+    for (int j = tid; j < T; j += nth) {
+      sup[j] = j < s ? (uint64_t)s_lam[j] + 1 : 0;
+      co[j] = j < s ? s_x[j] : make_double2(0.0, 0.0);
+    }
+    if (tid == 0) {
+      a.size[prob] = (uint64_t)s;
+      a.iters[prob] = (uint64_t)iters;
+      a.resid[prob] = rn;
+      a.aborted[prob] = aborted;
+      if (a.hlen) a.hlen[prob] = (uint64_t)tlast;
+    }
+  }
+}
+
+struct OmpPlan {
+  size_t total;
+  int gmode;
+  bool rsm, wsm, bufg;
+  int off_g, off_r, off_w, off_tw, off_small, tw_a;
+};
+
+template <class V, bool HAD>
+OmpPlan omp_plan(const DevOp& op, int64_t T) {
+  OmpPlan p{};
+  const int64_t n = op.n, m = op.m;
+  auto al = [](size_t b) { return ((b + 15) / 16) * 16; };
+  const size_t buf = al((size_t)(n + (n >> OLOGP)) * sizeof(V));
+  const size_t gfull = al(HAD ? (size_t)n * 2 : (size_t)n * sizeof(V));
+  const size_t ghalf = al((size_t)(n / 2 + 1) * sizeof(V));
+  const size_t r = al((size_t)m * sizeof(V));
+  const size_t w = al((size_t)T * (T + 1) / 2 * 16);
+  p.tw_a = (op.log2n + 1) / 2;
+  const size_t tw = HAD ? 0 : al(2 * (((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) + 4) * sizeof(V);
+  const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
+                       al(4 * (size_t)((n + 31) / 32));
+  const size_t cap = (size_t)smem_optin() - 2048;
+  size_t tot = tw + small;
+  // the transform buffer lives in smem unless even it does not fit with the
+  // kernel table (then it is an L2-resident per-CTA global buffer)
+  const size_t gmin = HAD ? gfull : ghalf;
+  p.bufg = tot + buf + gmin > cap;
+  if (!p.bufg) tot += buf;
+  p.wsm = tot + w + gmin <= cap;  // W next: the least-squares phase is latency bound
+  if (p.wsm) tot += w;
+  p.gmode = 0;
+  if (!(HAD && !op.glat)) {
+    if (tot + gfull <= cap) { p.gmode = 1; tot += gfull; }
+    else if (!HAD && tot + ghalf <= cap) { p.gmode = 2; tot += ghalf; }
+  }
+  p.rsm = tot + r <= cap;
+  if (p.rsm) tot += r;
+  p.total = tot;
+  size_t off = p.bufg ? 0 : buf;
+  p.off_tw = (int)off; off += tw;
+  p.off_w = (int)off; if (p.wsm) off += w;
+  p.off_g = (int)off; off += p.gmode == 1 ? gfull : (p.gmode == 2 ? ghalf : 0);
+  p.off_r = (int)off; if (p.rsm) off += r;
+  p.off_small = (int)off;
+  return p;
+}
+
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
+void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
+  auto f = k_omp<V, HAD, RPT, GMODE, BUFG>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  f<<<grid, OMP_THREADS, smem, st>>>(k);
+}
+
+template <class V, bool HAD, int RPT, bool BUFG>
+void launch_g(const OmpK& k, int gmode, int grid, size_t smem, cudaStream_t st) {
+  if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG>(k, grid, smem, st);
+  else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG>(k, grid, smem, st);
+  else launch_k<V, HAD, RPT, 0, BUFG>(k, grid, smem, st);
+}
+
+template <class V, bool HAD, int RPT>
+cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  const OmpPlan p = omp_plan<V, HAD>(op, a.max_iter);
+  if (p.total > (size_t)smem_optin() - 2048) return cudaErrorInvalidConfiguration;
+  OmpK k{};
+  k.op = op;
+  k.y = a.y;
+  k.tol = a.tol;
+  k.batch = a.batch;
+  k.T = (int)a.max_iter;
+  k.fast_until = a.fast_until;
+  k.support = a.support;
+  k.coeffs = a.coeffs;
+  k.size = a.size;
+  k.iters = a.iters;
+  k.hlen = a.hlen;
+  k.resid = a.resid;
+  k.aborted = a.aborted;
+  k.modes = a.modes;
+  k.hist = a.hist;
+  k.w_ws = a.w_ws;
+  k.h0_ws = a.h0_ws;
+  k.mag_ws = a.mag_ws;
+  k.r_ws = a.r_ws;
+  k.queue = a.queue;
+  k.r_smem = p.rsm;
+  k.w_smem = p.wsm;
+  k.buf_ws = a.buf_ws;
+  if (p.bufg && !a.buf_ws) return cudaErrorInvalidValue;
+  k.off_g = p.off_g;
+  k.off_r = p.off_r;
+  k.off_w = p.off_w;
+  k.off_tw = p.off_tw;
+  k.off_small = p.off_small;
+  k.tw_a = p.tw_a;
+  k.margin = is_double(a.dtype) ? 1e-10 : 1e-5;
+  const int grid = std::max(1, a.grid);
+  if (p.bufg) launch_g<V, HAD, RPT, true>(k, p.gmode, grid, p.total, st);
+  else launch_g<V, HAD, RPT, false>(k, p.gmode, grid, p.total, st);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+template <class V, bool HAD>
+cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
+  if (a.op->n >= 32 * 8 * 16) return launch_omp_t<V, HAD, 8>(a, st);
+  return launch_omp_t<V, HAD, 2>(a, st);
+}
+
+}  // namespace
+}  // namespace fmp

@@ -342,15 +342,16 @@ def test_omp_config2_shape(fmp, oracle, mode):
         assert sorted(res.support[b, :s]) == list(np.flatnonzero(X[b]) + 1)
 
 
-def test_omp_config4_shape_c64(fmp, oracle):
-    # config 4 shape (reduced batch): Fourier N=16384, M=4096, K=128, c64, 30 dB noise,
-    # halt at ||r|| <= ||noise|| or 2K iterations
+@pytest.mark.parametrize("dtype,tol", [(np.complex64, 1e-4), (np.complex128, 1e-10)])
+def test_omp_config4_shape(fmp, oracle, dtype, tol):
+    # config 4 shape (reduced batch): Fourier N=16384, M=4096, K=128, c64 and c128,
+    # 30 dB noise, halt at ||r|| <= ||noise|| or 2K iterations
     n, m, k, B = 16384, 4096, 128, 2
     sigma = np.sqrt(k / (2 * n * 1e3))
     om = oracle.make_row_selection(n, m, oracle.derive_seed(4, 1 << 40))
     op = fmp.SensingOperator("fourier", n, om)
     Y, X, nn = fmp.make_batch("fourier", n, om, k, B, base_seed=4, noise_stddev=sigma, want_x=True)
-    Y32 = Y.astype(np.complex64)
+    Y32 = Y.astype(dtype)
     res = fmp.omp_solve_batch(op, Y32, fmp.SolveConfig(2 * k, 0.0, "adaptive"), tolerances=nn)
     agree = 0
     for b in range(B):
@@ -359,7 +360,8 @@ def test_omp_config4_shape_c64(fmp, oracle):
         same = list(res.support[b, :s]) == list(r.support)
         agree += same
         if same:
-            assert rel(res.coeffs[b, :s], r.coeffs) < 1e-4
+            assert rel(res.coeffs[b, :s], r.coeffs) < tol
+            assert int(res.iterations[b]) == r.iterations_run
         truth = set((np.flatnonzero(X[b]) + 1).tolist())
         assert len(truth & set(res.support[b, :s].tolist())) >= 0.9 * len(truth)
     assert agree == B
