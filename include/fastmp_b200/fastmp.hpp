@@ -1,0 +1,249 @@
+// fastmp_b200/fastmp.hpp — C++ drop-in for the reference library's
+// correlation / OMP interface (/root/reference/proj/include/fastmp/*.hpp).
+//
+// Same namespace, type names, signatures, argument meaning and exceptions as
+// the reference, so code written against `fastmp::` recompiles against this
+// header and links libfastmp_b200.so instead of libfastmp.a.  Every transform,
+// kernel build, fast update, least-squares solve and OMP iteration runs on the
+// GPU through the C ABI in include/fmp.h; nothing computes on the host except
+// closed-form scalars (entry, product_index, the analytic cost formulas).
+//
+// Differences a caller can observe:
+//   - least squares is an incremental Cholesky on Gram entries looked up in
+//     the correlation kernel for both LeastSquaresMethod values; coefficients
+//     agree with the reference's MGS-QR to ~1e-14 relative, and supports are
+//     identical (the reference's own 1e-9 identification tie band absorbs the
+//     last-bit differences); rank deficiency uses the normal-equations pivot
+//     floor (solvers.cpp:32,144)
+//   - FlopCounter / CostReport carry the analytic Table-I counts (the GPU does
+//     not count executed operations)
+//   - non-power-of-two Fourier sizes (the reference's dense fallback) throw
+//     std::invalid_argument
+//   - the batched overload omp_solve_batch is an addition
+#pragma once
+
+#include <complex>
+#include <cstddef>
+#include <cstdint>
+#include <iosfwd>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fastmp {
+
+// ------------------------------------------------------------------ types
+using cplx = std::complex<double>;
+using cvec = std::vector<cplx>;
+
+enum class TransformKind { Fourier, Hadamard };
+const char* to_string(TransformKind kind) noexcept;
+TransformKind parse_kind(const std::string& name);
+
+constexpr bool is_power_of_two(std::size_t n) noexcept { return n && !(n & (n - 1)); }
+constexpr std::size_t log2_floor(std::size_t n) noexcept {
+  std::size_t p = 0;
+  while (n >>= 1) ++p;
+  return p;
+}
+double l2_norm(const cvec& v) noexcept;
+double l2_distance(const cvec& a, const cvec& b);
+
+// ----------------------------------------------------------------- random
+std::uint64_t splitmix64(std::uint64_t x) noexcept;
+std::uint64_t derive_seed(std::uint64_t base, std::uint64_t index) noexcept;
+
+// ------------------------------------------------------------- cost model
+inline constexpr std::uint64_t kComplexMulFlops = 6;
+inline constexpr std::uint64_t kComplexAddFlops = 2;
+
+struct FlopCounter {
+  std::uint64_t complex_mul = 0, complex_add = 0, real_mul = 0, real_add = 0;
+  std::uint64_t flops() const noexcept {
+    return kComplexMulFlops * complex_mul + kComplexAddFlops * complex_add + real_mul + real_add;
+  }
+  void reset() noexcept { *this = FlopCounter{}; }
+};
+
+enum class CorrelationMode { Conventional, Fast, Adaptive };
+const char* to_string(CorrelationMode mode) noexcept;
+CorrelationMode parse_mode(const std::string& name);
+
+std::uint64_t conventional_iteration_flops(TransformKind kind, std::size_t n);
+std::uint64_t fast_iteration_flops(TransformKind kind, std::size_t n, std::size_t t);
+std::size_t crossover_iteration(TransformKind kind, std::size_t n);
+
+struct IterationCost {
+  std::size_t t = 0;
+  CorrelationMode mode_used = CorrelationMode::Conventional;
+  std::uint64_t analytic_flops = 0;
+  FlopCounter counted;  // analytic here (see header comment)
+  bool dense_fallback = false;
+};
+
+struct CostReport {
+  TransformKind kind = TransformKind::Fourier;
+  std::size_t n = 0;
+  std::vector<IterationCost> iterations;
+  std::uint64_t kernel_precompute_flops = 0;
+  std::uint64_t least_squares_flops = 0;
+  std::uint64_t identification_flops = 0;
+  void write_csv(std::ostream& os) const;
+};
+
+// ----------------------------------------------------------------- device
+// A GPU context (device, stream, workspace).  Operators bind to the calling
+// thread's default device unless one is given.
+class Device {
+ public:
+  explicit Device(int ordinal = 0);
+  ~Device();
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  void* handle() const noexcept { return ctx_; }
+  int ordinal() const noexcept { return ordinal_; }
+  static std::shared_ptr<Device> default_device();
+
+ private:
+  void* ctx_ = nullptr;
+  int ordinal_ = 0;
+};
+
+// ------------------------------------------------------------- transforms
+class StructuredUnitary {
+ public:
+  StructuredUnitary(TransformKind kind, std::size_t n);
+  TransformKind kind() const noexcept { return kind_; }
+  std::size_t size() const noexcept { return n_; }
+  bool fast_path() const noexcept { return true; }
+  cvec forward(const cvec& v, FlopCounter* fc = nullptr) const;  // U v
+  cvec adjoint(const cvec& v, FlopCounter* fc = nullptr) const;  // U^H v
+  cplx entry(std::size_t row, std::size_t col) const;
+  cvec column(std::size_t col) const;
+  std::size_t product_index(std::size_t i, std::size_t j) const;
+  cvec dense() const;
+
+ private:
+  void* unit_op() const;  // lazily built device operator (all transforms)
+  TransformKind kind_;
+  std::size_t n_;
+  mutable std::shared_ptr<void> op_;
+};
+
+// ---------------------------------------------------------------- sensing
+struct RowSelection {
+  std::size_t n = 0;
+  std::vector<std::size_t> omega;  // 1-based, sorted
+  std::size_t m() const noexcept { return omega.size(); }
+};
+RowSelection make_row_selection(std::size_t n, std::size_t m, std::uint64_t seed);
+RowSelection make_row_selection(std::size_t n, std::vector<std::size_t> rows);
+
+class SensingOperator {
+ public:
+  SensingOperator(StructuredUnitary unitary, RowSelection selection,
+                  std::shared_ptr<Device> device = nullptr);
+  const StructuredUnitary& unitary() const noexcept { return unitary_; }
+  const RowSelection& selection() const noexcept { return selection_; }
+  std::size_t n() const noexcept { return unitary_.size(); }
+  std::size_t m() const noexcept { return selection_.omega.size(); }
+  cvec apply(const cvec& x, FlopCounter* fc = nullptr) const;
+  cvec apply_adjoint(const cvec& r, FlopCounter* fc = nullptr) const;
+  cvec column(std::size_t j) const;
+  void* handle() const noexcept { return op_.get(); }  // fmp_op
+  std::shared_ptr<void> device_handle() const noexcept { return op_; }
+
+ private:
+  StructuredUnitary unitary_;
+  RowSelection selection_;
+  std::shared_ptr<Device> device_;
+  std::shared_ptr<void> op_;
+};
+
+struct ProblemInstance {
+  TransformKind kind = TransformKind::Fourier;
+  std::size_t n = 0, m = 0, k = 0;
+  std::uint64_t seed = 0;
+  std::vector<std::size_t> omega;
+  cvec x_true, y, noise;
+};
+ProblemInstance make_instance(const SensingOperator& op, std::size_t k, double noise_stddev,
+                              std::uint64_t seed);
+
+// ----------------------------------------------------------------- kernel
+struct CorrelationKernel {
+  TransformKind kind = TransformKind::Fourier;
+  std::size_t n = 0;
+  std::size_t m = 0;
+  cvec c;
+  std::vector<double> values;               // Hadamard only
+  std::vector<std::uint32_t> value_index;   // Hadamard only
+  std::shared_ptr<void> device_op;          // the operator whose c this is
+};
+
+CorrelationKernel compute_kernel(const SensingOperator& op, FlopCounter* fc = nullptr);
+
+struct PermutationAction {
+  TransformKind kind = TransformKind::Fourier;
+  std::size_t n = 0;
+  std::size_t lambda = 1;
+  std::size_t map_index(std::size_t i) const;
+};
+
+struct FastUpdateOptions {
+  bool fourier_symmetry = false;  // accepted; results agree to rounding either way
+};
+
+cvec fast_update(const cvec& h0, const CorrelationKernel& kernel,
+                 const std::vector<std::size_t>& support, const cvec& coeffs,
+                 const FastUpdateOptions& opts = {}, FlopCounter* fc = nullptr);
+
+// ---------------------------------------------------------------- solvers
+enum class LeastSquaresMethod { IncrementalQR, NormalEquations };
+
+struct SolveConfig {
+  std::size_t max_iterations = 1;
+  double residual_tolerance = 0.0;
+  CorrelationMode correlation_mode = CorrelationMode::Conventional;
+  LeastSquaresMethod ls_method = LeastSquaresMethod::IncrementalQR;
+  bool fourier_symmetry = false;
+  bool record_correlations = false;
+  bool check_invariants = false;
+};
+SolveConfig default_config(std::size_t k, double y_norm);
+
+class RankDeficientError : public std::runtime_error {
+ public:
+  RankDeficientError(std::size_t position, const std::string& what)
+      : std::runtime_error(what), position_(position) {}
+  std::size_t position() const noexcept { return position_; }
+
+ private:
+  std::size_t position_;
+};
+
+struct RecoveryResult {
+  cvec x_hat;
+  std::vector<std::size_t> support;
+  cvec coeffs;
+  std::size_t iterations_run = 0;
+  double residual_norm = 0.0;
+  bool rank_deficient_abort = false;
+  CostReport costs;
+  std::vector<std::vector<std::size_t>> support_history;
+  std::vector<cvec> correlation_history;
+};
+
+RecoveryResult omp_solve(const SensingOperator& op, const cvec& y, const SolveConfig& cfg);
+
+// Batched extension: one launch solves every measurement vector.
+std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std::vector<cvec>& ys,
+                                            const SolveConfig& cfg);
+
+cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
+                   const cvec& y, LeastSquaresMethod method = LeastSquaresMethod::NormalEquations,
+                   FlopCounter* fc = nullptr);
+
+}  // namespace fastmp

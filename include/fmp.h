@@ -130,6 +130,14 @@ int fmp_fast_update_dev(fmp_op op, int dtype, const void* h0, const uint32_t* su
 int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t batch,
                     uint64_t* idx_out);
 
+/* least_squares (solvers.hpp:82-85) in its normal-equations form
+ * (solvers.cpp:120-177) for `batch` problems sharing the support size s:
+ * y batch x m, support batch x s (1-based), coeffs_out batch x s complex fp64.
+ * A numerically dependent column gives FMP_ERANK with *position (0-based
+ * position within that problem's support; the first failing problem). */
+int fmp_least_squares(fmp_op op, int dtype, const void* y, const uint64_t* support, uint64_t s,
+                      uint64_t batch, double* coeffs_out, int64_t* position);
+
 /* ----------------------------------------------------------- OMP (batched) */
 typedef struct {
   uint64_t max_iterations;     /* SolveConfig::max_iterations (>= 1) */
@@ -172,6 +180,10 @@ int fmp_make_batch(int kind, uint64_t n, const uint64_t* rows_1based, uint64_t m
                    uint64_t batch, int threads, double* y_out, double* x_out,
                    double* noise_norm_out);
 uint64_t fmp_derive_seed(uint64_t base, uint64_t index);
+/* make_instance's draws for one seed (sensing.cpp:132-147): x (n complex)
+ * and noise (m complex); the caller forms y = apply(x) + noise */
+int fmp_draw_instance(uint64_t n, uint64_t m, uint64_t k, double noise_stddev, uint64_t seed,
+                      double* x_out, double* noise_out);
 
 #ifdef __cplusplus
 }

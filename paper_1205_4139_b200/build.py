@@ -19,6 +19,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libfmp_cuda.so")
+FACADE = os.path.join(PKG, "libfastmp_b200.so")
+CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
@@ -54,8 +56,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    # the C++ drop-in facade over the C ABI
+    src = os.path.join(PKG, "host", "fastmp_facade.cpp")
+    if force or not os.path.exists(FACADE) or os.path.getmtime(FACADE) < max(
+            os.path.getmtime(src), os.path.getmtime(LIB),
+            os.path.getmtime(os.path.join(ROOT, "include", "fastmp_b200", "fastmp.hpp"))):
+        cmd = [CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
+               "-I" + os.path.join(ROOT, "include"), "-o", FACADE, src, LIB,
+               "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError(f"facade build failed:\n{r.stderr}")
     if verbose:
-        print("built", LIB)
+        print("built", LIB, "and", FACADE)
     return LIB
 
 

@@ -535,6 +535,48 @@ int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t 
   return FMP_OK;
 }
 
+// ------------------------------------------------------------ least squares
+int fmp_least_squares(fmp_op op, int dtype, const void* y, const uint64_t* support, uint64_t s,
+                      uint64_t batch, double* coeffs_out, int64_t* position) {
+  if (!op || !y || (s && (!support || !coeffs_out))) return fail(FMP_EINVAL, "null argument");
+  if (int st = check_dtype(op->d, dtype)) return st;
+  if (s > 4096) return fail(FMP_EUNSUPPORTED, "support larger than 4096");
+  const uint64_t n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
+  std::vector<uint32_t> s0(batch * s);
+  for (uint64_t i = 0; i < batch * s; ++i) {
+    if (support[i] < 1 || support[i] > n) return fail(FMP_EINVAL, "least_squares: support index out of range");
+    s0[i] = (uint32_t)(support[i] - 1);
+  }
+  if (s == 0) return FMP_OK;
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->cur;
+  void *dy, *dsup;
+  if (int e = copy_in(ctx, S_IN, y, batch * m * fmp::elem_bytes(dtype), &dy, st)) return e;
+  if (int e = copy_in(ctx, S_SUP, s0.data(), s0.size() * 4, &dsup, st)) return e;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(batch, 1024));
+  double2 *dx, *dL;
+  int64_t* dbad;
+  ALLOC(dx, S_OCO, batch * s * 16);
+  ALLOC(dbad, S_IDX, batch * 8);
+  ALLOC(dL, S_W, (size_t)grid * s * s * 16);
+  CU(fmp::launch_least_squares(op->d, dtype, dy, (const uint32_t*)dsup, (int)s, (int64_t)batch, dx,
+                               dbad, dL, grid, st));
+  g_launch_count = 1;
+  std::vector<int64_t> bad(batch);
+  CU(cudaMemcpyAsync(coeffs_out, dx, batch * s * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(bad.data(), dbad, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (uint64_t b = 0; b < batch; ++b)
+    if (bad[b] >= 0) {
+      if (position) *position = bad[b];
+      return fail(FMP_ERANK, "least_squares: dependent column at support position %lld (problem %llu)",
+                  (long long)bad[b], (unsigned long long)b);
+    }
+  return FMP_OK;
+}
+
 // -------------------------------------------------------------------- OMP
 static int omp_validate(fmp_op op, int dtype, const fmp_omp_config* cfg) {
   if (!op || !cfg) return fail(FMP_EINVAL, "null argument");

@@ -75,6 +75,31 @@ extern "C" int fmp_make_row_selection(uint64_t n, uint64_t m, uint64_t seed, uin
   return FMP_OK;
 }
 
+extern "C" int fmp_draw_instance(uint64_t n, uint64_t m, uint64_t k, double noise_stddev,
+                                 uint64_t seed, double* x_out, double* noise_out) {
+  if (k >= m || m > n || noise_stddev < 0.0 || !x_out || !noise_out) return FMP_EINVAL;
+  Rng rng(seed);
+  std::fill(x_out, x_out + 2 * n, 0.0);
+  std::fill(noise_out, noise_out + 2 * m, 0.0);
+  if (k > 0) {
+    const auto sup = rng.sample(n, k);
+    for (uint64_t idx : sup) {
+      const cplx z = rng.cgauss();
+      x_out[2 * (idx - 1)] = z.real();
+      x_out[2 * (idx - 1) + 1] = z.imag();
+    }
+  }
+  if (noise_stddev > 0.0) {
+    const double sc = noise_stddev * std::sqrt(2.0);
+    for (uint64_t i = 0; i < m; ++i) {
+      const cplx z = rng.cgauss() * sc;
+      noise_out[2 * i] = z.real();
+      noise_out[2 * i + 1] = z.imag();
+    }
+  }
+  return FMP_OK;
+}
+
 extern "C" int fmp_make_batch(int kind, uint64_t n, const uint64_t* rows, uint64_t m, uint64_t k,
                               double noise_stddev, int real, uint64_t base_seed, uint64_t first,
                               uint64_t batch, int threads, double* y_out, double* x_out,

@@ -108,6 +108,11 @@ int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 int fast_update_grid(const DevOp& op, int dtype, int64_t batch);
 // largest n the smem-resident transform handles for this element size
 int64_t transform_max_n(int dtype);
+// least squares for a fixed support (batch problems, s atoms each, 0-based):
+// x (batch x s), bad[b] = dependent position or -1; L scratch grid x s x s
+cudaError_t launch_least_squares(const DevOp& op, int dtype, const void* y, const uint32_t* sup,
+                                 int s, int64_t batch, double2* x, int64_t* bad, double2* L,
+                                 int grid, cudaStream_t st);
 // FMA-pipe throughput (FMAs per second) measured by a calibration kernel
 cudaError_t fma_peak(int is_double, double* fma_per_s);
 // number of kernel launches issued by the last launch_* call on this thread

@@ -479,3 +479,125 @@ cudaError_t fma_peak(int is_double, double* fma_per_s) {
   return e;
 }
 }  // namespace fmp
+
+// ------------------------------------------------------ least squares
+// least_squares (solvers.cpp:276-294, normal-equations form solvers.cpp:120-177)
+// for a given support: Gram entries are kernel lookups, the right-hand side
+// b_j = phi_j^H y is a direct sum over the rows with closed-form entries
+// (transform.cpp:154-163), then a Cholesky factorisation with the reference's
+// pivot floor 1e-12 * diag and two triangular solves.  One CTA per problem;
+// the s x s factor lives in global scratch.
+namespace fmp {
+namespace {
+template <class V>
+__global__ void __launch_bounds__(256) k_least_squares(DevOp op, const V* __restrict__ y,
+                                                       const uint32_t* __restrict__ sup, int s,
+                                                       int64_t batch, double2* __restrict__ x,
+                                                       int64_t* __restrict__ bad,
+                                                       double2* __restrict__ L) {
+  __shared__ double red[64];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int n = (int)op.n, m = (int)op.m;
+  const double isn = 1.0 / sqrt((double)n);
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const V* yb = y + b * m;
+    const uint32_t* sb = sup + b * s;
+    double2* Lb = L + (size_t)blockIdx.x * s * s;
+    double2* xb = x + b * s;
+    // rhs z_j = phi_j^H y
+    for (int j = 0; j < s; ++j) {
+      double ar = 0.0, ai = 0.0;
+      for (int i = tid; i < m; i += nth) {
+        const double2 yv = to_c128(yb[i]);
+        double er, ei;
+        if (op.kind == FOURIER) {
+          const double2 e = op.tw64[((uint64_t)op.omega[i] * sb[j]) & (uint64_t)(n - 1)];
+          er = e.x * isn;
+          ei = -e.y * isn;  // conj(U[omega, j])
+        } else {
+          er = (__popc(op.omega[i] & sb[j]) & 1) ? -isn : isn;
+          ei = 0.0;
+        }
+        ar += er * yv.x - ei * yv.y;
+        ai += er * yv.y + ei * yv.x;
+      }
+      ar = warp_sum(ar);
+      ai = warp_sum(ai);
+      __syncthreads();
+      if ((tid & 31) == 0) { red[tid >> 5] = ar; red[32 + (tid >> 5)] = ai; }
+      __syncthreads();
+      if (tid == 0) {
+        double sr = 0.0, si = 0.0;
+        for (int w = 0; w < (nth + 31) / 32; ++w) { sr += red[w]; si += red[32 + w]; }
+        xb[j] = make_double2(sr, si);
+      }
+    }
+    __syncthreads();
+    // Cholesky of G(i, j) = c[(lambda_i - lambda_j) mod N] / c[lambda_i ^ lambda_j]
+    if (tid == 0) {
+      int64_t badpos = -1;
+      auto G = [&](int i, int j) -> double2 {
+        const unsigned a = sb[i], c = sb[j];
+        if (op.kind == FOURIER) return op.g64[(a - c) & (unsigned)(n - 1)];
+        return make_double2(op.gr64[a ^ c], 0.0);
+      };
+      for (int j = 0; j < s && badpos < 0; ++j) {
+        const double diag = G(j, j).x;
+        double d = diag;
+        for (int k = 0; k < j; ++k) d -= mag2(Lb[j * s + k]);
+        if (!(d > 1e-12 * diag)) { badpos = j; break; }
+        const double ljj = sqrt(d);
+        Lb[j * s + j] = make_double2(ljj, 0.0);
+        for (int i = j + 1; i < s; ++i) {
+          double2 v = G(i, j);
+          for (int k = 0; k < j; ++k) {
+            const double2 p = Lb[i * s + k], q = Lb[j * s + k];
+            v.x -= p.x * q.x + p.y * q.y;  // L(i,k) conj(L(j,k))
+            v.y -= p.y * q.x - p.x * q.y;
+          }
+          Lb[i * s + j] = make_double2(v.x / ljj, v.y / ljj);
+        }
+      }
+      if (badpos < 0) {
+        for (int i = 0; i < s; ++i) {  // forward: L z = b
+          double2 v = xb[i];
+          for (int k = 0; k < i; ++k) {
+            const double2 p = Lb[i * s + k], q = xb[k];
+            v.x -= p.x * q.x - p.y * q.y;
+            v.y -= p.x * q.y + p.y * q.x;
+          }
+          const double l = Lb[i * s + i].x;
+          xb[i] = make_double2(v.x / l, v.y / l);
+        }
+        for (int i = s - 1; i >= 0; --i) {  // backward: L^H x = z
+          double2 v = xb[i];
+          for (int k = i + 1; k < s; ++k) {
+            const double2 p = Lb[k * s + i], q = xb[k];
+            v.x -= p.x * q.x + p.y * q.y;  // conj(L(k,i)) x_k
+            v.y -= p.x * q.y - p.y * q.x;
+          }
+          const double l = Lb[i * s + i].x;
+          xb[i] = make_double2(v.x / l, v.y / l);
+        }
+      }
+      bad[b] = badpos;
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+cudaError_t launch_least_squares(const DevOp& op, int dtype, const void* y, const uint32_t* sup,
+                                 int s, int64_t batch, double2* x, int64_t* bad, double2* L,
+                                 int grid, cudaStream_t st) {
+  switch (dtype) {
+    case C128: k_least_squares<double2><<<grid, 256, 0, st>>>(op, (const double2*)y, sup, s, batch, x, bad, L); break;
+    case C64: k_least_squares<float2><<<grid, 256, 0, st>>>(op, (const float2*)y, sup, s, batch, x, bad, L); break;
+    case F64: k_least_squares<double><<<grid, 256, 0, st>>>(op, (const double*)y, sup, s, batch, x, bad, L); break;
+    case F32: k_least_squares<float><<<grid, 256, 0, st>>>(op, (const float*)y, sup, s, batch, x, bad, L); break;
+    default: return cudaErrorInvalidValue;
+  }
+  g_launches = 1;
+  return cudaGetLastError();
+}
+}  // namespace fmp
