@@ -168,6 +168,39 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch,
 int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
                       const fmp_omp_config* cfg, fmp_omp_result* out, void* stream);
 
+/* ------------------------------------------- sharded single-signal solver */
+/* omp_solve for ONE large signal spread over `nshards` GPUs (config 5).
+ * Shard p owns the correlation entries k = p + nshards * k' (1-based atom
+ * k + 1).  Each iteration the caller exchanges two things between shards:
+ *   1. best = max over shards of fmp_large's local best |h|^2
+ *   2. pick = min over shards of fmp_large_first(best) (0 = none on that
+ *      shard), together with h0 at pick from the owning shard
+ * then calls fmp_large_advance(pick, h0) on every shard.  Least squares is
+ * replicated (bit-identical on every shard).  The identification rule is the
+ * reference's band argmax (solvers.cpp:90-101) evaluated globally.
+ * fmp_large_solve runs the whole loop for nshards = 1.  Fourier only. */
+typedef struct fmp_large_s* fmp_large;
+int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
+                     const fmp_omp_config* cfg, fmp_large* out);
+int fmp_large_destroy(fmp_large lg);
+/* y: m values (host); *local_best: max |h_1|^2 of this shard (t = 1), or -1
+ * when ||y|| <= tol (no iterations) */
+int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best);
+/* first 1-based atom of this shard with |h|^2 >= global_best (1 - 1e-9), or 0;
+ * h0_at (2 doubles) receives h0 there */
+int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0_at);
+/* append `atom` (1-based; h0_at its h0), least squares, residual, halting and
+ * the next correlation; *done = 1 when the solve has ended; *local_best as in
+ * fmp_large_begin for the next iteration */
+int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* done,
+                      double* local_best);
+/* end the solve without appending (zero correlation or a repeated atom) */
+int fmp_large_stop(fmp_large lg);
+int fmp_large_result(fmp_large lg, uint64_t* support, double* coeffs, uint64_t* support_size,
+                     uint64_t* iterations, double* residual, int32_t* aborted);
+int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* cfg,
+                    fmp_omp_result* out);
+
 /* ------------------------------------------------------ instance generation */
 /* seeded synthetic problems for the bench / parity harness, following the
  * reference's make_row_selection / make_instance recipes (sensing.cpp:61-70,

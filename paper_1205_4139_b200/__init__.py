@@ -100,6 +100,15 @@ _sig("fmp_argmax_band", C.c_int, _vp, C.c_int, _vp, _u64, _u64, _vp)
 _sig("fmp_omp_solve", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig), C.POINTER(OmpResult))
 _sig("fmp_omp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig),
      C.POINTER(OmpResult), _vp)
+_sig("fmp_large_create", C.c_int, _vp, C.c_int, _u64, _u64, C.POINTER(OmpConfig), C.POINTER(_vp))
+_sig("fmp_large_destroy", C.c_int, _vp)
+_sig("fmp_large_begin", C.c_int, _vp, _vp, C.c_double, C.POINTER(C.c_double))
+_sig("fmp_large_first", C.c_int, _vp, C.c_double, C.POINTER(_u64), _vp)
+_sig("fmp_large_advance", C.c_int, _vp, _u64, _vp, C.POINTER(C.c_int), C.POINTER(C.c_double))
+_sig("fmp_large_stop", C.c_int, _vp)
+_sig("fmp_large_result", C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp)
+_sig("fmp_large_solve", C.c_int, _vp, C.c_int, _vp, C.POINTER(OmpConfig), C.POINTER(OmpResult))
+_sig("fmp_least_squares", C.c_int, _vp, C.c_int, _vp, _vp, _u64, _u64, _vp, C.POINTER(C.c_int64))
 _sig("fmp_make_row_selection", C.c_int, _u64, _u64, _u64, _vp)
 _sig("fmp_make_batch", C.c_int, C.c_int, _u64, _vp, _u64, _u64, C.c_double, C.c_int, _u64, _u64,
      _u64, C.c_int, _vp, _vp, _vp)
@@ -497,6 +506,138 @@ def make_batch(kind, n: int, rows, k: int, batch: int, base_seed: int, first: in
     return Y, X, nn
 
 
+def least_squares(op: SensingOperator, support, y, dtype=None) -> np.ndarray:
+    """least_squares (solvers.hpp:82-85), normal-equations form, on the GPU.
+    Raises RankDeficientError(position) for dependent columns."""
+    y = op._prep(y, op.m, dtype)
+    Y = y[None] if y.ndim == 1 else y
+    sup = np.ascontiguousarray(np.asarray(support, np.uint64).reshape(Y.shape[0], -1))
+    s = sup.shape[1]
+    out = np.zeros((Y.shape[0], s), np.complex128)
+    pos = C.c_int64(-1)
+    st = _lib.fmp_least_squares(op.handle, DTYPES[Y.dtype], _ptr(Y), _ptr(sup) if s else None, s,
+                                Y.shape[0], _ptr(out) if s else None, C.byref(pos))
+    if st == 2:
+        e = RankDeficientError(2, (_lib.fmp_last_error() or b"").decode())
+        e.position = int(pos.value)
+        raise e
+    _check(st)
+    return out[0] if y.ndim == 1 else out
+
+
+# ------------------------------------------- sharded single-signal solver
+class LargeShard:
+    """Shard p of P of the config-5 solver (fmp_large_*): correlation entries
+    k = p + P k' live here; least squares is replicated."""
+
+    def __init__(self, op: SensingOperator, cfg: SolveConfig, shard: int = 0, nshards: int = 1,
+                 dtype=np.complex64):
+        self.op = op
+        self.dtype = np.dtype(dtype)
+        c = _config(cfg)
+        h = _vp()
+        _check(_lib.fmp_large_create(op.handle, DTYPES[self.dtype], shard, nshards, C.byref(c),
+                                     C.byref(h)))
+        self.handle = h
+        self.T = int(cfg.max_iterations)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.fmp_large_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def begin(self, y, tol: float) -> float:
+        y = np.ascontiguousarray(np.asarray(y, self.dtype))
+        self._y = y
+        b = C.c_double(0)
+        _check(_lib.fmp_large_begin(self.handle, _ptr(y), float(tol), C.byref(b)))
+        return b.value
+
+    def first(self, best: float):
+        a = _u64(0)
+        h = np.zeros(2)
+        _check(_lib.fmp_large_first(self.handle, float(best), C.byref(a), _ptr(h)))
+        return int(a.value), complex(h[0], h[1])
+
+    def advance(self, atom: int, h0: complex):
+        h = np.array([h0.real, h0.imag])
+        d = C.c_int(0)
+        b = C.c_double(0)
+        _check(_lib.fmp_large_advance(self.handle, int(atom), _ptr(h), C.byref(d), C.byref(b)))
+        return bool(d.value), b.value
+
+    def stop(self):
+        _check(_lib.fmp_large_stop(self.handle))
+
+    def result(self):
+        sup = np.zeros(self.T, np.uint64)
+        co = np.zeros(self.T, np.complex128)
+        sz, it = _u64(0), _u64(0)
+        rn = C.c_double(0)
+        ab = C.c_int32(0)
+        _check(_lib.fmp_large_result(self.handle, _ptr(sup), _ptr(co), C.byref(sz), C.byref(it),
+                                     C.byref(rn), C.byref(ab)))
+        s = sz.value
+        return sup[:s].copy(), co[:s].copy(), int(it.value), rn.value, bool(ab.value)
+
+
+class LocalExchange:
+    """In-process exchange for shards emulated on one device (tests)."""
+
+    def max(self, values):
+        return max(values)
+
+    def first(self, atoms):
+        cands = [(a, h) for a, h in atoms if a > 0]
+        return min(cands, key=lambda ah: ah[0]) if cands else (0, 0j)
+
+
+def sharded_solve(shards, y, tol: float, exchange=None):
+    """Drive shards through one solve (identification = the reference's band
+    argmax over the union of the shards, solvers.cpp:90-101).  `shards` holds
+    the local shard objects (all P of them when emulating on one device, one
+    per process otherwise with a distributed `exchange`)."""
+    ex = exchange or LocalExchange()
+    bests = [sh.begin(y, tol) for sh in shards]
+    best = ex.max(bests)
+    if best < 0:  # ||y|| <= tol: no iterations
+        return shards[0].result()
+    while True:
+        if best == 0.0:
+            for sh in shards:
+                sh.stop()
+            break
+        atom, h0 = ex.first([sh.first(best) for sh in shards])
+        outs = [sh.advance(atom, h0) for sh in shards]
+        if any(d for d, _ in outs):
+            break
+        best = ex.max([b for _, b in outs])
+    return shards[0].result()
+
+
+def large_solve(op: SensingOperator, y, cfg: SolveConfig, dtype=np.complex64):
+    """omp_solve for one large signal on one GPU (fmp_large_solve)."""
+    y = np.ascontiguousarray(np.asarray(y, dtype))
+    T = int(cfg.max_iterations)
+    sup = np.zeros(T, np.uint64)
+    co = np.zeros(T, np.complex128)
+    sz = np.zeros(1, np.uint64)
+    it = np.zeros(1, np.uint64)
+    rn = np.zeros(1)
+    ab = np.zeros(1, np.int32)
+    res = OmpResult(_ptr(sup), _ptr(co), _ptr(sz), _ptr(it), _ptr(rn), _ptr(ab), None, None, None)
+    c = _config(cfg)
+    _check(_lib.fmp_large_solve(op.handle, DTYPES[np.dtype(dtype)], _ptr(y), C.byref(c), C.byref(res)))
+    s = int(sz[0])
+    return sup[:s].copy(), co[:s].copy(), int(it[0]), float(rn[0]), bool(ab[0])
+
+
 # --------------------------------------------------- device (torch) variants
 def omp_solve_dev(op: SensingOperator, y, cfg: SolveConfig, out: dict, tolerances=None,
                   stream: Optional[int] = None) -> None:
@@ -552,4 +693,5 @@ __all__ = [
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
     "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
+    "least_squares", "LargeShard", "LocalExchange", "sharded_solve", "large_solve",
 ]

@@ -728,3 +728,374 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
 }
 
 }  // extern "C"
+
+// ===================================================== sharded single signal
+struct fmp_large_s {
+  fmp_op_s* op = nullptr;
+  int dtype = FMP_C64;
+  int P = 1, p = 0;
+  int64_t n = 0, m = 0, np = 0;
+  int T = 1;
+  int64_t fast_until = 0;
+  size_t eb = 8;
+  // device
+  void *h0s = nullptr, *hs = nullptr, *gcm = nullptr, *hfull = nullptr, *xdense = nullptr;
+  void *ax = nullptr, *r = nullptr, *y = nullptr, *xn = nullptr;
+  double2 *W = nullptr, *x = nullptr, *z = nullptr, *l = nullptr;
+  uint32_t* lam = nullptr;
+  double *part = nullptr, *scal = nullptr, *blkmax = nullptr, *dval = nullptr;
+  unsigned long long* dfirst = nullptr;
+  bool own_gcm = false;
+  // host state (mirrors omp_solve's loop variables, solvers.cpp:306-403)
+  int t = 0, s = 0, iters = 0, aborted = 0;
+  double yy = 0, tol = 0, rn = 0;
+  bool rn_explicit = true, done = true;
+  int view = 0;  // 0: h0s (t = 1), 1: hs (fast row), 2: hfull strided (conventional row)
+  std::vector<uint64_t> support;  // 0-based atoms in selection order
+  std::vector<uint8_t> sel;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int lg_alloc(fmp_large_s* lg, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 256));
+  if (e != cudaSuccess) return fail(FMP_ENOMEM, "large solver alloc (%zu bytes): %s", bytes,
+                                    cudaGetErrorString(e));
+  lg->allocs.push_back(*p);
+  return FMP_OK;
+}
+
+cudaStream_t lg_stream(fmp_large_s* lg) { return lg->op->ctx->cur; }
+
+// current correlation view of this shard
+void lg_view(fmp_large_s* lg, const void** base, int64_t* off, int64_t* stride) {
+  if (lg->view == 0) { *base = lg->h0s; *off = 0; *stride = 1; }
+  else if (lg->view == 1) { *base = lg->hs; *off = 0; *stride = 1; }
+  else { *base = lg->hfull; *off = lg->p; *stride = lg->P; }
+}
+
+int lg_local_best(fmp_large_s* lg, double* best) {
+  cudaStream_t st = lg_stream(lg);
+  const void* base;
+  int64_t off, stride;
+  lg_view(lg, &base, &off, &stride);
+  if (lg->view == 1) CU(fmp::lg_launch_reduce_max(lg->blkmax, lg->dval, st));
+  else CU(fmp::lg_launch_max(lg->dtype, base, off, stride, lg->np, lg->blkmax, lg->dval, st));
+  CU(cudaMemcpyAsync(best, lg->dval, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+// explicit residual r = y - Phi_Lambda x (replicated on every shard)
+int lg_residual(fmp_large_s* lg, double* rn) {
+  cudaStream_t st = lg_stream(lg);
+  CU(cudaMemsetAsync(lg->xdense, 0, (size_t)lg->n * lg->eb, st));
+  CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, lg->s, st));
+  if (int e = run_transform(lg->op, lg->dtype, 0, 0, 1, lg->xdense, lg->ax, 1, nullptr, st)) return e;
+  CU(fmp::lg_launch_resid(lg->dtype, lg->y, lg->ax, lg->r, lg->m, lg->part, lg->dval, st));
+  double r2 = 0;
+  CU(cudaMemcpyAsync(&r2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *rn = std::sqrt(r2);
+  return FMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
+                     const fmp_omp_config* cfg, fmp_large* out) {
+  if (!op || !cfg || !out) return fail(FMP_EINVAL, "null argument");
+  if (op->d.kind != fmp::FOURIER)
+    return fail(FMP_EUNSUPPORTED, "the sharded solver is implemented for Fourier operators");
+  if (dtype != FMP_C64 && dtype != FMP_C128) return fail(FMP_EINVAL, "complex dtypes only");
+  if (nshards < 1 || shard >= nshards || (uint64_t)op->d.n % nshards)
+    return fail(FMP_EINVAL, "bad shard %llu of %llu", (unsigned long long)shard,
+                (unsigned long long)nshards);
+  if (cfg->max_iterations < 1) return fail(FMP_EINVAL, "omp_solve: max_iterations must be >= 1");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  fmp_large_s* lg = new fmp_large_s;
+  lg->op = op;
+  lg->dtype = dtype;
+  lg->P = (int)nshards;
+  lg->p = (int)shard;
+  lg->n = op->d.n;
+  lg->m = op->d.m;
+  lg->np = lg->n / lg->P;
+  lg->T = (int)cfg->max_iterations;
+  lg->eb = fmp::elem_bytes(dtype);
+  {
+    fmp_omp_config c = *cfg;
+    lg->fast_until = c.mode == FMP_MODE_CONVENTIONAL ? 0
+                     : c.mode == FMP_MODE_FAST       ? std::numeric_limits<int64_t>::max()
+                     : c.mode == FMP_MODE_ADAPTIVE   ? (int64_t)fmp_crossover_iteration(FMP_FOURIER, (uint64_t)lg->n)
+                     : c.mode == FMP_MODE_GPU        ? (int64_t)fmp_gpu_crossover(FMP_FOURIER, (uint64_t)lg->n)
+                                                     : (int64_t)std::min<uint64_t>(c.fast_until, INT64_MAX);
+  }
+  const size_t eb = lg->eb;
+  const int grid = fmp::lg_grid();
+  int st = FMP_OK;
+  auto A = [&](void** p, size_t b) { if (!st) st = lg_alloc(lg, p, b); };
+  A(&lg->h0s, lg->np * eb);
+  A(&lg->hs, lg->np * eb);
+  A(&lg->hfull, lg->n * eb);
+  A(&lg->xdense, lg->n * eb);
+  A(&lg->ax, lg->m * eb);
+  A(&lg->r, lg->m * eb);
+  A(&lg->y, lg->m * eb);
+  A(&lg->xn, (size_t)lg->T * eb);
+  A((void**)&lg->W, (size_t)lg->T * (lg->T + 1) / 2 * 16);
+  A((void**)&lg->x, (size_t)lg->T * 16);
+  A((void**)&lg->z, (size_t)lg->T * 16);
+  A((void**)&lg->l, (size_t)lg->T * 16);
+  A((void**)&lg->lam, (size_t)lg->T * 4);
+  A((void**)&lg->part, (size_t)std::max(grid, (lg->T + 255) / 256) * 3 * 8);
+  A((void**)&lg->scal, 16 * 8);
+  A((void**)&lg->blkmax, (size_t)grid * 8);
+  A((void**)&lg->dval, 64);
+  A((void**)&lg->dfirst, 64);
+  if (!st && lg->P > 1) {
+    A(&lg->gcm, lg->n * eb);
+    lg->own_gcm = true;
+  }
+  if (st) {
+    fmp_large_destroy(lg);
+    return st;
+  }
+  const void* g = dtype == FMP_C128 ? (const void*)op->d.g64 : (const void*)op->d.g32;
+  if (lg->P > 1) {
+    cudaError_t e = fmp::lg_launch_classmajor(dtype, g, lg->gcm, lg->n, lg->P, ctx->cur);
+    if (e != cudaSuccess) {
+      fmp_large_destroy(lg);
+      return fail(FMP_ECUDA, "class-major kernel: %s", cudaGetErrorString(e));
+    }
+  } else {
+    lg->gcm = const_cast<void*>(g);
+  }
+  *out = lg;
+  return FMP_OK;
+}
+
+int fmp_large_destroy(fmp_large lg) {
+  if (!lg) return FMP_OK;
+  cudaSetDevice(lg->op->ctx->device);
+  cudaStreamSynchronize(lg->op->ctx->cur);
+  for (void* p : lg->allocs) cudaFree(p);
+  delete lg;
+  return FMP_OK;
+}
+
+int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best) {
+  if (!lg || !y || !local_best) return fail(FMP_EINVAL, "null argument");
+  if (!(tol >= 0.0)) return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
+  CU(cudaSetDevice(lg->op->ctx->device));
+  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  cudaStream_t st = lg_stream(lg);
+  CU(cudaMemcpyAsync(lg->y, y, lg->m * lg->eb, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(lg->scal, 0, 16 * 8, st));
+  CU(cudaStreamSynchronize(st));
+  // ||y||^2 (fp64, in the order a single thread would sum)
+  double yy = 0.0;
+  if (lg->dtype == FMP_C128) {
+    const double* v = (const double*)y;
+    for (int64_t i = 0; i < 2 * lg->m; ++i) yy += v[i] * v[i];
+  } else {
+    const float* v = (const float*)y;
+    for (int64_t i = 0; i < 2 * lg->m; ++i) yy += (double)v[i] * v[i];
+  }
+  lg->yy = yy;
+  lg->tol = tol;
+  lg->rn = std::sqrt(yy);
+  lg->rn_explicit = true;
+  lg->t = 0;
+  lg->s = 0;
+  lg->iters = 0;
+  lg->aborted = 0;
+  lg->support.clear();
+  lg->sel.assign((size_t)lg->n, 0);
+  if (lg->rn <= tol) {
+    lg->done = true;
+    *local_best = -1.0;
+    return FMP_OK;
+  }
+  lg->done = false;
+  const double gamma = lg->op->d.kind == fmp::FOURIER ? 0.0 : 0.0;
+  (void)gamma;
+  // scal: [0] gamma = c(1) = M/N, [1] yy, [2] zz
+  std::vector<double> sc(16, 0.0);
+  sc[0] = (double)lg->m / (double)lg->n;
+  sc[1] = yy;
+  CU(cudaMemcpyAsync(lg->scal, sc.data(), 16 * 8, cudaMemcpyHostToDevice, st));
+  // t = 1: h0 = Phi^H y (full transform, this shard's entries kept)
+  if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->y, lg->hfull, 1, nullptr, st)) return e;
+  CU(fmp::lg_launch_take(lg->dtype, lg->hfull, lg->h0s, lg->np, lg->P, lg->p, st));
+  lg->t = 1;
+  lg->view = 0;
+  CU(cudaStreamSynchronize(st));
+  return lg_local_best(lg, local_best);
+}
+
+int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0_at) {
+  if (!lg || !atom || !h0_at) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(lg->op->ctx->device));
+  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  cudaStream_t st = lg_stream(lg);
+  const double cut = global_best * (1.0 - 1e-9);  // kTieBandRel, solvers.cpp:40
+  const void* base;
+  int64_t off, stride;
+  lg_view(lg, &base, &off, &stride);
+  CU(cudaMemsetAsync(lg->dfirst, 0xff, 8, st));
+  CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, lg->dfirst, st));
+  unsigned long long kp = 0;
+  CU(cudaMemcpyAsync(&kp, lg->dfirst, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (kp == ~0ull) {
+    *atom = 0;
+    h0_at[0] = h0_at[1] = 0.0;
+    return FMP_OK;
+  }
+  *atom = (uint64_t)lg->p + (uint64_t)lg->P * kp + 1;
+  if (lg->dtype == FMP_C128) {
+    CU(cudaMemcpy(h0_at, (const char*)lg->h0s + kp * 16, 16, cudaMemcpyDeviceToHost));
+  } else {
+    float v[2];
+    CU(cudaMemcpy(v, (const char*)lg->h0s + kp * 8, 8, cudaMemcpyDeviceToHost));
+    h0_at[0] = v[0];
+    h0_at[1] = v[1];
+  }
+  return FMP_OK;
+}
+
+int fmp_large_stop(fmp_large lg) {
+  if (!lg) return fail(FMP_EINVAL, "null argument");
+  if (lg->done) return FMP_OK;
+  lg->done = true;
+  CU(cudaSetDevice(lg->op->ctx->device));
+  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  if (!lg->rn_explicit) {
+    if (int e = lg_residual(lg, &lg->rn)) return e;
+    lg->rn_explicit = true;
+  }
+  return FMP_OK;
+}
+
+int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* done,
+                      double* local_best) {
+  if (!lg || !h0_at || !done || !local_best) return fail(FMP_EINVAL, "null argument");
+  if (lg->done) {
+    *done = 1;
+    return FMP_OK;
+  }
+  if (atom < 1 || atom > (uint64_t)lg->n) return fail(FMP_EINVAL, "atom out of range");
+  const uint64_t pick = atom - 1;
+  if (lg->sel[pick]) {  // stagnation guard (solvers.cpp:365-367)
+    *done = 1;
+    return fmp_large_stop(lg);
+  }
+  CU(cudaSetDevice(lg->op->ctx->device));
+  cudaStream_t st = lg_stream(lg);
+  {
+    std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+    // least squares (replicated)
+    CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
+                         lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
+    double sc[3];
+    CU(cudaMemcpyAsync(sc, lg->scal + 2, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(sc + 1, lg->scal + 6, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (sc[1] != 0.0) {  // rank deficient: keep the previous state (solvers.cpp:380-385)
+      lg->aborted = 1;
+      lg->done = true;
+      *done = 1;
+      if (!lg->rn_explicit) {
+        if (int e = lg_residual(lg, &lg->rn)) return e;
+        lg->rn_explicit = true;
+      }
+      return FMP_OK;
+    }
+    lg->s += 1;
+    lg->support.push_back(pick);
+    lg->sel[pick] = 1;
+    lg->iters = lg->t;
+    const double zz = sc[0];
+    // residual and halting (solvers.cpp:388-402)
+    const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
+    const double r2id = lg->yy - zz;
+    const double margin = lg->dtype == FMP_C128 ? 1e-10 : 1e-5;
+    const bool near = !(r2id > lg->tol * lg->tol + margin * lg->yy);
+    if (next_conv || near) {
+      if (int e = lg_residual(lg, &lg->rn)) return e;
+      lg->rn_explicit = true;
+    } else {
+      lg->rn = std::sqrt(std::max(r2id, 0.0));
+      lg->rn_explicit = false;
+    }
+    if ((lg->rn_explicit && lg->rn <= lg->tol) || lg->t >= lg->T) {
+      lg->done = true;
+      *done = 1;
+      if (!lg->rn_explicit) {
+        if (int e = lg_residual(lg, &lg->rn)) return e;
+        lg->rn_explicit = true;
+      }
+      return FMP_OK;
+    }
+    // next correlation
+    lg->t += 1;
+    if ((int64_t)lg->t <= lg->fast_until) {
+      const void* xn = lg->xn;
+      CU(fmp::lg_launch_fast(lg->dtype, lg->h0s, lg->hs, lg->gcm, lg->np, lg->P, lg->p, lg->n,
+                             lg->lam, xn, lg->s, lg->blkmax, st));
+      lg->view = 1;
+    } else {
+      if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->r, lg->hfull, 1, nullptr, st)) return e;
+      lg->view = 2;
+    }
+  }
+  *done = 0;
+  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  return lg_local_best(lg, local_best);
+}
+
+int fmp_large_result(fmp_large lg, uint64_t* support, double* coeffs, uint64_t* support_size,
+                     uint64_t* iterations, double* residual, int32_t* aborted) {
+  if (!lg) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(lg->op->ctx->device));
+  if (support)
+    for (size_t j = 0; j < lg->support.size(); ++j) support[j] = lg->support[j] + 1;
+  if (coeffs && lg->s) CU(cudaMemcpy(coeffs, lg->x, (size_t)lg->s * 16, cudaMemcpyDeviceToHost));
+  if (support_size) *support_size = (uint64_t)lg->s;
+  if (iterations) *iterations = (uint64_t)lg->iters;
+  if (residual) *residual = lg->rn;
+  if (aborted) *aborted = lg->aborted;
+  return FMP_OK;
+}
+
+int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* cfg,
+                    fmp_omp_result* out) {
+  if (!op || !y || !cfg || !out) return fail(FMP_EINVAL, "null argument");
+  fmp_large lg = nullptr;
+  if (int e = fmp_large_create(op, dtype, 0, 1, cfg, &lg)) return e;
+  double best = 0.0;
+  int st = fmp_large_begin(lg, y, cfg->tolerances ? cfg->tolerances[0] : cfg->tolerance, &best);
+  int done = best < 0.0;
+  while (!st && !done) {
+    if (best == 0.0) {  // nothing left to select (solvers.cpp:363)
+      st = fmp_large_stop(lg);
+      break;
+    }
+    uint64_t atom = 0;
+    double h0[2];
+    if ((st = fmp_large_first(lg, best, &atom, h0))) break;
+    st = fmp_large_advance(lg, atom, h0, &done, &best);
+  }
+  if (!st)
+    st = fmp_large_result(lg, out->support, out->coeffs, out->support_size, out->iterations,
+                          out->residual, out->aborted);
+  fmp_large_destroy(lg);
+  return st;
+}
+
+}  // extern "C"

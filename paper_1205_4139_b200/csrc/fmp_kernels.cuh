@@ -113,6 +113,27 @@ int64_t transform_max_n(int dtype);
 cudaError_t launch_least_squares(const DevOp& op, int dtype, const void* y, const uint32_t* sup,
                                  int s, int64_t batch, double2* x, int64_t* bad, double2* L,
                                  int grid, cudaStream_t st);
+// sharded single-signal solver kernels (fmp_large.cu)
+int lg_grid();
+cudaError_t lg_launch_fast(int dtype, const void* h0s, void* hs, const void* gcm, int64_t np, int P,
+                           int p, int64_t n, const uint32_t* lam, const void* xn, int s,
+                           double* blkmax, cudaStream_t st);
+cudaError_t lg_launch_max(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
+                          double* blkmax, double* out, cudaStream_t st);
+cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st);
+cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
+                            double cut, unsigned long long* first, cudaStream_t st);
+cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, double2* z, double2* l,
+                         uint32_t* lam, void* xn, double* part, double* scal, int T, int s,
+                         unsigned pick, double2 bnew, cudaStream_t st);
+cudaError_t lg_launch_scatter_x(int dtype, void* out, const uint32_t* lam, const double2* x, int s,
+                                cudaStream_t st);
+cudaError_t lg_launch_resid(int dtype, const void* y, const void* ax, void* r, int64_t m,
+                            double* part, double* out, cudaStream_t st);
+cudaError_t lg_launch_take(int dtype, const void* src, void* dst, int64_t np, int P, int p,
+                           cudaStream_t st);
+cudaError_t lg_launch_classmajor(int dtype, const void* g, void* gcm, int64_t n, int P,
+                                 cudaStream_t st);
 // FMA-pipe throughput (FMAs per second) measured by a calibration kernel
 cudaError_t fma_peak(int is_double, double* fma_per_s);
 // number of kernel launches issued by the last launch_* call on this thread

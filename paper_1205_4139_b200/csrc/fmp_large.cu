@@ -1,0 +1,394 @@
+// Kernels of the sharded single-signal solver (config 5: one N = 2^24 signal
+// over the whole GPU, or P GPUs).  Shard p of P owns the correlation entries
+// k = p + P k' (cyclic), so that
+//   * the fast update of a shard reads the kernel class c = (p - lambda) mod P,
+//     stored class-major (gcm[c][j'] = c[c + P j']), contiguously, and
+//   * the band argmax reduces per shard to (best |h|^2) and (first index in
+//     the band), exchanged between shards (solvers.cpp:90-101).
+// Least squares is replicated on every shard with deterministic reductions,
+// so all shards hold bit-identical coefficients.
+#include "fmp_kcommon.cuh"
+
+namespace fmp {
+namespace {
+
+constexpr int LG_THREADS = 256;
+constexpr int LG_RPT = 4;
+constexpr int LG_CHUNK = 1024;
+
+// h[k'] = h0[k'] - sum_tau x_tau c[(p + P k' - lambda_tau) mod N] over this
+// shard; per-CTA max |h|^2 into blkmax
+template <class V>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_fast(const V* __restrict__ h0s, V* __restrict__ hs,
+                                                        const V* __restrict__ gcm, int64_t np, int P,
+                                                        int p, int64_t n, const uint32_t* __restrict__ lam,
+                                                        const V* __restrict__ xn, int s,
+                                                        double* __restrict__ blkmax) {
+  __shared__ unsigned s_lam[LG_CHUNK];
+  __shared__ V s_x[LG_CHUNK];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tile = (int64_t)32 * LG_RPT;
+  const int64_t ntiles = (np + tile - 1) / tile;
+  const int nwarps = LG_THREADS / 32;
+  double best = 0.0;
+  for (int64_t tb = (int64_t)blockIdx.x * nwarps; tb < ntiles; tb += (int64_t)gridDim.x * nwarps) {
+    const int64_t t0 = tb + warp;
+    const int64_t k0 = t0 * tile;
+    V acc[LG_RPT];
+#pragma unroll
+    for (int r = 0; r < LG_RPT; ++r) {
+      const int64_t k = k0 + lane + 32 * r;
+      acc[r] = (t0 < ntiles && k < np) ? h0s[k] : zero_of(V{});
+    }
+    for (int c0 = 0; c0 < s; c0 += LG_CHUNK) {
+      const int cn = min(LG_CHUNK, s - c0);
+      __syncthreads();
+      for (int j = tid; j < cn; j += LG_THREADS) {
+        s_lam[j] = lam[c0 + j];
+        s_x[j] = xn[c0 + j];
+      }
+      __syncthreads();
+      if (t0 < ntiles) {
+        for (int tau = 0; tau < cn; ++tau) {
+          const int64_t d = ((int64_t)p + n - (int64_t)s_lam[tau]) % n;  // (p - lambda) mod N
+          const int64_t cls = d % P, off = d / P;
+          const V* g = gcm + cls * np;
+          const V x = s_x[tau];
+          int64_t j = k0 + lane + off;
+          if (j >= np) j -= np;
+#pragma unroll
+          for (int r = 0; r < LG_RPT; ++r) {
+            int64_t jj = j + 32 * r;
+            if (jj >= np) jj -= np;
+            msub(acc[r], x, __ldg(g + jj));
+          }
+        }
+      }
+    }
+    if (t0 < ntiles) {
+#pragma unroll
+      for (int r = 0; r < LG_RPT; ++r) {
+        const int64_t k = k0 + lane + 32 * r;
+        if (k < np) {
+          hs[k] = acc[r];
+          best = fmax(best, mag2(acc[r]));
+        }
+      }
+    }
+  }
+  best = block_max(best, red);
+  if (tid == 0) blkmax[blockIdx.x] = best;
+}
+
+// per-CTA max |v|^2 of a strided view v[k'] = base[off + stride k'], k' < cnt
+template <class V>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_max(const V* __restrict__ base, int64_t off,
+                                                       int64_t stride, int64_t cnt,
+                                                       double* __restrict__ blkmax) {
+  __shared__ double red[32];
+  double best = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += (int64_t)gridDim.x * blockDim.x)
+    best = fmax(best, mag2(base[off + stride * k]));
+  best = block_max(best, red);
+  if (threadIdx.x == 0) blkmax[blockIdx.x] = best;
+}
+
+__global__ void k_lg_reduce_max(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+  __shared__ double red[32];
+  double b = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) b = fmax(b, part[i]);
+  b = block_max(b, red);
+  if (threadIdx.x == 0) *out = b;
+}
+
+// smallest shard position k' with |v|^2 >= cut (atomicMin over the grid)
+template <class V>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_first(const V* __restrict__ base, int64_t off,
+                                                         int64_t stride, int64_t cnt, double cut,
+                                                         unsigned long long* __restrict__ first) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (mag2(base[off + stride * k]) >= cut) {
+      atomicMin(first, (unsigned long long)k);
+      break;  // later k of this thread are larger
+    }
+  }
+}
+
+// ---- replicated least squares (same arithmetic as k_omp, deterministic)
+struct LgLs {
+  double2* W;        // column-major packed, capacity T
+  double2* x;        // T
+  double2* z;        // T
+  double2* l;        // T
+  uint32_t* lam;     // T, 0-based atoms
+  void* xn;          // T (data dtype): -x for the fast update
+  double* part;      // block partials (3 per block)
+  double* scal;      // [0] gamma [1] yy [2] zz [3] d [4] znew.x [5] znew.y [6] aborted
+  int T;
+};
+
+__device__ __forceinline__ int lg_wofs(int T, int i, int j) {
+  return j * T - (j * (j - 1)) / 2 + (i - j);
+}
+
+template <bool HAD>
+__device__ __forceinline__ double2 lg_gram(const DevOp& op, unsigned a, unsigned b) {
+  if constexpr (HAD) return make_double2(op.gr64[a ^ b], 0.0);
+  else return op.g64[(a - b) & (unsigned)(op.n - 1)];
+}
+
+// l = W a (a_j = G(lambda_j, pick)), per-block partials of |l|^2 and l^H z
+template <bool HAD>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_ls_a(DevOp op, LgLs L, int s, unsigned pick) {
+  __shared__ double red[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double ll = 0.0, lzr = 0.0, lzi = 0.0;
+  if (i < s) {
+    double ar = 0.0, ai = 0.0;
+    for (int j = 0; j <= i; ++j) {
+      const double2 w = L.W[lg_wofs(L.T, i, j)], v = lg_gram<HAD>(op, L.lam[j], pick);
+      ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
+      ai = fma(w.x, v.y, fma(w.y, v.x, ai));
+    }
+    L.l[i] = make_double2(ar, ai);
+    const double2 zc = L.z[i];
+    ll = ar * ar + ai * ai;
+    lzr = ar * zc.x + ai * zc.y;
+    lzi = ar * zc.y - ai * zc.x;
+  }
+  ll = block_sum(ll, red);
+  lzr = block_sum(lzr, red);
+  lzi = block_sum(lzi, red);
+  if (threadIdx.x == 0) {
+    L.part[3 * blockIdx.x] = ll;
+    L.part[3 * blockIdx.x + 1] = lzr;
+    L.part[3 * blockIdx.x + 2] = lzi;
+  }
+}
+
+// d, z_s (single thread, fixed order: identical on every shard)
+__global__ void k_lg_ls_b(LgLs L, int nblk, double2 bnew) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double ll = 0.0, lzr = 0.0, lzi = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    ll += L.part[3 * b];
+    lzr += L.part[3 * b + 1];
+    lzi += L.part[3 * b + 2];
+  }
+  const double gamma = L.scal[0];
+  const double d2 = gamma - ll;
+  if (!(d2 > 1e-12 * gamma)) {  // solvers.cpp:32,144
+    L.scal[6] = 1.0;
+    return;
+  }
+  const double d = sqrt(d2);
+  L.scal[3] = d;
+  L.scal[4] = (bnew.x - lzr) / d;
+  L.scal[5] = (bnew.y - lzi) / d;
+  L.scal[6] = 0.0;
+}
+
+// new row of W and x = W^H z, one warp per column; appends the atom
+template <class V>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_ls_c(LgLs L, int s, unsigned pick, double xscale) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (L.scal[6] != 0.0) return;
+  const double d = L.scal[3];
+  const double2 znew = make_double2(L.scal[4], L.scal[5]);
+  V* xn = reinterpret_cast<V*>(L.xn);
+  if (j < s) {
+    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+    for (int i = j + lane; i < s; i += 32) {
+      const double2 l = L.l[i], w = L.W[lg_wofs(L.T, i, j)], zc = L.z[i];
+      ar += l.x * w.x + l.y * w.y;
+      ai += l.x * w.y - l.y * w.x;
+      br += w.x * zc.x + w.y * zc.y;
+      bi += w.x * zc.y - w.y * zc.x;
+    }
+    ar = warp_sum(ar);
+    ai = warp_sum(ai);
+    br = warp_sum(br);
+    bi = warp_sum(bi);
+    if (lane == 0) {
+      const double2 wn = make_double2(-ar / d, -ai / d);
+      L.W[lg_wofs(L.T, s, j)] = wn;
+      const double xr = br + wn.x * znew.x + wn.y * znew.y;
+      const double xi = bi + wn.x * znew.y - wn.y * znew.x;
+      L.x[j] = make_double2(xr, xi);
+      from_c128(make_double2(xr * xscale, xi * xscale), xn[j]);
+    }
+  } else if (j == s && lane == 0) {
+    L.W[lg_wofs(L.T, s, s)] = make_double2(1.0 / d, 0.0);
+    L.z[s] = znew;
+    L.lam[s] = pick;
+    const double2 xs = make_double2(znew.x / d, znew.y / d);
+    L.x[s] = xs;
+    from_c128(make_double2(xs.x * xscale, xs.y * xscale), xn[s]);
+    L.scal[2] += znew.x * znew.x + znew.y * znew.y;  // zz
+  }
+}
+
+// dense sparse-estimate vector for the forward transform: out[lambda_j] = x_j
+template <class V>
+__global__ void k_lg_scatter_x(V* __restrict__ out, const uint32_t* __restrict__ lam,
+                               const double2* __restrict__ x, int s) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < s) from_c128(x[j], out[lam[j]]);
+}
+
+// r = y - Phi x (Phi x given at the rows), per-block partial ||r||^2
+template <class V>
+__global__ void __launch_bounds__(LG_THREADS) k_lg_resid(const V* __restrict__ y,
+                                                         const V* __restrict__ ax, V* __restrict__ r,
+                                                         int64_t m, double* __restrict__ part) {
+  __shared__ double red[32];
+  double r2 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const V v = sub(y[i], ax[i]);
+    r[i] = v;
+    r2 += mag2(v);
+  }
+  r2 = block_sum(r2, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = r2;
+}
+
+__global__ void k_lg_sum(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < cnt; ++i) s += part[i];  // fixed order
+  *out = s;
+}
+
+// shard view of a full vector: dst[k'] = src[p + P k']
+template <class V>
+__global__ void k_lg_take(const V* __restrict__ src, V* __restrict__ dst, int64_t np, int P, int p) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < np;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = src[p + (int64_t)P * k];
+}
+
+// class-major kernel: gcm[c][j'] = c[c + P j']
+template <class V>
+__global__ void k_lg_classmajor(const V* __restrict__ g, V* __restrict__ gcm, int64_t n, int P) {
+  const int64_t np = n / P;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / np, j = i - c * np;
+    gcm[i] = g[c + (int64_t)P * j];
+  }
+}
+
+}  // namespace
+
+int lg_grid() { return num_sms() * 4; }
+
+cudaError_t lg_launch_fast(int dtype, const void* h0s, void* hs, const void* gcm, int64_t np, int P,
+                           int p, int64_t n, const uint32_t* lam, const void* xn, int s,
+                           double* blkmax, cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128)
+    k_lg_fast<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)h0s, (double2*)hs, (const double2*)gcm,
+                                                    np, P, p, n, lam, (const double2*)xn, s, blkmax);
+  else
+    k_lg_fast<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)h0s, (float2*)hs, (const float2*)gcm,
+                                                   np, P, p, n, lam, (const float2*)xn, s, blkmax);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_max(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
+                          double* blkmax, double* out, cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128)
+    k_lg_max<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)base, off, stride, cnt, blkmax);
+  else
+    k_lg_max<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)base, off, stride, cnt, blkmax);
+  k_lg_reduce_max<<<1, 1024, 0, st>>>(blkmax, grid, out);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st) {
+  k_lg_reduce_max<<<1, 1024, 0, st>>>(blkmax, lg_grid(), out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
+                            double cut, unsigned long long* first, cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128)
+    k_lg_first<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)base, off, stride, cnt, cut, first);
+  else
+    k_lg_first<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)base, off, stride, cnt, cut, first);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, double2* z, double2* l,
+                         uint32_t* lam, void* xn, double* part, double* scal, int T, int s,
+                         unsigned pick, double2 bnew, cudaStream_t st) {
+  LgLs L{W, x, z, l, lam, xn, part, scal, T};
+  const int nblk = std::max(1, (s + LG_THREADS - 1) / LG_THREADS);
+  if (op.kind == HADAMARD) k_lg_ls_a<true><<<nblk, LG_THREADS, 0, st>>>(op, L, s, pick);
+  else k_lg_ls_a<false><<<nblk, LG_THREADS, 0, st>>>(op, L, s, pick);
+  k_lg_ls_b<<<1, 32, 0, st>>>(L, nblk, bnew);
+  const int warps = s + 1, cblk = (warps * 32 + LG_THREADS - 1) / LG_THREADS;
+  const double xscale = op.kind == HADAMARD ? -1.0 / (double)op.n : -1.0;
+  if (dtype == C128) k_lg_ls_c<double2><<<cblk, LG_THREADS, 0, st>>>(L, s, pick, xscale);
+  else k_lg_ls_c<float2><<<cblk, LG_THREADS, 0, st>>>(L, s, pick, xscale);
+  g_launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_scatter_x(int dtype, void* out, const uint32_t* lam, const double2* x, int s,
+                                cudaStream_t st) {
+  const int blocks = std::max(1, (s + 255) / 256);
+  if (dtype == C128) k_lg_scatter_x<double2><<<blocks, 256, 0, st>>>((double2*)out, lam, x, s);
+  else k_lg_scatter_x<float2><<<blocks, 256, 0, st>>>((float2*)out, lam, x, s);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_resid(int dtype, const void* y, const void* ax, void* r, int64_t m,
+                            double* part, double* out, cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128)
+    k_lg_resid<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)y, (const double2*)ax, (double2*)r, m, part);
+  else
+    k_lg_resid<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)y, (const float2*)ax, (float2*)r, m, part);
+  k_lg_sum<<<1, 32, 0, st>>>(part, grid, out);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_sum(const double* part, int cnt, double* out, cudaStream_t st) {
+  k_lg_sum<<<1, 32, 0, st>>>(part, cnt, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_take(int dtype, const void* src, void* dst, int64_t np, int P, int p,
+                           cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128) k_lg_take<double2><<<grid, 256, 0, st>>>((const double2*)src, (double2*)dst, np, P, p);
+  else k_lg_take<float2><<<grid, 256, 0, st>>>((const float2*)src, (float2*)dst, np, P, p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_classmajor(int dtype, const void* g, void* gcm, int64_t n, int P,
+                                 cudaStream_t st) {
+  const int grid = lg_grid();
+  if (dtype == C128) k_lg_classmajor<double2><<<grid, 256, 0, st>>>((const double2*)g, (double2*)gcm, n, P);
+  else k_lg_classmajor<float2><<<grid, 256, 0, st>>>((const float2*)g, (float2*)gcm, n, P);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace fmp
