@@ -168,6 +168,12 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch,
 int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
                       const fmp_omp_config* cfg, fmp_omp_result* out, void* stream);
 
+/* profiling aid: when enabled, each fused solve accumulates SM cycles per
+ * phase (conventional correlation, fast correlation, identification, least
+ * squares, residual, other), summed over CTAs, readable afterwards */
+int fmp_set_phase_profiling(int enabled);
+int fmp_phase_cycles(fmp_ctx ctx, double* out6);
+
 /* ------------------------------------------- sharded single-signal solver */
 /* omp_solve for ONE large signal spread over `nshards` GPUs (config 5).
  * Shard p owns the correlation entries k = p + nshards * k' (1-based atom

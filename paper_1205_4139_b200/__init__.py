@@ -76,6 +76,8 @@ class OmpResult(C.Structure):
 _sig("fmp_version", C.c_int)
 _sig("fmp_fma_peak", C.c_int, _vp, C.c_int, C.POINTER(C.c_double))
 _sig("fmp_last_error", C.c_char_p)
+_sig("fmp_set_phase_profiling", C.c_int, C.c_int)
+_sig("fmp_phase_cycles", C.c_int, _vp, _vp)
 _sig("fmp_last_launch_count", C.c_int)
 _sig("fmp_ctx_create", C.c_int, C.c_int, C.POINTER(_vp))
 _sig("fmp_ctx_destroy", C.c_int, _vp)
@@ -142,6 +144,10 @@ def _check(status: int) -> None:
     raise cls(status, msg)
 
 
+def set_phase_profiling(enabled: bool) -> None:
+    _check(_lib.fmp_set_phase_profiling(int(enabled)))
+
+
 def last_launch_count() -> int:
     return int(_lib.fmp_last_launch_count())
 
@@ -188,6 +194,12 @@ class Context:
         v = C.c_double(0)
         _check(_lib.fmp_fma_peak(self.handle, int(double), C.byref(v)))
         return v.value
+
+    def phase_cycles(self) -> dict:
+        """Per-phase SM cycles of the last fused solve (fmp_set_phase_profiling(1))."""
+        v = np.zeros(6)
+        _check(_lib.fmp_phase_cycles(self.handle, _ptr(v)))
+        return dict(zip(["conventional", "fast", "identify", "least_squares", "residual", "other"], v))
 
     def close(self) -> None:
         if getattr(self, "handle", None):

@@ -22,6 +22,7 @@ using fmp::DevOp;
 namespace {
 
 thread_local std::string g_err;
+int g_phase_prof = 0;
 thread_local int g_launch_count = 0;
 
 int fail(int code, const char* fmt, ...) {
@@ -72,7 +73,7 @@ struct Workspace {
 };
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
-            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF };
+            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH };
 
 }  // namespace
 
@@ -146,6 +147,24 @@ int copy_in(fmp_ctx_s* ctx, int slot, const void* host, size_t bytes, void** dev
 extern "C" {
 
 int fmp_version(void) { return 1; }
+
+int fmp_set_phase_profiling(int enabled) {
+  g_phase_prof = enabled;
+  return FMP_OK;
+}
+
+int fmp_phase_cycles(fmp_ctx ctx, double* out6) {
+  if (!ctx || !out6) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(ctx->device));
+  cudaError_t e = cudaSuccess;
+  void* ph = ctx->ws.get(S_PH, 64, &e);
+  if (!ph) return fail(FMP_ENOMEM, "phase buffer");
+  unsigned long long v[6];
+  CU(cudaStreamSynchronize(ctx->cur));
+  CU(cudaMemcpy(v, ph, sizeof(v), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 6; ++i) out6[i] = (double)v[i];
+  return FMP_OK;
+}
 
 int fmp_fma_peak(fmp_ctx ctx, int is_double, double* out) {
   if (!ctx || !out) return fail(FMP_EINVAL, "null argument");
@@ -647,6 +666,12 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   ALLOC(q, S_Q, 64);
   a.queue = q;
   CU(cudaMemsetAsync(q, 0, 4, st));
+  if (g_phase_prof) {
+    unsigned long long* ph;
+    ALLOC(ph, S_PH, 64);
+    CU(cudaMemsetAsync(ph, 0, 64, st));
+    a.phase_ws = ph;
+  }
   cudaError_t e = fmp::launch_omp(a, st);
   g_launch_count = fmp::last_launch_count();
   if (e == cudaErrorInvalidConfiguration)

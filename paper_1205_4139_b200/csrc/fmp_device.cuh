@@ -276,14 +276,31 @@ __device__ __forceinline__ void transform_pass(V* buf, int log2n, int logS, cons
 // Whole in-place transform of one vector held by the calling block, radix
 // RMAX passes then one smaller remainder pass; padding period RMAX.
 // Ends with a __syncthreads().
+// pass 0 of a transform whose input is produced on the fly: LOAD(slot)
+// returns the input element at (unpadded) slot, so the buffer needs no
+// zero-fill or scatter beforehand
+template <int R, int LOGP, bool INV, bool HAD, class V, class LOAD>
+__device__ __forceinline__ void first_pass_loaded(V* buf, int log2n, const LOAD& load, int tid,
+                                                  int nth) {
+  const int nsub = 1 << (log2n - log2_of<R>::v);
+  for (int u = tid; u < nsub; u += nth) {
+    V v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = load(u * R + j);
+    if constexpr (HAD) wht_reg<R>(v);
+    else dft_reg<R, INV>(v);
+#pragma unroll
+    for (int j = 0; j < R; ++j) buf[padx<LOGP>(u * R + j)] = v[j];
+  }
+}
+
 // log2tab: size of the twiddle table (defaults to the vector); a block that
 // runs the first stages of a longer transform passes the full length.
 template <int RMAX, bool INV, bool HAD, class V, class TW>
 __device__ void block_transform(V* buf, int log2n, const TW& tw, int tid, int nth,
-                                int log2tab = -1) {
+                                int log2tab = -1, int s = 0) {
   constexpr int LOGP = log2_of<RMAX>::v;
   if (log2tab < 0) log2tab = log2n;
-  int s = 0;
   for (; log2n - s >= LOGP; s += LOGP) {
     transform_pass<RMAX, LOGP, INV, HAD>(buf, log2n, s, tw, tid, nth, log2tab);
     __syncthreads();

@@ -94,6 +94,7 @@ struct OmpArgs {
   void* buf_ws;             // grid x (n + n/8) (data dtype): transform buffer when n exceeds smem
   int* queue;               // work counter (zeroed before launch)
   int grid;
+  unsigned long long* phase_ws;  // optional per-phase cycle totals (6)
 };
 
 // launchers (return cudaError_t); all async on `stream`

@@ -28,6 +28,7 @@ namespace {
 
 constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
 constexpr int OLOGP = 3;
+constexpr int LSG = 8;  // threads per row / column in the least-squares passes
 
 struct OmpK {
   DevOp op;
@@ -52,10 +53,11 @@ struct OmpK {
   int* queue;
   // shared-memory plan
   void* buf_ws;  // grid x (n + n/8) when the buffer lives in global memory
-  int r_smem, w_smem;
-  int off_g, off_r, off_w, off_tw, off_small;
+  int r_smem, w_smem, map_smem;
+  int off_g, off_r, off_w, off_tw, off_small, off_map;
   int tw_a;       // two-level twiddle split
   double margin;  // relative slack on the residual identity
+  unsigned long long* phase_ws;  // optional: cycles per phase (conv, fast, argmax, ls, resid, other)
 };
 
 template <bool HAD>
@@ -127,6 +129,17 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   unsigned* s_lam = reinterpret_cast<unsigned*>(p); p += ((4 * (size_t)T + 15) / 16) * 16;
   unsigned* s_sel = reinterpret_cast<unsigned*>(p);  // n bits: atoms selected so far
 
+  // slot -> row map of the Omega scatter (-1: zero slot), so the adjoint's
+  // first pass reads r directly
+  int16_t* s_map = a.map_smem ? reinterpret_cast<int16_t*>(sm + a.off_map) : nullptr;
+  // slot -> support position of the sparse estimate (forward transform input)
+  int16_t* s_xmap = a.map_smem ? s_map + ((n + 7) / 8) * 8 : nullptr;
+  if (s_map) {
+    for (int i = tid; i < n; i += nth) s_map[i] = -1;
+    __syncthreads();
+    for (int j = tid; j < m; j += nth)
+      s_map[HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n)] = (int16_t)j;
+  }
   V* h0w = reinterpret_cast<V*>(a.h0_ws) + (size_t)blockIdx.x * n;
   double* msc = a.mag_ws + (size_t)blockIdx.x * n;  // used only when a warp owns > 1 tile
   const double gamma = HAD ? op.gr64[0] : op.g64[0].x;  // c(1) = M/N
@@ -147,6 +160,18 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
   const bool regs_only = ntiles > 0 && ntiles <= nw;  // every thread owns <= 1 tile
 
+  // opt-in phase profile (thread 0's clock between phase boundaries, which
+  // all end in a block-wide barrier)
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long ph_last = clock64();
+  auto mark = [&](int phase) {
+    if (a.phase_ws && tid == 0) {
+      const unsigned long long now = clock64();
+      ph[phase] += now - ph_last;
+      ph_last = now;
+    }
+  };
+
   for (;;) {
     __syncthreads();
     if (tid == 0) s_prob = atomicAdd(a.queue, 1);
@@ -157,6 +182,8 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
     const double tol = a.tol[prob];
 
     for (int i = tid; i < (n + 31) / 32; i += nth) s_sel[i] = 0u;
+    if (s_xmap)
+      for (int i = tid; i < n; i += nth) s_xmap[i] = -1;
     double yy = 0.0;
     for (int j = tid; j < m; j += nth) yy += mag2(y[j]);
     yy = block_sum(yy, red);
@@ -169,15 +196,30 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
     // explicit residual r = y - Phi_Lambda x by one forward transform of the
     // sparse estimate (replaces update_residual, solvers.cpp:180-192)
     auto residual_explicit = [&](int cnt) -> double {
-      for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
-      __syncthreads();
-      for (int j = tid; j < cnt; j += nth) {
-        V xv;
-        from_c128(s_x[j], xv);
-        buf[padx<OLOGP>(HAD ? (int)s_lam[j] : (int)brev_n(s_lam[j], log2n))] = xv;
+      if (s_xmap && log2n >= OLOGP) {
+        __syncthreads();
+        first_pass_loaded<ORMAX, OLOGP, false, HAD>(
+            buf, log2n,
+            [&](int slot) {
+              const int q = s_xmap[slot];
+              V xv = zv;
+              if (q >= 0) from_c128(s_x[q], xv);
+              return xv;
+            },
+            tid, nth);
+        __syncthreads();
+        block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth, -1, OLOGP);
+      } else {
+        for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
+        __syncthreads();
+        for (int j = tid; j < cnt; j += nth) {
+          V xv;
+          from_c128(s_x[j], xv);
+          buf[padx<OLOGP>(HAD ? (int)s_lam[j] : (int)brev_n(s_lam[j], log2n))] = xv;
+        }
+        __syncthreads();
+        block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth);
       }
-      __syncthreads();
-      block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth);
       double r2 = 0.0;
       for (int j = tid; j < m; j += nth) {
         const V rv = sub(y[j], scale(buf[padx<OLOGP>((int)op.omega[j])], sc));
@@ -199,15 +241,25 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
                          : nullptr;
         double best = 0.0;
         double m2[RPT];
+        mark(5);
         if (!fast_row) {
           // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
           const V* r = t == 1 ? y : rs;
-          for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
-          __syncthreads();
-          for (int j = tid; j < m; j += nth)
-            buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
-          __syncthreads();
-          block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
+          if (s_map && log2n >= OLOGP) {
+            __syncthreads();  // buf may still be read (previous argmax / h0)
+            first_pass_loaded<ORMAX, OLOGP, true, HAD>(
+                buf, log2n, [&](int slot) { const int q = s_map[slot]; return q >= 0 ? r[q] : zv; },
+                tid, nth);
+            __syncthreads();
+            block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth, -1, OLOGP);
+          } else {
+            for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
+            __syncthreads();
+            for (int j = tid; j < m; j += nth)
+              buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
+            __syncthreads();
+            block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
+          }
           if (t == 1) {
             // h0 = Phi^H y stays in buf (scaled, padded) for the fast rows
             for (int i = tid; i < nbuf; i += nth) buf[i] = scale(buf[i], sc);
@@ -262,6 +314,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         }
         // identification with the tie band (solvers.cpp:90-101, :362-367)
         best = block_max(best, red);
+        mark(fast_row ? 1 : 0);
         if (best == 0.0) break;
         const double cut = best * (1.0 - kTieBandRel);
         unsigned first = 0xffffffffu;
@@ -280,54 +333,86 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         const unsigned pick = block_min_u(first, redu);
         // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
         if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
+        // b_s = h0[pick], read early so its latency hides behind the row pass
+        const V bpre = buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick];
+        mark(2);
 
         // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H).
-        // l = W a with a_j = G(lambda_j, pick) looked up in c; thread i owns row i
-        for (int i = tid; i < s; i += nth) {
-          double ar = 0.0, ai = 0.0;
-          for (int j = 0; j <= i; ++j) {
-            const double2 w = W[wofs(T, i, j)], v = gram_of(s_lam[j], pick);
-            ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
-            ai = fma(w.x, v.y, fma(w.y, v.x, ai));
-          }
-          s_l[i] = make_double2(ar, ai);
-        }
+        // l = W a with a_j = G(lambda_j, pick) looked up in c.  Eight threads
+        // per row (lane group q = tid % 8 sums j = q, q+8, ...), reduced with
+        // three shuffles, so all 512 threads share the O(s^2) work; the same
+        // pass accumulates |l|^2 and l^H z into per-warp partials
         double ll = 0.0, lzr = 0.0, lzi = 0.0;
-        for (int i = tid; i < s; i += nth) {
-          const double2 l = s_l[i], zc = s_z[i];
-          ll += l.x * l.x + l.y * l.y;
-          lzr += l.x * zc.x + l.y * zc.y;  // conj(l) z
-          lzi += l.x * zc.y - l.y * zc.x;
+        for (int base = 0; base < s; base += nth / LSG) {
+          const int i = base + tid / LSG, q = tid % LSG;
+          double ar = 0.0, ai = 0.0;
+          if (i < s)
+            for (int j = q; j <= i; j += LSG) {
+              const double2 w = W[wofs(T, i, j)], v = gram_of(s_lam[j], pick);
+              ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
+              ai = fma(w.x, v.y, fma(w.y, v.x, ai));
+            }
+#pragma unroll
+          for (int o = LSG / 2; o; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+          }
+          if (i < s && q == 0) {
+            s_l[i] = make_double2(ar, ai);
+            const double2 zc = s_z[i];
+            ll += ar * ar + ai * ai;
+            lzr += ar * zc.x + ai * zc.y;  // conj(l) z
+            lzi += ar * zc.y - ai * zc.x;
+          }
         }
-        block_sum3(ll, lzr, lzi, red);  // also publishes s_l
+        ll = warp_sum(ll);
+        lzr = warp_sum(lzr);
+        lzi = warp_sum(lzi);
+        if (lane == 0) {
+          red[warp] = ll;
+          red[32 + warp] = lzr;
+          red[64 + warp] = lzi;
+        }
+        __syncthreads();  // publishes s_l and the partials
+        ll = lzr = lzi = 0.0;
+        for (int w = 0; w < nw; ++w) {  // fixed order: every thread the same value
+          ll += red[w];
+          lzr += red[32 + w];
+          lzi += red[64 + w];
+        }
         const double d2 = gamma - ll;
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
         if (!(d2 > 1e-12 * gamma)) { aborted = 1; break; }
         const double d = sqrt(d2);
-        const double2 bnew = to_c128(buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
+        const double2 bnew = to_c128(bpre);
         const double2 znew = make_double2((bnew.x - lzr) / d, (bnew.y - lzi) / d);
-        // one pass per column j < s (a warp each) yields both the new row of W,
-        // W_sj = -(1/d) sum_{i=j}^{s-1} conj(l_i) W_ij, and the coefficient
-        // x_j = sum_{i=j}^{s-1} conj(W_ij) z_i + conj(W_sj) z_s   (x = W^H z)
-        for (int j = warp; j < s; j += nw) {
-          double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-          for (int i = j + lane; i < s; i += 32) {
-            const double2 l = s_l[i], w = W[wofs(T, i, j)], zc = s_z[i];
-            ar += l.x * w.x + l.y * w.y;  // conj(l) w
-            ai += l.x * w.y - l.y * w.x;
-            br += w.x * zc.x + w.y * zc.y;  // conj(w) z
-            bi += w.x * zc.y - w.y * zc.x;
+        // new row of W, one pass per column j < s (eight threads each; column
+        // j of the packed W is contiguous): W_sj = -(1/d) sum_{i=j}^{s-1}
+        // conj(l_i) W_ij.  Older rows never change, so x = W^H z only gains
+        // the new term: x_j += conj(W_sj) z_s
+        for (int base = 0; base < s; base += nth / LSG) {
+          const int j = base + tid / LSG, q = tid % LSG;
+          double ar = 0.0, ai = 0.0;
+          if (j < s) {
+            const double2* Wc = W + wofs(T, j, j);
+            for (int i = j + q; i < s; i += LSG) {
+              const double2 l = s_l[i], w = Wc[i - j];
+              ar = fma(l.x, w.x, fma(l.y, w.y, ar));  // conj(l) w
+              ai = fma(l.x, w.y, fma(-l.y, w.x, ai));
+            }
           }
-          ar = warp_sum(ar);
-          ai = warp_sum(ai);
-          br = warp_sum(br);
-          bi = warp_sum(bi);
-          if (lane == 0) {
+#pragma unroll
+          for (int o = LSG / 2; o; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+          }
+          if (j < s && q == 0) {
             const double2 wn = make_double2(-ar / d, -ai / d);
             W[wofs(T, s, j)] = wn;
-            const double xr = br + wn.x * znew.x + wn.y * znew.y;
-            const double xi = bi + wn.x * znew.y - wn.y * znew.x;
+            const double2 xo = s_x[j];
+            const double xr = xo.x + wn.x * znew.x + wn.y * znew.y;
+            const double xi = xo.y + wn.x * znew.y - wn.y * znew.x;
             s_x[j] = make_double2(xr, xi);
             from_c128(make_double2(xr * xscale, xi * xscale), s_xn[j]);
           }
@@ -337,6 +422,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           s_z[s] = znew;
           s_lam[s] = pick;
           s_sel[pick >> 5] |= 1u << (pick & 31);
+          if (s_xmap) s_xmap[HAD ? (int)pick : (int)brev_n(pick, log2n)] = (int16_t)s;
           const double2 xs = make_double2(znew.x / d, znew.y / d);
           s_x[s] = xs;
           from_c128(make_double2(xs.x * xscale, xs.y * xscale), s_xn[s]);
@@ -345,6 +431,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         ++s;
         __syncthreads();
         iters = t;
+        mark(3);
 
         // ---- residual and halting (solvers.cpp:388-402)
         const bool next_conv = t < T && !((int64_t)(t + 1) <= a.fast_until);
@@ -357,9 +444,11 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           rn = sqrt(fmax(r2id, 0.0));
           rn_explicit = false;
         }
+        mark(4);
         if (rn_explicit && rn <= tol) break;
       }
       if (!rn_explicit) rn = residual_explicit(s);
+      mark(4);
     }
     // ---- results (RecoveryResult, solvers.hpp:53-64)
     uint64_t* sup = a.support + prob * T;
@@ -376,13 +465,15 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
       if (a.hlen) a.hlen[prob] = (uint64_t)tlast;
     }
   }
+  if (a.phase_ws && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(a.phase_ws + i, ph[i]);
 }
 
 struct OmpPlan {
   size_t total;
   int gmode;
-  bool rsm, wsm, bufg;
-  int off_g, off_r, off_w, off_tw, off_small, tw_a;
+  bool rsm, wsm, bufg, msm;
+  int off_g, off_r, off_w, off_tw, off_small, off_map, tw_a;
 };
 
 template <class V, bool HAD>
@@ -415,12 +506,16 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   }
   p.rsm = tot + r <= cap;
   if (p.rsm) tot += r;
+  const size_t mapb = 2 * al((size_t)((n + 7) / 8) * 8 * 2);  // row map + support map
+  p.msm = !p.bufg && m <= 32767 && T <= 32767 && tot + mapb <= cap;
+  if (p.msm) tot += mapb;
   p.total = tot;
   size_t off = p.bufg ? 0 : buf;
   p.off_tw = (int)off; off += tw;
   p.off_w = (int)off; if (p.wsm) off += w;
   p.off_g = (int)off; off += p.gmode == 1 ? gfull : (p.gmode == 2 ? ghalf : 0);
   p.off_r = (int)off; if (p.rsm) off += r;
+  p.off_map = (int)off; if (p.msm) off += mapb;
   p.off_small = (int)off;
   return p;
 }
@@ -467,6 +562,8 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.queue = a.queue;
   k.r_smem = p.rsm;
   k.w_smem = p.wsm;
+  k.map_smem = p.msm;
+  k.off_map = p.off_map;
   k.buf_ws = a.buf_ws;
   if (p.bufg && !a.buf_ws) return cudaErrorInvalidValue;
   k.off_g = p.off_g;
@@ -476,6 +573,7 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.off_small = p.off_small;
   k.tw_a = p.tw_a;
   k.margin = is_double(a.dtype) ? 1e-10 : 1e-5;
+  k.phase_ws = a.phase_ws;
   const int grid = std::max(1, a.grid);
   if (p.bufg) launch_g<V, HAD, RPT, true>(k, p.gmode, grid, p.total, st);
   else launch_g<V, HAD, RPT, false>(k, p.gmode, grid, p.total, st);
