@@ -197,6 +197,10 @@ __host__ __device__ constexpr int brev_small(int j) {
   return r;
 }
 
+// j with brev_small<R>(j) == q (bit reversal is an involution)
+template <int R>
+__host__ __device__ constexpr int brev_inv(int q) { return brev_small<R>(q); }
+
 template <int R> struct log2_of { static constexpr int v = R <= 1 ? 0 : 1 + log2_of<R / 2>::v; };
 template <> struct log2_of<1> { static constexpr int v = 0; };
 
@@ -241,14 +245,27 @@ __device__ __forceinline__ void pass_one(V* buf, int log2n, int logS, int log2ta
       // twiddle index brev(j) * o * 2^log2tab / (R S)
       const int step = o << (log2tab - logS - LOGR);
       if constexpr (TW::kPowers) {
-        V w[R];
-        w[1] = tw(step);
-        if (INV) w[1].y = -w[1].y;
+        // powers w^q applied as they are formed; only w, w^2, w^4, w^8 stay
+        // live (register pressure at 64 registers per thread)
+        V w1 = tw(step);
+        if (INV) w1.y = -w1.y;
+        V p2 = w1, p4 = w1, p8 = w1;
 #pragma unroll
-        for (int q = 2; q < R; ++q)
-          w[q] = (q & 1) ? cmul(w[q - 1], w[1]) : cmul(w[q / 2], w[q / 2]);
-#pragma unroll
-        for (int j = 1; j < R; ++j) v[j] = cmul(v[j], w[brev_small<R>(j)]);
+        for (int q = 1; q < R; ++q) {
+          V wq;
+          if (q == 1) wq = w1;
+          else if (q == 2) wq = p2 = cmul(w1, w1);
+          else if (q == 4) wq = p4 = cmul(p2, p2);
+          else if (q == 8) wq = p8 = cmul(p4, p4);
+          else {
+            wq = (q & 8) ? p8 : ((q & 4) ? p4 : p2);
+            const int rest = q & ((q & 8) ? 7 : ((q & 4) ? 3 : 1));
+            if (rest & 4) wq = cmul(wq, p4);
+            if (rest & 2) wq = cmul(wq, p2);
+            if (rest & 1) wq = cmul(wq, w1);
+          }
+          v[brev_inv<R>(q)] = cmul(v[brev_inv<R>(q)], wq);
+        }
       } else {
 #pragma unroll
         for (int j = 1; j < R; ++j) {

@@ -58,7 +58,10 @@ template <> __device__ __forceinline__ const float* fourier_table<float>(const D
 
 constexpr int RMAX = 16;
 constexpr int LOGP = 4;
-constexpr int OMP_THREADS = 512;
+#ifndef FMP_OMP_THREADS
+#define FMP_OMP_THREADS 512
+#endif
+constexpr int OMP_THREADS = FMP_OMP_THREADS;
 constexpr int FU_THREADS = 512;
 
 __device__ __forceinline__ double inv_sqrt_n(int n) { return 1.0 / sqrt((double)n); }

@@ -583,7 +583,10 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
 
 template <class V, bool HAD>
 cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
-  if (a.op->n >= 32 * 8 * 16) return launch_omp_t<V, HAD, 8>(a, st);
+  // lanes own RPT outputs; pick RPT so that one tile per warp covers n
+  constexpr int NW = OMP_THREADS / 32;
+  if (a.op->n >= 32 * 8 * NW && OMP_THREADS <= 512) return launch_omp_t<V, HAD, 8>(a, st);
+  if (a.op->n >= 32 * 4 * NW) return launch_omp_t<V, HAD, 4>(a, st);
   return launch_omp_t<V, HAD, 2>(a, st);
 }
 
