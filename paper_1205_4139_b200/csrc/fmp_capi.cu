@@ -73,7 +73,7 @@ struct Workspace {
 };
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
-            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH };
+            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC };
 
 }  // namespace
 
@@ -130,6 +130,9 @@ int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_om
     void* w;
     ALLOC(w, S_WORK, (size_t)batch * op->d.n * fmp::elem_bytes(dtype));
     a.work = w;
+    int* sy;
+    ALLOC(sy, S_SYNC, (32 + batch) * sizeof(int));
+    a.sync = sy;
   }
   CU(fmp::launch_transform(a, st));
   g_launch_count = fmp::last_launch_count();
@@ -286,12 +289,20 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
     spos[i] = slots[i].first;
     srow[i] = slots[i].second;
   }
+  // scatter offsets per 256 slots (large-n transform blocks start on them)
+  const uint64_t noff = n / 256 + 1;
+  std::vector<uint32_t> soff(noff, 0);
+  for (uint64_t i = 0, k = 0; i < noff; ++i) {
+    while (k < m && spos[k] < i * 256) ++k;
+    soff[i] = (uint32_t)k;
+  }
   cudaError_t e = cudaSuccess;
 #define OPALLOC(p, bytes) \
   if ((e = cudaMalloc(&p, (bytes))) != cudaSuccess) return cleanup(fail(FMP_ENOMEM, "operator alloc: %s", cudaGetErrorString(e)))
   OPALLOC(d.omega, m * 4);
   OPALLOC(d.scat_pos, m * 4);
   OPALLOC(d.scat_row, m * 4);
+  OPALLOC(d.scat_off, noff * 4);
   OPALLOC(d.g64, n * 16);
   if (kind == FMP_FOURIER) {
     OPALLOC(d.tw64, n * 16);
@@ -306,7 +317,8 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   int launches = 0;
   if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(d.scat_pos, spos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d.scat_row, srow.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      (e = cudaMemcpyAsync(d.scat_row, srow.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d.scat_off, soff.data(), noff * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return cleanup(fail(FMP_ECUDA, "omega copy: %s", cudaGetErrorString(e)));
   if (kind == FMP_FOURIER) {
     if ((e = fmp::launch_twiddles(d, st)) != cudaSuccess)
@@ -339,7 +351,7 @@ int fmp_operator_destroy(fmp_op op) {
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->cur);
   DevOp& d = op->d;
-  for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
+  for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.scat_off, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
                   (void*)d.gr64, (void*)d.glat})
     if (p) cudaFree(p);
   delete op;

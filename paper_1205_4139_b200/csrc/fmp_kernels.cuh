@@ -32,6 +32,7 @@ struct DevOp {
   // Hadamard): the large-n transform's blocks find their rows by bisection
   uint32_t* scat_pos = nullptr;  // m, ascending slots
   uint32_t* scat_row = nullptr;  // m, index into the m-vector for each slot
+  uint32_t* scat_off = nullptr;  // n/256 + 1: number of slots below 256 i (n >= 256)
 };
 
 struct TransformArgs {
@@ -45,6 +46,7 @@ struct TransformArgs {
   int64_t batch;
   uint64_t* argmax_out;  // optional: band argmax of |out|^2 per vector (dense out only)
   void* work;            // batch x n scratch, required when n > transform_max_n(dtype)
+  int* sync;             // 32 + batch ints of scratch (job-queue path), optional
 };
 
 struct FastUpdateArgs {

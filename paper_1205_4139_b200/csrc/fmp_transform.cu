@@ -199,13 +199,9 @@ __global__ void __launch_bounds__(256) k_transform_cluster(DevOp op, const V* __
   const int lo_slot = (int)c * B;
   // this block's Omega rows: bisection in the slot-sorted scatter
   int k0 = 0, k1 = 0;
-  if (in_omega) {
-    int lo = 0, hi = m;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)op.scat_pos[mid] < lo_slot) lo = mid + 1; else hi = mid; }
-    k0 = lo;
-    hi = m;
-    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)op.scat_pos[mid] < lo_slot + B) lo = mid + 1; else hi = mid; }
-    k1 = lo;
+  if (in_omega) {  // B is a multiple of 256
+    k0 = (int)op.scat_off[lo_slot >> 8];
+    k1 = (int)op.scat_off[(lo_slot + B) >> 8];
   }
   for (int64_t b = cid; b < batch; b += ncl) {
     V* vec = dst + b * n;
@@ -249,6 +245,147 @@ __global__ void __launch_bounds__(256) k_transform_cluster(DevOp op, const V* __
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------- job-queue large-n transform
+// Same two-phase factorisation as the cluster path, but scheduled as a queue
+// of jobs over a persistent grid: job A(b, c) transforms block c of vector b in
+// smem and publishes it (release); job B(b, c) waits for vector b's K A-jobs
+// (acquire) and finishes offsets [c B/K, (c+1) B/K) in registers.  Jobs are
+// issued in vector order with B(b, .) lagging A(b, .) by D vectors, so a
+// B-job's inputs are normally complete (and L2-resident) when it starts and no
+// CTA ever idles at a barrier.  A-jobs never wait, and every job is claimed by
+// a running CTA, so the waits cannot deadlock.
+template <class V, bool INV, bool HAD, int K>
+__global__ void __launch_bounds__(256, 3) k_transform_queue(DevOp op, const V* __restrict__ in,
+                                                         V* dst, int64_t batch, int in_omega,
+                                                         int* __restrict__ counter,
+                                                         int* __restrict__ done, int lag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_job;
+  V* buf = reinterpret_cast<V*>(smem_raw);
+  constexpr int LOGK = log2_of<K>::v;
+  const int log2n = op.log2n, n = (int)op.n, m = (int)op.m;
+  const int log2b = log2n - LOGK, B = 1 << log2b;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const V* tw = twiddles<V>(op);
+  const double sc = 1.0 / sqrt((double)n);
+  const V z = zero_of(V{});
+  // job j -> step i = j / (2K); within a step: K A-jobs of vector i, then K
+  // B-jobs of vector i - lag
+  const int64_t steps = batch + lag;
+  const int64_t njobs = steps * 2 * K;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_job = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t j = s_job;
+    if (j >= njobs) break;
+    const int64_t step = j / (2 * K);
+    const int r = (int)(j - step * 2 * K);
+    const bool isA = r < K;
+    const int c = isA ? r : r - K;
+    const int64_t b = isA ? step : step - lag;
+    if (b < 0 || b >= batch) continue;
+    V* vec = dst + b * (int64_t)n;
+    if (isA) {
+      const int lo_slot = c * B;
+      if (in_omega) {
+        for (int i = tid; i < B + (B >> LOGP); i += nth) buf[i] = z;
+        // this block's rows in the slot-sorted scatter (B is a multiple of 256)
+        const int k0 = (int)op.scat_off[lo_slot >> 8], k1 = (int)op.scat_off[(lo_slot + B) >> 8];
+        __syncthreads();
+        const V* rr = in + b * m;
+        for (int k = k0 + tid; k < k1; k += nth)
+          buf[padx<LOGP>((int)op.scat_pos[k] - lo_slot)] = rr[op.scat_row[k]];
+      } else {
+        const V* v = in + b * n;
+        for (int i = tid; i < B; i += nth) {
+          const unsigned p = (unsigned)(lo_slot + i);
+          buf[padx<LOGP>(i)] = v[HAD ? p : brev_n(p, log2n)];
+        }
+      }
+      __syncthreads();
+      block_transform<RMAX, INV, HAD>(buf, log2b, TwTable<V>{tw}, tid, nth, log2n);
+      for (int i = tid; i < B; i += nth) __stcg(vec + lo_slot + i, buf[padx<LOGP>(i)]);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(done + b, 1);
+      }
+    } else {
+      if (tid == 0) {
+        while (atomicAdd(done + b, 0) < K) __nanosleep(64);
+        __threadfence();
+      }
+      __syncthreads();
+      const int o0 = c * (B / K);
+      for (int o = o0 + tid; o < o0 + B / K; o += nth) {
+        V v[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) v[q] = __ldcg(vec + o + q * B);
+        if constexpr (HAD) {
+          wht_reg<K>(v);
+        } else {
+#pragma unroll
+          for (int q = 1; q < K; ++q) {
+            V w = tw[brev_small<K>(q) * o];
+            if (INV) w.y = -w.y;
+            v[q] = cmul(v[q], w);
+          }
+          dft_reg<K, INV>(v);
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) __stcg(vec + o + q * B, scale(v[q], sc));
+      }
+    }
+  }
+}
+
+template <class V, bool INV, bool HAD, int K>
+cudaError_t launch_tr_queue_k(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  const int64_t B = op.n / K;
+  const size_t smem = (size_t)(B + (B >> LOGP)) * sizeof(V);
+  auto kern = k_transform_queue<V, INV, HAD, K>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  V* dst = a.out_omega ? (V*)a.work : (V*)a.out;
+  if (!dst) dst = (V*)a.work;
+  if (!dst || !a.sync) return cudaErrorInvalidValue;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  const int grid = std::max(1, occ) * num_sms();
+  // lag in vectors: enough jobs in flight that a vector's A-jobs are done
+  // when its B-jobs are claimed
+  const int lag = std::max(1, (2 * grid) / (2 * K) + 1);
+  int* counter = a.sync;
+  int* done = a.sync + 32;
+  cudaError_t e = cudaMemsetAsync(a.sync, 0, (size_t)(32 + a.batch) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, 256, smem, st>>>(op, (const V*)a.in, dst, a.batch, a.in_omega, counter, done, lag);
+  ++g_launches;
+  const int g2 = num_sms() * 8;
+  if (a.out_omega) {
+    k_out<V><<<g2, 256, 0, st>>>(dst, (V*)a.out, a.batch, 1, op.omega, op.m, op.log2n, 1);
+    ++g_launches;
+  }
+  if (a.argmax_out && !a.out_omega) {
+    const int g3 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+    k_argmax<V><<<g3, 512, 0, st>>>(dst, op.n, a.batch, a.argmax_out);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+template <class V, bool INV, bool HAD>
+cudaError_t launch_tr_queue(const TransformArgs& a, cudaStream_t st, int k) {
+  switch (k) {
+    case 2: return launch_tr_queue_k<V, INV, HAD, 2>(a, st);
+    case 4: return launch_tr_queue_k<V, INV, HAD, 4>(a, st);
+    case 8: return launch_tr_queue_k<V, INV, HAD, 8>(a, st);
+    case 16: return launch_tr_queue_k<V, INV, HAD, 16>(a, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <class V, bool INV, bool HAD, int K>
@@ -361,6 +498,9 @@ template <class V, bool HAD>
 cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
   if (a.op->n > transform_max_n(a.dtype)) {
     const int k = a.op->scat_pos ? cluster_k<V>(a.op->n, a.dtype) : 0;
+    if (k && a.sync)
+      return a.inverse ? launch_tr_queue<V, true, HAD>(a, st, k)
+                       : launch_tr_queue<V, false, HAD>(a, st, k);
     if (k)
       return a.inverse ? launch_tr_cluster<V, true, HAD>(a, st, k)
                        : launch_tr_cluster<V, false, HAD>(a, st, k);
