@@ -442,6 +442,17 @@ int cluster_k(int64_t n, int dtype) {
   return (int)k;
 }
 
+// block size for the job-queue path (three CTAs per SM): 64 KB blocks, 32 KB
+// for 4-byte elements (measured on config 3)
+template <class V>
+int queue_k(int64_t n, int dtype) {
+  const int64_t target = sizeof(V) <= 4 ? 32 * 1024 : 64 * 1024;
+  int64_t k = 2;
+  while (k <= 16 && (n / k) * (int64_t)sizeof(V) > target) k *= 2;
+  if (k > 16 || n / k > transform_max_n(dtype)) return 0;
+  return (int)k;
+}
+
 template <class V, bool INV, bool HAD>
 cudaError_t launch_tr_cluster(const TransformArgs& a, cudaStream_t st, int k) {
   switch (k) {
@@ -498,6 +509,10 @@ template <class V, bool HAD>
 cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
   if (a.op->n > transform_max_n(a.dtype)) {
     const int k = a.op->scat_pos ? cluster_k<V>(a.op->n, a.dtype) : 0;
+    const int kq = a.op->scat_pos ? queue_k<V>(a.op->n, a.dtype) : 0;
+    if (kq && a.sync)
+      return a.inverse ? launch_tr_queue<V, true, HAD>(a, st, kq)
+                       : launch_tr_queue<V, false, HAD>(a, st, kq);
     if (k && a.sync)
       return a.inverse ? launch_tr_queue<V, true, HAD>(a, st, k)
                        : launch_tr_queue<V, false, HAD>(a, st, k);
