@@ -168,6 +168,29 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch,
 int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
                       const fmp_omp_config* cfg, fmp_omp_result* out, void* stream);
 
+/* ------------------------------------------------------- CoSaMP (batched) */
+/* cosamp_solve (solvers.hpp:73-78, solvers.cpp:413-544) with sparsity k over
+ * `batch` measurement vectors.  cfg as for OMP: max_iterations, tolerance(s),
+ * record_correlations; mode CONVENTIONAL / FAST / ADAPTIVE (the reference's
+ * adaptive_cosamp_uses_fast, cost_model.cpp:91-96; GPU and CUSTOM behave as
+ * FAST).  Supports come out ascending like the reference's.  Merge, band
+ * selection and pruning follow select_largest (solvers.cpp:62-86) exactly;
+ * least squares is the normal-equations Cholesky in fp64. */
+typedef struct {
+  uint64_t* support;          /* batch x k, ascending 1-based atoms, 0 padded */
+  double* coeffs;             /* batch x k complex (fp64) */
+  uint64_t* support_size;     /* batch */
+  uint64_t* iterations;       /* batch */
+  double* residual;           /* batch */
+  int32_t* aborted;           /* batch: rank_deficient_abort */
+  uint64_t* support_history;  /* optional batch x max_iterations x k (0 padded) */
+  void* history;              /* optional batch x max_iterations x n (dtype) */
+} fmp_cosamp_result;
+int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
+                     const fmp_omp_config* cfg, fmp_cosamp_result* out);
+int fmp_cosamp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
+                         const fmp_omp_config* cfg, fmp_cosamp_result* out, void* stream);
+
 /* profiling aid: when enabled, each fused solve accumulates SM cycles per
  * phase (conventional correlation, fast correlation, identification, least
  * squares, residual, other), summed over CTAs, readable afterwards */

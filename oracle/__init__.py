@@ -136,6 +136,8 @@ class Oracle:
                                            C.c_uint64, C.POINTER(SolveConfig), C.c_int,
                                            u64p, f64p, u64p, f64p,
                                            np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]
+        L.fmpo_cosamp_solve.argtypes = [C.c_int, C.c_uint64, u64p, C.c_uint64, f64p, C.c_uint64,
+                                        C.POINTER(SolveConfig), C.POINTER(SolveResult), u64p]
         L.fmpo_impl.restype = C.c_char_p
 
     # -- helpers ------------------------------------------------------------
@@ -288,6 +290,37 @@ class Oracle:
         return Recovery(sup[:s].copy(), co.view(np.complex128)[:s].copy(), int(res.iterations_run),
                         float(res.residual_norm), bool(res.rank_deficient_abort), H,
                         [int(v) for v in modes[: res.history_len if record else T]])
+
+    def cosamp_solve(self, kind: str, n: int, omega, y, k: int, max_iterations: int, tol: float,
+                     mode="conventional", symmetry=False, record=False):
+        """solvers.cpp:413-544.  Returns (Recovery, support_history list of arrays)."""
+        omega = _u(omega)
+        T, K = int(max_iterations), int(k)
+        cfg = SolveConfig(T, tol, MODE[mode], 1, int(symmetry), int(record))
+        sup = np.zeros(max(K, 1), np.uint64)
+        co = np.zeros(2 * max(K, 1))
+        hist = np.zeros(2 * n * T) if record else None
+        sh = np.zeros(T * max(K, 1), np.uint64)
+        modes = np.zeros(T, np.int32)
+        res = SolveResult()
+        res.support = sup.ctypes.data_as(C.POINTER(C.c_uint64))
+        res.coeffs = co.ctypes.data_as(C.POINTER(C.c_double))
+        res.correlation_history = (hist.ctypes.data_as(C.POINTER(C.c_double))
+                                   if record else C.POINTER(C.c_double)())
+        res.mode_used = modes.ctypes.data_as(C.POINTER(C.c_int))
+        self._check(self.lib.fmpo_cosamp_solve(KIND[kind], n, omega, len(omega), _c(y), K,
+                                               C.byref(cfg), C.byref(res), sh))
+        s, it = res.support_size, int(res.iterations_run)
+        H = []
+        if record:
+            hv = hist.view(np.complex128).reshape(T, n)
+            H = [hv[i].copy() for i in range(res.history_len)]
+        shv = sh.reshape(T, max(K, 1))
+        SH = [row[row > 0].copy() for row in shv[:it]]
+        rec = Recovery(sup[:s].copy(), co.view(np.complex128)[:s].copy(), it,
+                       float(res.residual_norm), bool(res.rank_deficient_abort), H,
+                       [int(v) for v in modes[: res.history_len if record else it]])
+        return rec, SH
 
     def omp_solve_batch(self, kind: str, n: int, omega, Y, max_iterations: int, tol: float,
                         mode="fast", threads=0):

@@ -890,6 +890,147 @@ int fmpo_omp_solve(int kind, uint64_t n, const uint64_t* omega, uint64_t m,
   return st;
 }
 
+/* solvers.cpp:62-86: the `count` largest values of m[0..n): positions above
+ * the band around the rank-`count` boundary, then the smallest positions
+ * inside the band; writes `count` positions (first the sure ones, then the
+ * tied ones, each in index order) */
+static int cmp_desc_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x < y) - (x > y);
+}
+static void select_largest(const double* m, uint64_t n, uint64_t count, uint64_t* out) {
+  if (count >= n) {
+    for (uint64_t j = 0; j < n; ++j) out[j] = j;
+    return;
+  }
+  double* sorted = (double*)malloc(sizeof(double) * n);
+  memcpy(sorted, m, sizeof(double) * n);
+  qsort(sorted, n, sizeof(double), cmp_desc_double);
+  const double boundary = sorted[count - 1];
+  free(sorted);
+  const double hi = boundary * (1.0 + kTieBandRel);
+  const double lo = boundary * (1.0 - kTieBandRel);
+  uint64_t o = 0;
+  for (uint64_t j = 0; j < n; ++j)
+    if (m[j] > hi) out[o++] = j;
+  for (uint64_t j = 0; j < n && o < count; ++j)
+    if (m[j] <= hi && m[j] >= lo) out[o++] = j;
+}
+
+static int cmp_u64_asc(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* cost_model.cpp:76-96 */
+static int adaptive_cosamp_uses_fast(int kind, uint64_t n, uint64_t k) {
+  if (k == 0) return 1;
+  return (kind == 0 ? 6 : 2) * n * k <= conventional_flops(kind, n);
+}
+
+/* solvers.cpp:413-544.  out->support / coeffs need k entries; support_history
+ * (max_iterations x k, zero padded) may be NULL. */
+int fmpo_cosamp_solve(int kind, uint64_t n, const uint64_t* omega, uint64_t m,
+                      const double* y_in, uint64_t k, const fmpo_solve_config* cfg,
+                      fmpo_solve_result* out, uint64_t* support_history) {
+  if (validate_selection(n, omega, m)) return 1;
+  if (cfg->max_iterations < 1 || !(cfg->residual_tolerance >= 0.0)) return 1;
+  const cx* y = (const cx*)y_in;
+  const uint64_t T = cfg->max_iterations;
+  out->support_size = 0;
+  out->iterations_run = 0;
+  out->rank_deficient_abort = 0;
+  out->history_len = 0;
+  cx* r = (cx*)malloc(sizeof(cx) * m);
+  memcpy(r, y, sizeof(cx) * m);
+  double rn = l2_norm(r, m);
+  out->residual_norm = rn;
+  if (k == 0 || rn <= cfg->residual_tolerance) {
+    free(r);
+    return 0;
+  }
+  const int fast = cfg->mode == 1 || (cfg->mode == 2 && adaptive_cosamp_uses_fast(kind, n, k));
+  const uint64_t count = 2 * k < n ? 2 * k : n;
+  kernel_t ker;
+  int have_kernel = 0, st = 0;
+  cx* h = (cx*)malloc(sizeof(cx) * n);
+  cx* h0 = (cx*)malloc(sizeof(cx) * n);
+  double* mg = (double*)malloc(sizeof(double) * (n > 3 * k ? n : 3 * k));
+  uint64_t* pos = (uint64_t*)malloc(sizeof(uint64_t) * (n > 3 * k ? n : 3 * k));
+  uint64_t* merged = (uint64_t*)malloc(sizeof(uint64_t) * 3 * k);
+  cx* cols = (cx*)malloc(sizeof(cx) * m * 3 * k);
+  cx* b = (cx*)malloc(sizeof(cx) * 3 * k);
+  uint64_t* sup = out->support;
+  cx* coeffs = (cx*)out->coeffs;
+  uint64_t s = 0;
+
+  for (uint64_t t = 1; t <= T; ++t) {
+    if (out->mode_used) out->mode_used[t - 1] = fast;
+    if (t == 1) {
+      op_apply_adjoint(kind, n, omega, m, r, h);
+      if (fast) memcpy(h0, h, sizeof(cx) * n);
+    } else if (fast) {
+      if (!have_kernel) {
+        st = compute_kernel(kind, n, omega, m, &ker);
+        if (st) break;
+        have_kernel = 1;
+      }
+      fast_update(&ker, h0, sup, coeffs, s, cfg->fourier_symmetry, h);
+    } else {
+      op_apply_adjoint(kind, n, omega, m, r, h);
+    }
+    if (cfg->record_correlations && out->correlation_history) {
+      memcpy(out->correlation_history + 2 * n * out->history_len, h, sizeof(cx) * n);
+      out->history_len++;
+    }
+    /* top_atoms (solvers.cpp:105-118), then the sorted union with the support */
+    for (uint64_t j = 0; j < n; ++j) mg[j] = cx_mag2(h[j]);
+    select_largest(mg, n, count, pos);
+    for (uint64_t j = 0; j < count; ++j) pos[j] += 1;
+    qsort(pos, count, sizeof(uint64_t), cmp_u64_asc);
+    uint64_t ns = 0, i = 0, j = 0;
+    while (i < s || j < count) {
+      if (j >= count || (i < s && sup[i] < pos[j])) merged[ns++] = sup[i++];
+      else if (i >= s || pos[j] < sup[i]) merged[ns++] = pos[j++];
+      else { merged[ns++] = sup[i++]; ++j; }
+    }
+    for (uint64_t q = 0; q < ns; ++q) op_column(kind, n, omega, m, merged[q], cols + q * m);
+    if (normal_equations(cols, ns, m, y, b)) {
+      out->rank_deficient_abort = 1;
+      break;
+    }
+    /* prune to the k strongest (merged is ascending: band ties -> smallest atom) */
+    for (uint64_t q = 0; q < ns; ++q) mg[q] = cx_mag2(b[q]);
+    const uint64_t keep = k < ns ? k : ns;
+    select_largest(mg, ns, keep, pos);
+    qsort(pos, keep, sizeof(uint64_t), cmp_u64_asc); /* atom order == position order */
+    s = keep;
+    for (uint64_t q = 0; q < keep; ++q) {
+      sup[q] = merged[pos[q]];
+      coeffs[q] = b[pos[q]];
+      op_column(kind, n, omega, m, sup[q], cols + q * m);
+    }
+    update_residual(cols, coeffs, s, m, y, r);
+    rn = l2_norm(r, m);
+    if (support_history)
+      for (uint64_t q = 0; q < k; ++q) support_history[(t - 1) * k + q] = q < s ? sup[q] : 0;
+    out->iterations_run = t;
+    out->residual_norm = rn;
+    if (rn <= cfg->residual_tolerance) break;
+  }
+  out->support_size = s;
+  if (have_kernel) kernel_free(&ker);
+  free(r);
+  free(h);
+  free(h0);
+  free(mg);
+  free(pos);
+  free(merged);
+  free(cols);
+  free(b);
+  return st;
+}
+
 /* batched driver: one solve per host thread, like fastmp_cli.cpp:273-303 */
 typedef struct {
   int kind;

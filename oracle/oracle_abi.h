@@ -113,6 +113,14 @@ int fmpo_omp_solve_batch(int kind, uint64_t n, const uint64_t* omega,
                          uint64_t* iterations, double* residual,
                          int* aborted);
 
+/* CoSaMP with sparsity k (solvers.hpp:73-78, solvers.cpp:413-544); mode as
+ * for OMP (0 conventional, 1 fast, 2 adaptive = adaptive_cosamp_uses_fast).
+ * out->support / out->coeffs hold k entries (ascending atoms);
+ * support_history (max_iterations x k, zero padded) may be NULL. */
+int fmpo_cosamp_solve(int kind, uint64_t n, const uint64_t* omega, uint64_t m,
+                      const double* y, uint64_t k, const fmpo_solve_config* cfg,
+                      fmpo_solve_result* out, uint64_t* support_history);
+
 /* which implementation this library is: "restatement" or "reference" */
 const char* fmpo_impl(void);
 

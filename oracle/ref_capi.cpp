@@ -258,6 +258,35 @@ int fmpo_omp_solve(int kind, uint64_t n, const uint64_t* omega, uint64_t m,
   });
 }
 
+int fmpo_cosamp_solve(int kind, uint64_t n, const uint64_t* omega, uint64_t m,
+                      const double* y, uint64_t k, const fmpo_solve_config* c,
+                      fmpo_solve_result* out, uint64_t* support_history) {
+  return guard([&] {
+    const SensingOperator op = make_op(kind, n, omega, m);
+    const RecoveryResult res = cosamp_solve(op, load(y, m), k, config_of(c));
+    out->support_size = res.support.size();
+    std::copy(res.support.begin(), res.support.end(), out->support);
+    store(res.coeffs, out->coeffs);
+    out->iterations_run = res.iterations_run;
+    out->residual_norm = res.residual_norm;
+    out->rank_deficient_abort = res.rank_deficient_abort ? 1 : 0;
+    out->history_len = res.correlation_history.size();
+    if (out->correlation_history)
+      for (std::size_t i = 0; i < res.correlation_history.size(); ++i)
+        store(res.correlation_history[i], out->correlation_history + 2 * n * i);
+    if (out->mode_used)
+      for (std::size_t i = 0; i < res.costs.iterations.size(); ++i)
+        out->mode_used[i] =
+            res.costs.iterations[i].mode_used == CorrelationMode::Fast ? 1 : 0;
+    if (support_history)
+      for (std::size_t i = 0; i < res.support_history.size(); ++i) {
+        std::fill(support_history + k * i, support_history + k * (i + 1), 0);
+        std::copy(res.support_history[i].begin(), res.support_history[i].end(),
+                  support_history + k * i);
+      }
+  });
+}
+
 int fmpo_omp_solve_batch(int kind, uint64_t n, const uint64_t* omega,
                          uint64_t m, const double* y, uint64_t batch,
                          const fmpo_solve_config* c, int threads,

@@ -73,6 +73,11 @@ class OmpResult(C.Structure):
                 ("history", _vp)]
 
 
+class CosampResult(C.Structure):
+    _fields_ = [("support", _vp), ("coeffs", _vp), ("support_size", _vp), ("iterations", _vp),
+                ("residual", _vp), ("aborted", _vp), ("support_history", _vp), ("history", _vp)]
+
+
 _sig("fmp_version", C.c_int)
 _sig("fmp_fma_peak", C.c_int, _vp, C.c_int, C.POINTER(C.c_double))
 _sig("fmp_last_error", C.c_char_p)
@@ -102,6 +107,10 @@ _sig("fmp_argmax_band", C.c_int, _vp, C.c_int, _vp, _u64, _u64, _vp)
 _sig("fmp_omp_solve", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig), C.POINTER(OmpResult))
 _sig("fmp_omp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig),
      C.POINTER(OmpResult), _vp)
+_sig("fmp_cosamp_solve", C.c_int, _vp, C.c_int, _vp, _u64, _u64, C.POINTER(OmpConfig),
+     C.POINTER(CosampResult))
+_sig("fmp_cosamp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, _u64, C.POINTER(OmpConfig),
+     C.POINTER(CosampResult), _vp)
 _sig("fmp_large_create", C.c_int, _vp, C.c_int, _u64, _u64, C.POINTER(OmpConfig), C.POINTER(_vp))
 _sig("fmp_large_destroy", C.c_int, _vp)
 _sig("fmp_large_begin", C.c_int, _vp, _vp, C.c_double, C.POINTER(C.c_double))
@@ -537,6 +546,88 @@ def least_squares(op: SensingOperator, support, y, dtype=None) -> np.ndarray:
     return out[0] if y.ndim == 1 else out
 
 
+@dataclass
+class CosampBatch:
+    support: np.ndarray          # (batch, k) ascending 1-based, 0 padded
+    coeffs: np.ndarray           # (batch, k) complex128
+    support_size: np.ndarray
+    iterations: np.ndarray
+    residual: np.ndarray
+    aborted: np.ndarray
+    support_history: Optional[np.ndarray]  # (batch, T, k) or None
+    history: Optional[np.ndarray]          # (batch, T, n) or None
+
+
+def cosamp_solve_batch(op: SensingOperator, Y, k: int, cfg: SolveConfig, tolerances=None,
+                       dtype=None, want_history: bool = True) -> CosampBatch:
+    """cosamp_solve (solvers.hpp:73-78) over a batch of measurements (batch, m)."""
+    Y = np.asarray(Y)
+    if dtype is None:
+        dtype = Y.dtype if Y.dtype in DTYPES else np.complex128
+        if op.kind == FOURIER and not np.issubdtype(dtype, np.complexfloating):
+            dtype = np.complex128
+    Y = np.ascontiguousarray(Y, dtype=dtype)
+    if Y.ndim == 1:
+        Y = Y[None]
+    if Y.shape[-1] != op.m:
+        raise InvalidArgument(1, "cosamp_solve: measurement length mismatch")
+    B, T, n, K = Y.shape[0], int(cfg.max_iterations), op.n, int(k)
+    if T < 1:
+        raise InvalidArgument(1, "cosamp_solve: max_iterations must be >= 1")
+    kk = max(K, 1)
+    sup = np.zeros((B, kk), np.uint64)
+    co = np.zeros((B, kk), np.complex128)
+    sz = np.zeros(B, np.uint64)
+    it = np.zeros(B, np.uint64)
+    rn = np.zeros(B)
+    ab = np.zeros(B, np.int32)
+    sh = np.zeros((B, T, kk), np.uint64) if want_history else None
+    hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
+    tol = None
+    if tolerances is not None:
+        tarr = np.ascontiguousarray(np.broadcast_to(np.asarray(tolerances, np.float64), (B,)))
+        tol = tarr.ctypes.data_as(C.POINTER(C.c_double))
+    res = CosampResult(_ptr(sup), _ptr(co), _ptr(sz), _ptr(it), _ptr(rn), _ptr(ab),
+                       _ptr(sh) if sh is not None else None, _ptr(hist) if hist is not None else None)
+    c = _config(cfg, tol)
+    _check(_lib.fmp_cosamp_solve(op.handle, DTYPES[Y.dtype], _ptr(Y), B, K, C.byref(c),
+                                 C.byref(res)))
+    return CosampBatch(sup[:, :K], co[:, :K], sz, it, rn, ab.astype(bool),
+                       sh[:, :, :K] if sh is not None else None, hist)
+
+
+def cosamp_solve(op: SensingOperator, y, k: int, cfg: SolveConfig, dtype=None) -> RecoveryResult:
+    """cosamp_solve (solvers.hpp:73-78, solvers.cpp:413-544) for one vector."""
+    r = cosamp_solve_batch(op, np.asarray(y)[None], k, cfg, dtype=dtype)
+    s, iters = int(r.support_size[0]), int(r.iterations[0])
+    support = [int(v) for v in r.support[0, :s]]
+    coeffs = r.coeffs[0, :s].copy()
+    x = np.zeros(op.n, np.complex128)
+    for a, v in zip(support, coeffs):
+        x[a - 1] = v
+    sh = [[int(v) for v in row if v] for row in r.support_history[0, :iters]]
+    hist = [r.history[0, i].copy() for i in range(T_rec(r, iters))] if r.history is not None else []
+    fast = cfg.correlation_mode in ("fast", "gpu", "custom") or (
+        cfg.correlation_mode == "adaptive" and adaptive_cosamp_uses_fast(op.kind, op.n, k))
+    return RecoveryResult(x, support, coeffs, iters, float(r.residual[0]), bool(r.aborted[0]),
+                          sh, hist, [int(fast)] * len(hist))
+
+
+def T_rec(r: CosampBatch, iters: int) -> int:
+    """correlation vectors computed: one per completed iteration, plus the
+    one of an iteration that ended in a rank-deficient abort"""
+    return iters + (1 if bool(r.aborted[0]) else 0)
+
+
+def adaptive_cosamp_uses_fast(kind, n: int, k: int) -> bool:
+    """cost_model.cpp:91-96 (power-of-two n)."""
+    kind = KINDS.get(kind, kind)
+    if k == 0:
+        return True
+    logn = int(n).bit_length() - 1
+    return (6 if kind == FOURIER else 2) * n * k <= (5 if kind == FOURIER else 2) * n * logn
+
+
 # ------------------------------------------- sharded single-signal solver
 class LargeShard:
     """Shard p of P of the config-5 solver (fmp_large_*): correlation entries
@@ -705,5 +796,6 @@ __all__ = [
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
     "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
-    "least_squares", "LargeShard", "LocalExchange", "sharded_solve", "large_solve",
+    "least_squares", "cosamp_solve", "cosamp_solve_batch", "adaptive_cosamp_uses_fast",
+    "LargeShard", "LocalExchange", "sharded_solve", "large_solve",
 ]

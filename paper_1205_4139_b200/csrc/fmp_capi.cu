@@ -73,7 +73,8 @@ struct Workspace {
 };
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
-            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC };
+            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
+            S_OHSUP, S_OHSZ };
 
 }  // namespace
 
@@ -758,6 +759,156 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
   if (out->modes) CU(cudaMemcpyAsync(out->modes, d.modes, batch * T, cudaMemcpyDeviceToHost, st));
   if (out->history_len)
     CU(cudaMemcpyAsync(out->history_len, d.history_len, batch * 8, cudaMemcpyDeviceToHost, st));
+  if (cfg->record_correlations)
+    CU(cudaMemcpyAsync(out->history, d.history, batch * T * n * eb, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+// ------------------------------------------------------------------ CoSaMP
+static int cosamp_validate(fmp_op op, int dtype, uint64_t k, const fmp_omp_config* cfg) {
+  if (!op || !cfg) return fail(FMP_EINVAL, "null argument");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  if (cfg->max_iterations < 1) return fail(FMP_EINVAL, "cosamp_solve: max_iterations must be >= 1");
+  if (!cfg->tolerances && !(cfg->tolerance >= 0.0))
+    return fail(FMP_EINVAL, "cosamp_solve: tolerance must be >= 0");
+  if (cfg->mode < 0 || cfg->mode > 4) return fail(FMP_EINVAL, "unknown correlation mode");
+  if (k > 1024) return fail(FMP_EUNSUPPORTED, "cosamp_solve: k > 1024");
+  if (op->d.kind == fmp::HADAMARD && !op->d.glat)
+    return fail(FMP_EUNSUPPORTED, "hadamard solve needs m <= 32767 (int16 lattice)");
+  return FMP_OK;
+}
+
+static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
+                             const fmp_omp_config* cfg, const double* dtol, fmp_cosamp_result* out,
+                             cudaStream_t st) {
+  fmp_ctx_s* ctx = op->ctx;
+  const int64_t T = (int64_t)cfg->max_iterations, n = op->d.n, m = op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  fmp::CosArgs a{};
+  a.op = &op->d;
+  a.dtype = dtype;
+  a.y = y;
+  a.tol = dtol;
+  a.batch = (int64_t)batch;
+  a.max_iter = T;
+  a.k = (int64_t)k;
+  bool fast = true;  // FAST, GPU, CUSTOM
+  if (cfg->mode == FMP_MODE_CONVENTIONAL) fast = false;
+  if (cfg->mode == FMP_MODE_ADAPTIVE)  // cost_model.cpp:76-96
+    fast = k == 0 || (op->d.kind == fmp::FOURIER ? 6u : 2u) * (uint64_t)n * k <=
+                         (op->d.kind == fmp::FOURIER ? 5u : 2u) * (uint64_t)n * (uint64_t)op->d.log2n;
+  a.fast = fast ? 1 : 0;
+  a.support = out->support;
+  a.coeffs = (double2*)out->coeffs;
+  a.size = out->support_size;
+  a.iters = out->iterations;
+  a.resid = out->residual;
+  a.aborted = out->aborted;
+  a.hist_sup = out->support_history;
+  a.hist = cfg->record_correlations ? out->history : nullptr;
+  a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
+  if (a.hist_sup) {
+    uint64_t* hs;
+    ALLOC(hs, S_OHSZ, (size_t)batch * T * 8);
+    a.hist_size = hs;
+  }
+  const size_t c3 = 3 * (size_t)std::max<uint64_t>(k, 1);
+  double2* L;
+  ALLOC(L, S_W, (size_t)std::max(a.grid, 1) * c3 * c3 * 16);
+  a.L_ws = L;
+  void* h0;
+  ALLOC(h0, S_H0, (size_t)std::max(a.grid, 1) * n * eb);
+  a.h0_ws = h0;
+  double* mag;
+  ALLOC(mag, S_MAG, (size_t)std::max(a.grid, 1) * n * 8);
+  a.mag_ws = mag;
+  void* r;
+  ALLOC(r, S_R, (size_t)std::max(a.grid, 1) * m * eb);
+  a.r_ws = r;
+  int* q;
+  ALLOC(q, S_Q, 64);
+  a.queue = q;
+  CU(cudaMemsetAsync(q, 0, 4, st));
+  if (out->support_history)
+    CU(cudaMemsetAsync(out->support_history, 0, (size_t)batch * T * k * 8, st));
+  if (batch == 0) return FMP_OK;
+  cudaError_t e = fmp::launch_cosamp(a, st);
+  g_launch_count = fmp::last_launch_count();
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(FMP_EUNSUPPORTED, "n = %lld, k = %llu exceed the CoSaMP kernel's shared-memory plan",
+                (long long)n, (unsigned long long)k);
+  CU(e);
+  return FMP_OK;
+}
+
+int fmp_cosamp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
+                         const fmp_omp_config* cfg, fmp_cosamp_result* out, void* stream) {
+  if (int s = cosamp_validate(op, dtype, k, cfg)) return s;
+  if (!y || !out || !out->support || !out->coeffs || !out->support_size || !out->iterations ||
+      !out->residual || !out->aborted)
+    return fail(FMP_EINVAL, "null buffer");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = pick_stream(ctx, stream);
+  const double* dtol = cfg->tolerances;
+  if (!dtol) {
+    std::vector<double> tv(batch, cfg->tolerance);
+    void* p;
+    if (int s = copy_in(ctx, S_TOL, tv.data(), batch * 8, &p, st)) return s;
+    CU(cudaStreamSynchronize(st));
+    dtol = (const double*)p;
+  }
+  return cosamp_dev_locked(op, dtype, y, batch, k, cfg, dtol, out, st);
+}
+
+int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
+                     const fmp_omp_config* cfg, fmp_cosamp_result* out) {
+  if (int s = cosamp_validate(op, dtype, k, cfg)) return s;
+  if (!y || !out || !out->support || !out->coeffs || !out->support_size || !out->iterations ||
+      !out->residual || !out->aborted)
+    return fail(FMP_EINVAL, "null buffer");
+  if (cfg->record_correlations && !out->history)
+    return fail(FMP_EINVAL, "record_correlations needs a history buffer");
+  if (cfg->tolerances)
+    for (uint64_t b = 0; b < batch; ++b)
+      if (!(cfg->tolerances[b] >= 0.0)) return fail(FMP_EINVAL, "cosamp_solve: tolerance must be >= 0");
+  fmp_ctx_s* ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaStream_t st = ctx->cur;
+  const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
+  const uint64_t kk = std::max<uint64_t>(k, 1);
+  const size_t eb = fmp::elem_bytes(dtype);
+  void* dy;
+  if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
+  std::vector<double> tv;
+  if (!cfg->tolerances) tv.assign(batch, cfg->tolerance);
+  void* dtol;
+  if (int s = copy_in(ctx, S_TOL, cfg->tolerances ? cfg->tolerances : tv.data(), batch * 8, &dtol, st))
+    return s;
+  fmp_cosamp_result d{};
+  ALLOC(d.support, S_OSUP, batch * kk * 8);
+  ALLOC(d.coeffs, S_OCO, batch * kk * 16);
+  ALLOC(d.support_size, S_OSZ, batch * 8);
+  ALLOC(d.iterations, S_OIT, batch * 8);
+  ALLOC(d.residual, S_ORES, batch * 8);
+  ALLOC(d.aborted, S_OAB, batch * 4);
+  if (out->support_history) ALLOC(d.support_history, S_OHSUP, batch * T * kk * 8);
+  if (cfg->record_correlations) ALLOC(d.history, S_OHIST, batch * T * n * eb);
+  if (int s = cosamp_dev_locked(op, dtype, dy, batch, k, cfg, (const double*)dtol, &d, st)) return s;
+  if (k) {
+    CU(cudaMemcpyAsync(out->support, d.support, batch * k * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(out->coeffs, d.coeffs, batch * k * 16, cudaMemcpyDeviceToHost, st));
+    if (out->support_history)
+      CU(cudaMemcpyAsync(out->support_history, d.support_history, batch * T * k * 8,
+                         cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaMemcpyAsync(out->support_size, d.support_size, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->iterations, d.iterations, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->residual, d.residual, batch * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(out->aborted, d.aborted, batch * 4, cudaMemcpyDeviceToHost, st));
   if (cfg->record_correlations)
     CU(cudaMemcpyAsync(out->history, d.history, batch * T * n * eb, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));

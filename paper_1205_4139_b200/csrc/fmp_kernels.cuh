@@ -99,6 +99,30 @@ struct OmpArgs {
   unsigned long long* phase_ws;  // optional per-phase cycle totals (6)
 };
 
+struct CosArgs {
+  const DevOp* op;
+  int dtype;
+  const void* y;            // batch x m
+  const double* tol;        // batch
+  int64_t batch, max_iter, k;
+  int fast;
+  uint64_t* support;        // batch x k
+  double2* coeffs;          // batch x k
+  uint64_t* size;
+  uint64_t* iters;
+  double* resid;
+  int32_t* aborted;
+  uint64_t* hist_sup;       // batch x T x k, optional
+  uint64_t* hist_size;      // batch x T, optional (with hist_sup)
+  void* hist;               // batch x T x n, optional
+  double* mag_ws;           // grid x n
+  void* h0_ws;              // grid x n
+  double2* L_ws;            // grid x (3k)^2
+  void* r_ws;               // grid x m
+  int* queue;
+  int grid;
+};
+
 // launchers (return cudaError_t); all async on `stream`
 cudaError_t launch_transform(const TransformArgs& a, cudaStream_t stream);
 cudaError_t launch_fast_update(const FastUpdateArgs& a, cudaStream_t stream);
@@ -106,6 +130,7 @@ cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t stream);
 cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t stream);
 cudaError_t launch_twiddles(const DevOp& op, cudaStream_t stream);
 cudaError_t launch_omp(const OmpArgs& a, cudaStream_t stream);
+cudaError_t launch_cosamp(const CosArgs& a, cudaStream_t stream);
 // resident CTA count the OMP launcher will use (sizes the workspaces)
 int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 int fast_update_grid(const DevOp& op, int dtype, int64_t batch);

@@ -94,6 +94,40 @@ def main():
                                                     float(r.rank_deficient_abort)])
             g[f"omp{i}_{mode}_modes"] = np.array(r.mode_used, np.int32)
     g["omp_count"] = np.array([len(solves)])
+    # CoSaMP (solvers.cpp:413-544): the noiseless-recovery and edge-case
+    # recipes of test_solvers.cpp:236-277 (own seeds for the noisy trials,
+    # the acceptance anchor shape of acceptance.cpp:198-205)
+    cos = []
+    for kind in ("fourier", "hadamard"):
+        om = R.make_row_selection(64, 32, 51)
+        x, y, e = R.make_instance(kind, 64, om, 4, 0.0, 52)
+        cos.append((kind, 64, om, y, 4, 8, 1e-9 * np.linalg.norm(y)))
+        for trial in range(3):
+            seed = R.derive_seed(80, trial)
+            om = R.make_row_selection(128, 64, R.derive_seed(seed, 1))
+            x, y, e = R.make_instance(kind, 128, om, 4, 0.05, seed)
+            cos.append((kind, 128, om, y, 4, 6, 1e-9 * np.linalg.norm(y)))
+    om = R.make_row_selection(64, 8, 61)
+    x, y, e = R.make_instance("fourier", 64, om, 4, 0.0, 62)
+    cos.append(("fourier", 64, om, y, 4, 6, 0.0))  # rank-deficient abort
+    om = R.make_row_selection(8192, 64, 55)
+    x, y, e = R.make_instance("fourier", 8192, om, 4, 0.0, 56)
+    cos.append(("fourier", 8192, om, y, 4, 6, 0.0))
+    for i, (kind, n, om, y, k, T, tol) in enumerate(cos):
+        g[f"cos{i}_meta"] = np.array([0 if kind == "fourier" else 1, n, len(om), k, T], np.uint64)
+        g[f"cos{i}_tol"] = np.array([tol])
+        g[f"cos{i}_omega"], g[f"cos{i}_y"] = om, y
+        for mode in ("conventional", "fast"):
+            r, sh = R.cosamp_solve(kind, n, om, y, k, T, tol, mode=mode)
+            g[f"cos{i}_{mode}_support"] = r.support
+            g[f"cos{i}_{mode}_coeffs"] = r.coeffs
+            g[f"cos{i}_{mode}_scalars"] = np.array([r.iterations_run, r.residual_norm,
+                                                    float(r.rank_deficient_abort)])
+            hist = np.zeros((T, k), np.uint64)
+            for t, row in enumerate(sh):
+                hist[t, : len(row)] = row
+            g[f"cos{i}_{mode}_history"] = hist
+    g["cos_count"] = np.array([len(cos)])
     np.savez_compressed(os.path.join(OUT, "reference_golden.npz"), **g)
     print("wrote", os.path.join(OUT, "reference_golden.npz"))
 

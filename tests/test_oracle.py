@@ -66,6 +66,42 @@ def test_omp_matches_golden_bitwise(oracle, gold):
             assert r.mode_used[: r.iterations_run] == list(gold[f"omp{i}_{mode}_modes"][: r.iterations_run])
 
 
+def test_cosamp_matches_golden_bitwise(oracle, gold):
+    # CoSaMP (solvers.cpp:413-544) against the reference's own outputs
+    for i in range(int(gold["cos_count"][0])):
+        kind, n, m, k, T = (int(v) for v in gold[f"cos{i}_meta"])
+        tol = float(gold[f"cos{i}_tol"][0])
+        for mode in ("conventional", "fast"):
+            r, sh = oracle.cosamp_solve(KN[kind], n, gold[f"cos{i}_omega"], gold[f"cos{i}_y"], k, T,
+                                        tol, mode=mode)
+            assert np.array_equal(r.support, gold[f"cos{i}_{mode}_support"]), (i, mode)
+            assert np.array_equal(r.coeffs, gold[f"cos{i}_{mode}_coeffs"]), (i, mode)
+            it, rn, ab = gold[f"cos{i}_{mode}_scalars"]
+            assert r.iterations_run == int(it) and r.residual_norm == rn
+            assert r.rank_deficient_abort == bool(ab)
+            hist = gold[f"cos{i}_{mode}_history"]
+            assert [list(row) for row in sh] == [list(row[row > 0]) for row in hist[: r.iterations_run]]
+
+
+def test_cosamp_edge_cases(oracle):
+    # test_solvers.cpp:236-277: noiseless recovery, k = 0, rank-deficient abort
+    for kind in ("fourier", "hadamard"):
+        om = oracle.make_row_selection(64, 32, 51)
+        x, y, e = oracle.make_instance(kind, 64, om, 4, 0.0, 52)
+        r, _ = oracle.cosamp_solve(kind, 64, om, y, 4, 8, 1e-9 * np.linalg.norm(y))
+        assert list(r.support) == [j + 1 for j in np.flatnonzero(x)]
+        assert r.residual_norm < 1e-9 * np.linalg.norm(y)
+    om = oracle.make_row_selection(64, 8, 61)
+    x, y, e = oracle.make_instance("fourier", 64, om, 4, 0.0, 62)
+    r, _ = oracle.cosamp_solve("fourier", 64, om, y, 0, 1, np.linalg.norm(y))
+    assert r.iterations_run == 0 and len(r.support) == 0
+    a, sa = oracle.cosamp_solve("fourier", 64, om, y, 4, 6, 0.0, "conventional")
+    b, sb = oracle.cosamp_solve("fourier", 64, om, y, 4, 6, 0.0, "fast")
+    assert a.rank_deficient_abort and b.rank_deficient_abort
+    assert a.iterations_run == b.iterations_run
+    assert [list(v) for v in sa] == [list(v) for v in sb]
+
+
 # ------------------------------------------------- live reference agreement
 def test_restatement_bitwise_equals_reference(oracle, reference):
     for kind in ("fourier", "hadamard"):
@@ -86,6 +122,26 @@ def test_restatement_bitwise_equals_reference(oracle, reference):
                         assert a.residual_norm == b.residual_norm
                         for p, q in zip(a.correlation_history, b.correlation_history):
                             assert np.array_equal(p, q)
+
+
+def test_cosamp_restatement_equals_reference(oracle, reference):
+    # all modes, both kinds, noisy and noiseless, 3k > n and 3k > m shapes
+    for kind in ("fourier", "hadamard"):
+        for (n, m, k) in ((64, 32, 4), (256, 96, 8), (512, 128, 16), (64, 64, 40), (256, 16, 8)):
+            for seed in range(3):
+                om = oracle.make_row_selection(n, m, oracle.derive_seed(seed, 1))
+                y = oracle.make_instance(kind, n, om, k, 0.05 if seed % 2 else 0.0, seed)[1]
+                tol = 1e-9 * np.linalg.norm(y) if seed else 0.0
+                for mode in ("conventional", "fast", "adaptive"):
+                    a, sa = oracle.cosamp_solve(kind, n, om, y, k, max(k, 6), tol, mode, record=True)
+                    b, sb = reference.cosamp_solve(kind, n, om, y, k, max(k, 6), tol, mode, record=True)
+                    assert np.array_equal(a.support, b.support) and np.array_equal(a.coeffs, b.coeffs)
+                    assert (a.iterations_run, a.residual_norm, a.rank_deficient_abort) == \
+                        (b.iterations_run, b.residual_norm, b.rank_deficient_abort)
+                    assert [list(v) for v in sa] == [list(v) for v in sb]
+                    assert a.mode_used == b.mode_used
+                    for p, q in zip(a.correlation_history, b.correlation_history):
+                        assert np.array_equal(p, q)
 
 
 def test_least_squares_and_rank_errors(oracle, reference):
