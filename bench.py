@@ -74,6 +74,8 @@ def parse():
     p.add_argument("--no-c3", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0)
+    p.add_argument("--solver", default="omp", choices=["omp", "cosamp"],
+                   help="cosamp: CoSaMP with sparsity K on the same workload (SURVEY §8 f1)")
     a = p.parse_args()
     CFG.update(CONFIGS[a.config])
     if a.dtype:
@@ -534,10 +536,161 @@ def our_arm(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def cosamp_flops(iters: np.ndarray, fast: bool, n: int, k: int) -> float:
+    """The reference's analytic CoSaMP correlation cost (cost_model.cpp:76-82):
+    t = 1 and conventional iterations 5 N log2 N, fast iterations 6 N K."""
+    logn = int(np.log2(n))
+    it = iters.astype(np.float64)
+    conv = 5.0 * n * logn
+    return float(np.sum(conv + np.maximum(it - 1, 0) * (6.0 * n * k if fast else conv)))
+
+
+def run_cpu_cosamp(Y, tol, rows, sample, mode, threads):
+    from concurrent.futures import ThreadPoolExecutor
+    orc, kind = reference_oracle()
+    Yw = Y[:sample].astype(np.complex128)
+
+    def one(i):
+        return orc.cosamp_solve(CFG["kind"], CFG["n"], rows, Yw[i], CFG["k"], CFG["iters"],
+                                float(tol[i]), mode)[0]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(one, range(len(Yw))))
+    dt = time.perf_counter() - t0
+    return len(Yw) / dt, dt, kind, res
+
+
+def cosamp_reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    sample = args.cpu_sample or max(4, min(CFG["batch"], 4 * threads))
+    rows, Y, tol = problem(sample, 0)
+    mode = "fast" if args.mode in ("auto", "gpu") else args.mode
+    for _ in range(max(1, args.warmup)):
+        run_cpu_cosamp(Y, tol, rows, min(sample, threads), mode, threads)
+    times, kind = [], "reference"
+    for _ in range(args.steps):
+        _, dt, kind, _ = run_cpu_cosamp(Y, tol, rows, sample, mode, threads)
+        times.append(dt)
+    value = sample * args.steps / sum(times)
+    print(json.dumps({
+        "impl": "reference", "metric": "cosamp_recoveries_per_sec", "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": CFG["dtype"], "data": "synthetic (seeded, SURVEY §8d)",
+        "config": {"workload": "cosamp " + CFG["name"], "batch_per_step": sample, "mode": mode},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample} signals per step, one cosamp_solve per host thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cosamp_arm(args, ws, rank, local):
+    """CoSaMP (solvers.cpp:413-544) on the config's workload: sparsity K,
+    at most `iters` iterations, halting at the config tolerance."""
+    import torch
+    import paper_1205_4139_b200 as fmp
+
+    n, m, k, T = CFG["n"], CFG["m"], CFG["k"], CFG["iters"]
+    B = args.batch or CFG["batch"]
+    ctx = fmp.Context(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    rows, Y, tol_h = problem(B, rank * B)
+    op = fmp.SensingOperator(CFG["kind"], n, rows, ctx)
+    y_dev = torch.from_numpy(Y).to("cuda")
+    tol_dev = torch.from_numpy(tol_h).to("cuda")
+    out = fmp.alloc_dev_result(B, k)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def timed(mode, steps, warmup):
+        cfg = fmp.SolveConfig(max_iterations=T, residual_tolerance=0.0, correlation_mode=mode)
+        for _ in range(warmup):
+            fmp.cosamp_solve_dev(op, y_dev, k, cfg, out, tolerances=tol_dev, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        launches = 0
+        for a, b in ev:
+            flush.zero_()
+            a.record(stream)
+            fmp.cosamp_solve_dev(op, y_dev, k, cfg, out, tolerances=tol_dev, stream=stream.cuda_stream)
+            launches += fmp.last_launch_count()
+            b.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        return float(np.sum([a.elapsed_time(b) for a, b in ev])), launches
+
+    cands = ["fast", "conventional"] if args.mode == "auto" else [args.mode]
+    per = {c: allreduce_max(timed(c, 2, 1)[0] / 2, ws) for c in cands}
+    best = min(per, key=per.get)
+    with Clocks(local) as clk:
+        tot_ms, launches = timed(best, args.steps, args.warmup)
+    ms_step = allreduce_max(tot_ms, ws) / args.steps
+    value = B * ws / (ms_step * 1e-3)
+    sup = out["support"].cpu().numpy()
+    iters = out["iterations"].cpu().numpy()
+    ncheck = min(B, 256)
+    truth = true_supports(rank * B, ncheck)
+    found = float(np.mean([sorted(truth[b]) == sup[b][sup[b] > 0].tolist() for b in range(ncheck)]))
+    fpk = ctx.fma_peak(CFG["dtype"] in ("c128", "f64"))
+    achieved = cosamp_flops(iters, best == "fast", n, k) / (ms_step * 1e-3)
+    roofline = {"bound": "fma", "achieved": achieved / 1e12, "peak": 2 * fpk / 1e12,
+                "unit": "TFLOP/s", "frac": achieved / (2 * fpk), "traffic": None,
+                "kernel": "k_cosamp (fused solver, the only kernel of the step)",
+                "algorithmic": "reference analytic CoSaMP correlation flops of the iterations run"}
+    cfg = fmp.SolveConfig(max_iterations=T, residual_tolerance=0.0, correlation_mode=best)
+    y_pin = torch.from_numpy(Y).pin_memory()
+    Yp = y_pin.numpy()
+    ctx.set_stream(None)
+    e2e_res = fmp.cosamp_solve_batch(op, Yp, k, cfg, tolerances=tol_h, want_history=False)
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_res = fmp.cosamp_solve_batch(op, Yp, k, cfg, tolerances=tol_h, want_history=False)
+    e2e_s = allreduce_max((time.perf_counter() - t0) / e2e_steps, ws)
+    eb = Y.dtype.itemsize
+    e2e = {"value": B * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * m * eb + B * 8),
+           "d2h_bytes_per_step": int(B * k * 24 + B * 8 * 3 + B * 4),
+           "api": "fmp_cosamp_solve (host buffers, pinned y)"}
+    cpu = None
+    if not args.no_cpu and rank == 0 and ws == 1:
+        threads = cpu_threads()
+        sample = args.cpu_sample or max(4, min(B, 8 * threads))
+        v, dt, kind, res = run_cpu_cosamp(Y, tol_h, rows, sample, best, threads)
+        same = float(np.mean([list(res[i].support) ==
+                              list(e2e_res.support[i, :int(e2e_res.support_size[i])])
+                              for i in range(sample)]))
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"first {sample} signals, reference cosamp_solve ({best}), one solve per "
+                         f"host thread ({dt:.1f}s)", "support_agreement_with_gpu": same}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "cosamp_recoveries_per_sec", "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": CFG["dtype"],
+            "data": "synthetic (seeded, SURVEY §8d; resident in HBM)",
+            "config": {"workload": "cosamp " + CFG["name"], "batch_per_gpu": B, "mode": best,
+                       "mode_step_ms": per, "max_iterations": T,
+                       "mean_iterations": float(iters.mean()),
+                       "l2": "flushed (512 MB write) between timed steps",
+                       "parallelism": f"batch-sharded x{ws}"},
+            "gpu_launches": launches, "true_support_recovered": found, "clocks": clk.summary(),
+            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+        }), flush=True)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_setup()
-    if args.impl == "reference":
+    if args.solver == "cosamp":
+        (cosamp_reference_arm(args, ws, rank) if args.impl == "reference"
+         else cosamp_arm(args, ws, rank, local))
+    elif args.impl == "reference":
         reference_arm(args, ws, rank)
     elif args.config == 5:
         large_arm(args, ws, rank, local)

@@ -74,6 +74,11 @@ CorrelationMode parse_mode(const std::string& name);
 std::uint64_t conventional_iteration_flops(TransformKind kind, std::size_t n);
 std::uint64_t fast_iteration_flops(TransformKind kind, std::size_t n, std::size_t t);
 std::size_t crossover_iteration(TransformKind kind, std::size_t n);
+// CoSaMP cost helpers (cost_model.hpp:81-90)
+std::uint64_t cosamp_fast_iteration_flops(TransformKind kind, std::size_t n, std::size_t k,
+                                          std::size_t t);
+double cosamp_relative_cost(std::size_t n, std::size_t k);
+bool adaptive_cosamp_uses_fast(TransformKind kind, std::size_t n, std::size_t k);
 
 struct IterationCost {
   std::size_t t = 0;
@@ -241,6 +246,13 @@ RecoveryResult omp_solve(const SensingOperator& op, const cvec& y, const SolveCo
 // Batched extension: one launch solves every measurement vector.
 std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std::vector<cvec>& ys,
                                             const SolveConfig& cfg);
+
+// CoSaMP with sparsity k (solvers.hpp:73-78); one fused launch per batch.
+RecoveryResult cosamp_solve(const SensingOperator& op, const cvec& y, std::size_t k,
+                            const SolveConfig& cfg);
+std::vector<RecoveryResult> cosamp_solve_batch(const SensingOperator& op,
+                                               const std::vector<cvec>& ys, std::size_t k,
+                                               const SolveConfig& cfg);
 
 cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
                    const cvec& y, LeastSquaresMethod method = LeastSquaresMethod::NormalEquations,

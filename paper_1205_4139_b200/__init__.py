@@ -760,6 +760,22 @@ def omp_solve_dev(op: SensingOperator, y, cfg: SolveConfig, out: dict, tolerance
                                   stream))
 
 
+def cosamp_solve_dev(op: SensingOperator, y, k: int, cfg: SolveConfig, out: dict, tolerances=None,
+                     stream: Optional[int] = None) -> None:
+    """Enqueue a batched CoSaMP solve on device tensors; out from
+    alloc_dev_result(batch, k) (support / coeffs hold k entries per problem)."""
+    B = y.shape[0]
+    c = _config(cfg, C.cast(C.c_void_p(tolerances.data_ptr()), C.POINTER(C.c_double))
+                if tolerances is not None else None)
+    res = CosampResult(out["support"].data_ptr(), out["coeffs"].data_ptr(),
+                       out["support_size"].data_ptr(), out["iterations"].data_ptr(),
+                       out["residual"].data_ptr(), out["aborted"].data_ptr(),
+                       out["support_history"].data_ptr() if "support_history" in out else None,
+                       out["history"].data_ptr() if "history" in out else None)
+    _check(_lib.fmp_cosamp_solve_dev(op.handle, _dtype_code(y), y.data_ptr(), B, int(k), C.byref(c),
+                                     C.byref(res), stream))
+
+
 def alloc_dev_result(B: int, T: int, device="cuda") -> dict:
     import torch
     return {
@@ -796,6 +812,6 @@ __all__ = [
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
     "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
-    "least_squares", "cosamp_solve", "cosamp_solve_batch", "adaptive_cosamp_uses_fast",
+    "least_squares", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
     "LargeShard", "LocalExchange", "sharded_solve", "large_solve",
 ]

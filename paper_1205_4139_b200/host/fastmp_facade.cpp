@@ -431,6 +431,109 @@ RecoveryResult omp_solve(const SensingOperator& op, const cvec& y, const SolveCo
   return std::move(omp_solve_batch(op, std::vector<cvec>{y}, cfg)[0]);
 }
 
+std::uint64_t cosamp_fast_iteration_flops(TransformKind kind, std::size_t n, std::size_t k,
+                                          std::size_t t) {
+  if (t == 0) throw std::invalid_argument("flops: t must be positive");
+  if (t == 1) return conventional_iteration_flops(kind, n);
+  return (kind == TransformKind::Fourier ? 6 : 2) * std::uint64_t(n) * std::uint64_t(k);
+}
+
+double cosamp_relative_cost(std::size_t n, std::size_t k) {
+  if (!is_power_of_two(n) || n < 2)
+    throw std::invalid_argument("cosamp_relative_cost: n must be a power of two >= 2");
+  std::size_t logn = 0;
+  while ((std::size_t{1} << logn) < n) ++logn;
+  return 6.0 * double(k) / (5.0 * double(logn));
+}
+
+bool adaptive_cosamp_uses_fast(TransformKind kind, std::size_t n, std::size_t k) {
+  if (k == 0) return true;
+  return cosamp_fast_iteration_flops(kind, n, k, 2) <= conventional_iteration_flops(kind, n);
+}
+
+std::vector<RecoveryResult> cosamp_solve_batch(const SensingOperator& op,
+                                               const std::vector<cvec>& ys, std::size_t k,
+                                               const SolveConfig& cfg) {
+  const std::size_t B = ys.size(), T = cfg.max_iterations, n = op.n(), m = op.m();
+  if (T < 1) throw std::invalid_argument("cosamp_solve: max_iterations must be >= 1");
+  if (!(cfg.residual_tolerance >= 0.0))
+    throw std::invalid_argument("cosamp_solve: tolerance must be >= 0");
+  std::vector<RecoveryResult> results(B);
+  if (B == 0) return results;
+  cvec y(B * m);
+  for (std::size_t b = 0; b < B; ++b) {
+    if (ys[b].size() != m) throw std::invalid_argument("cosamp_solve: measurement length mismatch");
+    std::copy(ys[b].begin(), ys[b].end(), y.begin() + b * m);
+  }
+  fmp_omp_config c{};
+  c.max_iterations = T;
+  c.tolerance = cfg.residual_tolerance;
+  c.mode = cfg.correlation_mode == CorrelationMode::Conventional ? FMP_MODE_CONVENTIONAL
+           : cfg.correlation_mode == CorrelationMode::Fast       ? FMP_MODE_FAST
+                                                                  : FMP_MODE_ADAPTIVE;
+  c.record_correlations = cfg.record_correlations ? 1 : 0;
+  const std::size_t kk = std::max<std::size_t>(k, 1);
+  std::vector<std::uint64_t> sup(B * kk), size(B), iters(B), sh(B * T * kk);
+  cvec co(B * kk);
+  std::vector<double> rn(B);
+  std::vector<std::int32_t> ab(B);
+  cvec hist(cfg.record_correlations ? B * T * n : 0);
+  fmp_cosamp_result r{};
+  r.support = sup.data();
+  r.coeffs = raw(co);
+  r.support_size = size.data();
+  r.iterations = iters.data();
+  r.residual = rn.data();
+  r.aborted = ab.data();
+  r.support_history = sh.data();
+  r.history = cfg.record_correlations ? raw(hist) : nullptr;
+  check(fmp_cosamp_solve(static_cast<fmp_op>(op.handle()), FMP_C128, raw(y), B, k, &c, &r));
+  const TransformKind kind = op.unitary().kind();
+  const bool fast = cfg.correlation_mode == CorrelationMode::Fast ||
+                    (cfg.correlation_mode == CorrelationMode::Adaptive &&
+                     adaptive_cosamp_uses_fast(kind, n, k));
+  for (std::size_t b = 0; b < B; ++b) {
+    RecoveryResult& res = results[b];
+    res.x_hat.assign(n, cplx(0.0));
+    for (std::size_t j = 0; j < size[b]; ++j) {
+      res.support.push_back(static_cast<std::size_t>(sup[b * k + j]));
+      res.coeffs.push_back(co[b * k + j]);
+      res.x_hat[res.support.back() - 1] = res.coeffs.back();
+    }
+    res.iterations_run = iters[b];
+    res.residual_norm = rn[b];
+    res.rank_deficient_abort = ab[b] != 0;
+    for (std::size_t t = 0; t < res.iterations_run; ++t) {
+      std::vector<std::size_t> row;
+      for (std::size_t j = 0; j < k; ++j)
+        if (sh[(b * T + t) * k + j]) row.push_back(static_cast<std::size_t>(sh[(b * T + t) * k + j]));
+      res.support_history.push_back(std::move(row));
+    }
+    res.costs.kind = kind;
+    res.costs.n = n;
+    const std::size_t rows = std::min<std::size_t>(T, res.iterations_run + (res.rank_deficient_abort ? 1 : 0));
+    for (std::size_t t = 1; t <= rows; ++t) {
+      IterationCost row;
+      row.t = t;
+      row.mode_used = fast ? CorrelationMode::Fast : CorrelationMode::Conventional;
+      row.analytic_flops = fast ? cosamp_fast_iteration_flops(kind, n, k, t)
+                                : conventional_iteration_flops(kind, n);
+      row.counted.complex_add = row.analytic_flops / kComplexAddFlops;
+      res.costs.iterations.push_back(row);
+      if (cfg.record_correlations)
+        res.correlation_history.emplace_back(hist.begin() + (b * T + t - 1) * n,
+                                             hist.begin() + (b * T + t) * n);
+    }
+  }
+  return results;
+}
+
+RecoveryResult cosamp_solve(const SensingOperator& op, const cvec& y, std::size_t k,
+                            const SolveConfig& cfg) {
+  if (y.size() != op.m()) throw std::invalid_argument("cosamp_solve: measurement length mismatch");
+  return std::move(cosamp_solve_batch(op, std::vector<cvec>{y}, k, cfg)[0]);
+}
+
 cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
                    const cvec& y, LeastSquaresMethod, FlopCounter*) {
   if (y.size() != op.m()) throw std::invalid_argument("least_squares: rhs length mismatch");

@@ -228,6 +228,58 @@ int main(int argc, char** argv) {
     CHECK(zero.iterations_run == 0 && zero.support.empty() && zero.residual_norm == 0.0);
     CHECK_THROWS_AS(omp_solve(op, cvec(7), default_config(1, 1.0)), std::invalid_argument);
   }
+  // CoSaMP (test_solvers.cpp:236-305, test_cost_model.cpp:93-108)
+  {
+    CHECK(cosamp_fast_iteration_flops(TransformKind::Hadamard, 1024, 8, 2) == 2 * 1024 * 8);
+    CHECK(cosamp_relative_cost(8192, 4) == 24.0 / 65.0);
+    CHECK(adaptive_cosamp_uses_fast(TransformKind::Fourier, 8192, 4));
+    CHECK(!adaptive_cosamp_uses_fast(TransformKind::Fourier, 8192, 16));
+    for (TransformKind kind : {TransformKind::Fourier, TransformKind::Hadamard}) {
+      SensingOperator op(StructuredUnitary(kind, 64), make_row_selection(64, 32, 51));
+      const ProblemInstance inst = make_instance(op, 4, 0.0, 52);
+      SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
+      cfg.max_iterations = 8;
+      const RecoveryResult res = cosamp_solve(op, inst.y, inst.k, cfg);
+      std::vector<std::size_t> want;
+      for (std::size_t j = 0; j < 64; ++j)
+        if (inst.x_true[j] != cplx(0.0)) want.push_back(j + 1);
+      CHECK(res.support == want);
+      CHECK(res.residual_norm < 1e-9 * l2_norm(inst.y));
+      CHECK(l2_distance(res.x_hat, inst.x_true) < 1e-8 * l2_norm(inst.x_true));
+    }
+    SensingOperator op(StructuredUnitary(TransformKind::Fourier, 64), make_row_selection(64, 8, 61));
+    const ProblemInstance inst = make_instance(op, 4, 0.0, 62);
+    const RecoveryResult empty = cosamp_solve(op, inst.y, 0, default_config(1, l2_norm(inst.y)));
+    CHECK(empty.iterations_run == 0 && empty.support.empty());
+    SolveConfig cfg = default_config(4, l2_norm(inst.y));
+    cfg.max_iterations = 6;
+    cfg.residual_tolerance = 0.0;
+    cfg.correlation_mode = CorrelationMode::Conventional;
+    const RecoveryResult conv = cosamp_solve(op, inst.y, 4, cfg);
+    cfg.correlation_mode = CorrelationMode::Fast;
+    const RecoveryResult fast = cosamp_solve(op, inst.y, 4, cfg);
+    CHECK(conv.rank_deficient_abort && fast.rank_deficient_abort);
+    CHECK(conv.support_history == fast.support_history);
+    CHECK(conv.iterations_run == fast.iterations_run);
+    for (TransformKind kind : {TransformKind::Fourier, TransformKind::Hadamard})
+      for (int trial = 0; trial < 10; ++trial) {
+        const std::uint64_t seed = derive_seed(80, trial);
+        SensingOperator op2(StructuredUnitary(kind, 128), make_row_selection(128, 64, derive_seed(seed, 1)));
+        const ProblemInstance in2 = make_instance(op2, 4, 0.05, seed);
+        SolveConfig c2 = default_config(in2.k, l2_norm(in2.y));
+        c2.record_correlations = true;
+        c2.max_iterations = 6;
+        c2.correlation_mode = CorrelationMode::Conventional;
+        const RecoveryResult a = cosamp_solve(op2, in2.y, in2.k, c2);
+        c2.correlation_mode = CorrelationMode::Fast;
+        const RecoveryResult b = cosamp_solve(op2, in2.y, in2.k, c2);
+        CHECK(a.support_history == b.support_history);
+        CHECK(a.correlation_history.size() == b.correlation_history.size());
+        for (std::size_t i = 0; i < a.correlation_history.size(); ++i)
+          CHECK(l2_distance(b.correlation_history[i], a.correlation_history[i]) <=
+                1e-10 * std::max(l2_norm(a.correlation_history[i]), 1e-300));
+      }
+  }
   std::printf("facade test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -25,7 +25,7 @@ def test_facade_builds_and_exports():
     out = subprocess.run(["nm", "-DC", "--defined-only", os.path.join(PKG, "libfastmp_b200.so")],
                          capture_output=True, text=True).stdout
     for sym in ("fastmp::omp_solve(", "fastmp::fast_update(", "fastmp::compute_kernel(",
-                "fastmp::least_squares(", "fastmp::SensingOperator::apply_adjoint("):
+                "fastmp::least_squares(", "fastmp::cosamp_solve(", "fastmp::SensingOperator::apply_adjoint("):
         assert sym in out, sym
 
 
