@@ -74,7 +74,7 @@ struct Workspace {
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
             S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
-            S_OHSUP, S_OHSZ };
+            S_OHSUP };
 
 }  // namespace
 
@@ -808,14 +808,9 @@ static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch
   a.hist_sup = out->support_history;
   a.hist = cfg->record_correlations ? out->history : nullptr;
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
-  if (a.hist_sup) {
-    uint64_t* hs;
-    ALLOC(hs, S_OHSZ, (size_t)batch * T * 8);
-    a.hist_size = hs;
-  }
   const size_t c3 = 3 * (size_t)std::max<uint64_t>(k, 1);
   double2* L;
-  ALLOC(L, S_W, (size_t)std::max(a.grid, 1) * c3 * c3 * 16);
+  ALLOC(L, S_W, (size_t)std::max(a.grid, 1) * c3 * (c3 + 1) / 2 * 16);
   a.L_ws = L;
   void* h0;
   ALLOC(h0, S_H0, (size_t)std::max(a.grid, 1) * n * eb);
@@ -832,6 +827,12 @@ static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch
   CU(cudaMemsetAsync(q, 0, 4, st));
   if (out->support_history)
     CU(cudaMemsetAsync(out->support_history, 0, (size_t)batch * T * k * 8, st));
+  if (g_phase_prof) {
+    unsigned long long* ph;
+    ALLOC(ph, S_PH, 64);
+    CU(cudaMemsetAsync(ph, 0, 64, st));
+    a.phase_ws = ph;
+  }
   if (batch == 0) return FMP_OK;
   cudaError_t e = fmp::launch_cosamp(a, st);
   g_launch_count = fmp::last_launch_count();

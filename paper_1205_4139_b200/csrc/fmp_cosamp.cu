@@ -24,6 +24,8 @@ struct CosK {
   int64_t batch;
   int T, K;
   int fast;                 // fast updates (t >= 2) vs conventional
+  int s_cap;                // merged sizes whose packed L fits the smem region
+  int region;               // bytes of the transform-buffer / L region
   uint64_t* support;        // batch x K (final, ascending, 1-based)
   double2* coeffs;          // batch x K
   uint64_t* size;           // batch
@@ -31,7 +33,6 @@ struct CosK {
   double* resid;
   int32_t* aborted;
   uint64_t* hist_sup;       // batch x T x K (supports after each iteration), optional
-  uint64_t* hist_size;      // batch x T, optional
   void* hist;               // batch x T x n correlation history, optional
   // workspace per CTA
   double* mag_ws;           // n
@@ -39,6 +40,7 @@ struct CosK {
   double2* L_ws;            // (3K)^2
   void* r_ws;               // m
   int* queue;
+  unsigned long long* phase_ws;  // optional cycles per phase (conv, fast, identify, ls, resid, other)
 };
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
@@ -46,35 +48,51 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
 }
 
 // the count-th largest of m[0..len) (multiplicity counted): radix select on
-// the 64-bit patterns, 8 bits per round, histogram in smem.  All threads
-// return the same value.  `hist` needs 256 ints, `ctl` 4 ints.
+// the 64-bit patterns, 8 bits per round; the digit holding the count-th
+// largest is found by a parallel suffix scan of the 256-bin histogram.
+// All threads return the same value.  `hist` needs 256 ints, `ctl` 2; the
+// block must have >= 256 threads.
 __device__ double kth_largest(const double* m, int len, int count, int* hist, unsigned long long* ctl) {
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
+  __shared__ int wsum[8];
   unsigned long long prefix = 0, mask = 0;
   int need = count;
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 256; i += nth) hist[i] = 0;
+    if (tid < 256) hist[tid] = 0;
     __syncthreads();
     for (int i = tid; i < len; i += nth) {
       const unsigned long long k = dkey(m[i]);
       if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
     }
     __syncthreads();
-    if (tid == 0) {
-      int acc = 0, d = 255;
-      for (; d > 0; --d) {
-        if (acc + hist[d] >= need) break;
-        acc += hist[d];
+    // suffix sums: thread d (< 256) owns digit 255 - d, so an inclusive
+    // prefix over d is the count of candidates with digit >= 255 - d
+    int v = 0, incl = 0;
+    if (tid < 256) {
+      v = hist[255 - tid];
+      incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      ctl[0] = (unsigned long long)d;
-      ctl[1] = (unsigned long long)(need - acc);
+      if (lane == 31) wsum[w] = incl;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      for (int q = 0; q < w; ++q) incl += wsum[q];
+      const int before = incl - v;  // candidates with a larger digit
+      if (before < need && incl >= need) {
+        ctl[0] = (unsigned long long)(255 - tid);
+        ctl[1] = (unsigned long long)(need - before);
+      }
     }
     __syncthreads();
     prefix |= ctl[0] << shift;
     mask |= 255ull << shift;
     need = (int)ctl[1];
-    __syncthreads();
   }
+  __syncthreads();
   return __longlong_as_double((long long)prefix);
 }
 
@@ -107,45 +125,103 @@ __device__ int block_scan_excl(int v, int* tmp, int* total) {
   return before;
 }
 
+// select_largest (solvers.cpp:62-86) as ascending positions: the `count`
+// largest of vals[0..len) -- everything above the band around the
+// count-th largest value, then the smallest positions inside the band --
+// united with the positions set in `bits` (optional).  One index-ordered
+// compaction, so `out` comes out sorted.  Returns the number written.
+__device__ int select_band(const double* vals, int len, int count, const unsigned* bits,
+                           unsigned* out, int* s_hist, unsigned long long* s_ctl) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const bool all = count >= len;
+  double hi = INFINITY, lo = INFINITY;
+  if (!all) {
+    const double bnd = kth_largest(vals, len, count, s_hist, s_ctl);
+    hi = bnd * (1.0 + kTieBandRel);
+    lo = bnd * (1.0 - kTieBandRel);
+  }
+  const int per = (len + nth - 1) / nth, i0 = tid * per, i1 = min(len, i0 + per);
+  int nsure = 0, ntied = 0;
+  if (!all)
+    for (int i = i0; i < i1; ++i) {
+      const double v = vals[i];
+      nsure += v > hi;
+      ntied += v <= hi && v >= lo;
+    }
+  int tot_sure = 0;
+  const int tied_before = block_scan_excl(ntied, s_hist, nullptr);
+  block_scan_excl(nsure, s_hist, &tot_sure);
+  const int cap = count - tot_sure;  // tied positions taken, in index order
+  auto chosen = [&](int i, int& tr) {
+    const double v = vals[i];
+    bool sel = all || v > hi;
+    if (!sel && v <= hi && v >= lo) sel = tr++ < cap;
+    if (bits) sel = sel || ((bits[i >> 5] >> (i & 31)) & 1u);
+    return sel;
+  };
+  int nsel = 0, tr = tied_before;
+  for (int i = i0; i < i1; ++i) nsel += chosen(i, tr);
+  int total;
+  int o = block_scan_excl(nsel, s_hist, &total);
+  tr = tied_before;
+  for (int i = i0; i < i1; ++i)
+    if (chosen(i, tr)) out[o++] = (unsigned)i;
+  __syncthreads();
+  return total;
+}
+
 template <class V, bool HAD>
 __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[32];
-  __shared__ unsigned redu[32];
   __shared__ int s_hist[256];
   __shared__ unsigned long long s_ctl[4];
-  __shared__ int s_prob, s_cnt[4];
+  __shared__ int s_prob;
+  __shared__ double s_piv;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T, K = a.K;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
   const int nbuf = n + (n >> CLOGP);
   const V zv = zero_of(V{});
   const double sc = 1.0 / sqrt((double)n);
   const double xscale = HAD ? -1.0 / (double)n : -1.0;
   const int C2 = min(2 * K, n), C3 = 3 * K;
 
-  V* buf = reinterpret_cast<V*>(sm);
-  unsigned char* p = sm + ((sizeof(V) * (size_t)nbuf + 15) / 16) * 16;
+  V* buf = reinterpret_cast<V*>(sm);  // shared with L (packed) during least squares
+  unsigned char* p = sm + a.region;
   unsigned* s_sup = reinterpret_cast<unsigned*>(p); p += 4 * (size_t)C3;   // current support
   unsigned* s_mrg = reinterpret_cast<unsigned*>(p); p += 4 * (size_t)C3;   // merged atoms
-  unsigned* s_pick = reinterpret_cast<unsigned*>(p); p += 4 * (size_t)C3;  // picked / kept
+  unsigned* s_pick = reinterpret_cast<unsigned*>(p); p += 4 * (size_t)C3;  // kept positions
   p = sm + (((size_t)(p - sm) + 15) / 16) * 16;
-  double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // coefficients
-  double2* s_b = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // LS solution
+  double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // coefficients / z
+  double2* s_b = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // rhs (eliminated)
+  double2* s_t = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // LS solution
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)C3 + 15) / 16) * 16;
-  double* s_mg = reinterpret_cast<double*>(p); p += 8 * (size_t)C3;        // |b|^2 (C3)
-  unsigned* s_bits = reinterpret_cast<unsigned*>(p);                         // support bitmap (n bits)
+  double* s_mg = reinterpret_cast<double*>(p); p += 8 * (size_t)C3;        // |b|^2
+  unsigned* s_bits = reinterpret_cast<unsigned*>(p);                         // support bitmap
 
   double* msc = a.mag_ws + (size_t)blockIdx.x * n;
   V* h0w = reinterpret_cast<V*>(a.h0_ws) + (size_t)blockIdx.x * n;
-  double2* L = a.L_ws + (size_t)blockIdx.x * C3 * C3;
+  double2* Lg = a.L_ws + (size_t)blockIdx.x * C3 * (C3 + 1) / 2;  // packed lower triangle
   V* rs = reinterpret_cast<V*>(a.r_ws) + (size_t)blockIdx.x * m;
   const V* gF = fourier_table<V>(op);
   const uint16_t* gH = op.glat;
   const V* twt = twiddles<V>(op);
+  // Gram entry phi_a^H phi_b from the kernel (kernel.cpp:113-140)
   auto gram = [&](unsigned ga, unsigned gb) -> double2 {
     if constexpr (HAD) return make_double2(op.gr64[ga ^ gb], 0.0);
     else return op.g64[(ga - gb) & (unsigned)(n - 1)];
+  };
+
+  // opt-in phase profile (thread 0's clock between barrier-terminated phases)
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long ph_last = clock64();
+  auto mark = [&](int phase) {
+    if (a.phase_ws && tid == 0) {
+      const unsigned long long now = clock64();
+      ph[phase] += now - ph_last;
+      ph_last = now;
+    }
   };
 
   for (;;) {
@@ -164,7 +240,8 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
     for (int i = tid; i < (n + 31) / 32; i += nth) s_bits[i] = 0u;
     if (!(K == 0 || rn <= tol)) {
       for (int t = 1; t <= T; ++t) {
-        // ---- correlation
+        // ---- correlation: U^H scatter(r) (t = 1 or conventional) or the
+        //      fast update on the current estimate (kernel.cpp:209-303)
         V* hrow = a.hist ? reinterpret_cast<V*>(a.hist) + ((size_t)prob * T + (t - 1)) * n : nullptr;
         if (t == 1 || !a.fast) {
           const V* r = t == 1 ? y : rs;
@@ -189,158 +266,83 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
           }
         }
         __syncthreads();
-        // ---- the C2 largest (top_atoms, solvers.cpp:105-118 -> select_largest)
-        //      united with the support (std::set_union): one index-ordered
-        //      compaction of "sure, or among the first tied, or in the support"
-        {
-          double hi = INFINITY, lo = INFINITY;
-          if (C2 < n) {
-            const double bnd = kth_largest(msc, n, C2, s_hist, s_ctl);
-            hi = bnd * (1.0 + kTieBandRel);
-            lo = bnd * (1.0 - kTieBandRel);
-          }
-          const int per = (n + nth - 1) / nth, i0 = tid * per, i1 = min(n, i0 + per);
-          int nsure = 0, ntied = 0;
-          if (C2 < n)
-            for (int i = i0; i < i1; ++i) {
-              const double v = msc[i];
-              nsure += v > hi;
-              ntied += v <= hi && v >= lo;
-            }
-          int tot_sure;
-          const int tied_before = block_scan_excl(ntied, s_hist, nullptr);
-          block_scan_excl(nsure, s_hist, &tot_sure);
-          const int cap = C2 - tot_sure;  // tied positions taken, in index order
-          int nsel = 0, tr = tied_before;
-          for (int i = i0; i < i1; ++i) {
-            const double v = msc[i];
-            bool sel = C2 >= n || v > hi;
-            if (!sel && v <= hi && v >= lo) sel = tr++ < cap;
-            sel = sel || (s_bits[i >> 5] >> (i & 31) & 1u);
-            nsel += sel;
-          }
-          int total;
-          int o = block_scan_excl(nsel, s_hist, &total);
-          tr = tied_before;
-          for (int i = i0; i < i1; ++i) {
-            const double v = msc[i];
-            bool sel = C2 >= n || v > hi;
-            if (!sel && v <= hi && v >= lo) sel = tr++ < cap;
-            sel = sel || (s_bits[i >> 5] >> (i & 31) & 1u);
-            if (sel) s_mrg[o++] = (unsigned)i;
-          }
-          if (tid == 0) s_cnt[3] = total;
-          __syncthreads();
+        mark(t == 1 || !a.fast ? 0 : 1);
+        // ---- merged = sorted(support) U top_atoms(h, 2K) (solvers.cpp:105-118, 471-478)
+        const int sm_ = select_band(msc, n, C2, s_bits, s_mrg, s_hist, s_ctl);
+        // ---- normal equations on merged (solvers.cpp:120-177): Cholesky,
+        //      left-looking like the reference, one warp per row dot
+        mark(2);
+        // Right-looking LDL^H of the Gram on merged (entries looked up in the
+        // kernel), the rhs phi^H y = h0[merged] eliminated in the same sweep:
+        // one barrier per column.  Pivot j is g_jj - sum_k |l_jk|^2 with the
+        // terms subtracted in the reference's order (solvers.cpp:148-160).
+        const double diag = gram(0u, 0u).x;
+        double2* L = sm_ <= a.s_cap ? reinterpret_cast<double2*>(sm) : Lg;
+        auto row = [](int i) { return (size_t)i * (i + 1) / 2; };
+        __syncthreads();  // buf is free
+        for (int i = warp; i < sm_; i += nw) {
+          const unsigned li = s_mrg[i];
+          for (int l = lane; l <= i; l += 32) L[row(i) + l] = gram(li, s_mrg[l]);
+          if (lane == 0) s_b[i] = to_c128(h0w[li]);
         }
-        const int sm_ = s_cnt[3];
-        if (tid == 0) s_cnt[1] = s;
-        // ---- least squares on merged: Cholesky of the Gram lookups
-        for (int e = tid; e < sm_ * sm_; e += nth) {
-          const int i = e / sm_, j = e % sm_;
-          if (i >= j) L[i * sm_ + j] = gram(s_mrg[i], s_mrg[j]);
-        }
-        for (int i = tid; i < sm_; i += nth) s_b[i] = to_c128(h0w[s_mrg[i]]);  // phi_i^H y
         __syncthreads();
-        int bad = 0;
+        bool bad = false;
         for (int j = 0; j < sm_; ++j) {
-          // column j: pivot (one thread), then the rows below (all threads)
-          if (tid == 0) {
-            const double diag = gram(s_mrg[j], s_mrg[j]).x;
-            double d = L[j * sm_ + j].x;
-            for (int k = 0; k < j; ++k) d -= mag2(L[j * sm_ + k]);
-            if (!(d > 1e-12 * diag)) s_cnt[0] = -1;
-            else {
-              s_cnt[0] = 0;
-              L[j * sm_ + j] = make_double2(sqrt(d), 0.0);
+          const double d = L[row(j) + j].x;
+          if (!(d > 1e-12 * diag)) { bad = true; break; }
+          const double inv = 1.0 / d;
+          const double2 bj = s_b[j];
+          for (int i = j + 1 + warp; i < sm_; i += nw) {
+            const size_t ri = row(i);
+            const double2 aij = L[ri + j];
+            const double2 u = make_double2(aij.x * inv, aij.y * inv);  // a_ij / d_j
+            for (int l = j + 1 + lane; l <= i; l += 32) {
+              const double2 alj = L[row(l) + j];
+              double2 v = L[ri + l];
+              v.x -= u.x * alj.x + u.y * alj.y;  // a_il -= a_ij conj(a_lj) / d_j
+              v.y -= u.y * alj.x - u.x * alj.y;
+              L[ri + l] = v;
             }
-          }
-          __syncthreads();
-          if (s_cnt[0] < 0) { bad = 1; break; }
-          const double ljj = L[j * sm_ + j].x;
-          for (int i = j + 1 + tid; i < sm_; i += nth) {
-            double2 v = L[i * sm_ + j];
-            for (int k = 0; k < j; ++k) {
-              const double2 pp = L[i * sm_ + k], q = L[j * sm_ + k];
-              v.x -= pp.x * q.x + pp.y * q.y;
-              v.y -= pp.y * q.x - pp.x * q.y;
+            if (lane == 0) {
+              s_b[i].x -= u.x * bj.x - u.y * bj.y;
+              s_b[i].y -= u.x * bj.y + u.y * bj.x;
             }
-            L[i * sm_ + j] = make_double2(v.x / ljj, v.y / ljj);
           }
           __syncthreads();
         }
         if (bad) { aborted = 1; break; }
-        if (tid == 0) {
-          for (int i = 0; i < sm_; ++i) {  // L z = b
-            double2 v = s_b[i];
-            for (int k = 0; k < i; ++k) {
-              const double2 pp = L[i * sm_ + k], q = s_b[k];
-              v.x -= pp.x * q.x - pp.y * q.y;
-              v.y -= pp.x * q.y + pp.y * q.x;
-            }
-            const double l = L[i * sm_ + i].x;
-            s_b[i] = make_double2(v.x / l, v.y / l);
+        // back substitution of D L'^H x = b' (column-oriented; x into s_t):
+        // x_i = (b'_i - sum_{k>i} conj(a_ki) x_k) / d_i
+        for (int i = sm_ - 1; i >= 0; --i) {
+          const size_t ri = row(i);
+          const double d = L[ri + i].x;
+          const double2 xi = make_double2(s_b[i].x / d, s_b[i].y / d);
+          for (int q = tid; q < i; q += nth) {
+            const double2 pp = L[ri + q];
+            s_b[q].x -= pp.x * xi.x + pp.y * xi.y;
+            s_b[q].y -= pp.x * xi.y - pp.y * xi.x;
           }
-          for (int i = sm_ - 1; i >= 0; --i) {  // L^H x = z
-            double2 v = s_b[i];
-            for (int k = i + 1; k < sm_; ++k) {
-              const double2 pp = L[k * sm_ + i], q = s_b[k];
-              v.x -= pp.x * q.x + pp.y * q.y;
-              v.y -= pp.x * q.y - pp.y * q.x;
-            }
-            const double l = L[i * sm_ + i].x;
-            s_b[i] = make_double2(v.x / l, v.y / l);
-          }
-          // ---- prune to the K largest |b|^2 (select_largest, band rule)
-          const int keep = min(K, sm_);
-          for (int i = 0; i < sm_; ++i) s_mg[i] = mag2(s_b[i]);
-          int ns = 0, nt = 0;
-          if (keep < sm_) {
-            // count-th largest by selection (sm_ <= 3K is small)
-            double bnd = 0.0;
-            {
-              int done = 0;
-              double prev = INFINITY;
-              while (done < keep) {
-                double best = -1.0;
-                int mult = 0;
-                for (int i = 0; i < sm_; ++i)
-                  if (s_mg[i] < prev) {
-                    if (s_mg[i] > best) { best = s_mg[i]; mult = 1; }
-                    else if (s_mg[i] == best) ++mult;
-                  }
-                bnd = best;
-                done += mult;
-                prev = best;
-              }
-            }
-            const double hi = bnd * (1.0 + kTieBandRel), lo = bnd * (1.0 - kTieBandRel);
-            for (int i = 0; i < sm_; ++i)
-              if (s_mg[i] > hi) s_pick[ns++] = (unsigned)i;
-            for (int i = 0; i < sm_ && ns + nt < keep; ++i)
-              if (s_mg[i] <= hi && s_mg[i] >= lo) { s_pick[ns + nt] = (unsigned)i; ++nt; }
-            // kept positions ascending (positions order == atom order)
-            for (int i = 1; i < keep; ++i) {
-              const unsigned v = s_pick[i];
-              int j = i - 1;
-              while (j >= 0 && s_pick[j] > v) { s_pick[j + 1] = s_pick[j]; --j; }
-              s_pick[j + 1] = v;
-            }
-          } else {
-            for (int i = 0; i < sm_; ++i) s_pick[i] = (unsigned)i;
-          }
-          for (int i = 0; i < s_cnt[1]; ++i) s_bits[s_sup[i] >> 5] &= ~(1u << (s_sup[i] & 31));
-          for (int i = 0; i < keep; ++i) {
-            s_bits[s_mrg[s_pick[i]] >> 5] |= 1u << (s_mrg[s_pick[i]] & 31);
-            s_sup[i] = s_mrg[s_pick[i]];
-            s_x[i] = s_b[s_pick[i]];
-            from_c128(make_double2(s_x[i].x * xscale, s_x[i].y * xscale), s_xn[i]);
-          }
-          s_cnt[0] = keep;
+          if (tid == 0) s_t[i] = xi;
+          __syncthreads();
         }
+        mark(3);
+        for (int i = tid; i < sm_; i += nth) s_mg[i] = mag2(s_t[i]);
+        for (int i = tid; i < s; i += nth) atomicAnd(&s_bits[s_sup[i] >> 5], ~(1u << (s_sup[i] & 31)));
         __syncthreads();
-        s = s_cnt[0];
+        const int keep = select_band(s_mg, sm_, min(K, sm_), nullptr, s_pick, s_hist, s_ctl);
+        for (int i = tid; i < keep; i += nth) {
+          const unsigned atom = s_mrg[s_pick[i]];
+          const double2 xv = s_t[s_pick[i]];
+          atomicOr(&s_bits[atom >> 5], 1u << (atom & 31));
+          s_sup[i] = atom;
+          s_x[i] = xv;
+          from_c128(make_double2(xv.x * xscale, xv.y * xscale), s_xn[i]);
+        }
+        s = keep;
+        __syncthreads();
+        mark(2);
         // ---- residual r = y - Phi_S x (one forward transform)
-        for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
+        for (int i = tid; i < nbuf; i += nth) buf[i] = zv;  // (after the barrier above)
         __syncthreads();
         for (int j = tid; j < s; j += nth) {
           V xv;
@@ -356,11 +358,11 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
           r2 += mag2(rv);
         }
         rn = sqrt(block_sum(r2, red));
+        mark(4);
         iters = t;
-        if (a.hist_sup && tid == 0) {
+        if (a.hist_sup) {
           uint64_t* hs = a.hist_sup + ((size_t)prob * T + (t - 1)) * K;
-          for (int j = 0; j < K; ++j) hs[j] = j < s ? (uint64_t)s_sup[j] + 1 : 0;
-          a.hist_size[prob * T + (t - 1)] = (uint64_t)s;
+          for (int j = tid; j < K; j += nth) hs[j] = j < s ? (uint64_t)s_sup[j] + 1 : 0;
         }
         if (rn <= tol) break;
       }
@@ -377,7 +379,10 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
       a.resid[prob] = rn;
       a.aborted[prob] = aborted;
     }
+    mark(5);
   }
+  if (a.phase_ws && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(a.phase_ws + i, ph[i]);
 }
 
 template <class V, bool HAD>
@@ -385,9 +390,16 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   const DevOp& op = *c.op;
   const int64_t n = op.n;
   const int C3 = 3 * (int)c.k;
-  const size_t smem = ((sizeof(V) * (size_t)(n + (n >> CLOGP)) + 15) / 16) * 16 + 12 * (size_t)C3 + 16 +
-                      16 * 2 * (size_t)C3 + ((sizeof(V) * (size_t)C3 + 15) / 16) * 16 + 8 * (size_t)C3 +
-                      4 * (size_t)((n + 31) / 32) + 64;
+  const size_t small = 12 * (size_t)C3 + 16 + 16 * 3 * (size_t)C3 +
+                       ((sizeof(V) * (size_t)C3 + 15) / 16) * 16 + 8 * (size_t)C3 +
+                       4 * (size_t)((n + 31) / 32) + 64;
+  const size_t bufb = ((sizeof(V) * (size_t)(n + (n >> CLOGP)) + 15) / 16) * 16;
+  const size_t avail = (size_t)smem_optin() - 4096 - small;
+  const size_t want = 16 * (size_t)C3 * (C3 + 1) / 2;
+  const size_t region = std::max(bufb, std::min(want, avail) / 16 * 16);
+  int s_cap = 0;
+  while (s_cap < C3 && 16 * (size_t)(s_cap + 1) * (s_cap + 2) / 2 <= region) ++s_cap;
+  const size_t smem = region + small;
   if (smem > (size_t)smem_optin() - 4096) return cudaErrorInvalidConfiguration;
   CosK k{};
   k.op = op;
@@ -397,6 +409,8 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   k.T = (int)c.max_iter;
   k.K = (int)c.k;
   k.fast = c.fast;
+  k.s_cap = s_cap;
+  k.region = (int)region;
   k.support = c.support;
   k.coeffs = c.coeffs;
   k.size = c.size;
@@ -404,13 +418,13 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   k.resid = c.resid;
   k.aborted = c.aborted;
   k.hist_sup = c.hist_sup;
-  k.hist_size = c.hist_size;
   k.hist = c.hist;
   k.mag_ws = c.mag_ws;
   k.h0_ws = c.h0_ws;
   k.L_ws = c.L_ws;
   k.r_ws = c.r_ws;
   k.queue = c.queue;
+  k.phase_ws = c.phase_ws;
   auto f = k_cosamp<V, HAD>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   f<<<std::max(1, c.grid), CS_THREADS, smem, st>>>(k);

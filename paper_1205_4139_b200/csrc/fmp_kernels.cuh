@@ -113,7 +113,6 @@ struct CosArgs {
   double* resid;
   int32_t* aborted;
   uint64_t* hist_sup;       // batch x T x k, optional
-  uint64_t* hist_size;      // batch x T, optional (with hist_sup)
   void* hist;               // batch x T x n, optional
   double* mag_ws;           // grid x n
   void* h0_ws;              // grid x n
@@ -121,6 +120,7 @@ struct CosArgs {
   void* r_ws;               // grid x m
   int* queue;
   int grid;
+  unsigned long long* phase_ws;
 };
 
 // launchers (return cudaError_t); all async on `stream`

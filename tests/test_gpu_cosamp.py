@@ -51,8 +51,11 @@ def test_cosamp_golden(fmp):
 @pytest.mark.parametrize("kind", ["fourier", "hadamard"])
 @pytest.mark.parametrize("mode", ["conventional", "fast", "adaptive"])
 @pytest.mark.parametrize("n,m,k", [(64, 32, 4), (128, 64, 4), (256, 96, 8), (1024, 256, 16),
-                                   (4096, 1024, 32), (512, 128, 40), (64, 64, 40), (256, 16, 8)])
+                                   (4096, 1024, 32), (512, 128, 40), (64, 64, 40), (256, 16, 8),
+                                   (4096, 1024, 64)])
 def test_cosamp_matches_oracle(fmp, oracle, kind, mode, n, m, k):
+    # k = 64 at n = 4096 (config-2 shape): merged sets of up to 3k = 192 atoms
+    # exceed the shared-memory Cholesky (~166) and take the global-memory path
     op = None
     for seed in range(3):
         om = oracle.make_row_selection(n, m, oracle.derive_seed(seed + 7 * n, 1))
