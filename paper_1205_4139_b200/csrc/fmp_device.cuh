@@ -351,11 +351,13 @@ __device__ __forceinline__ unsigned warp_min_u(unsigned v) {
 }
 
 // block-wide reductions; `red` needs 32 doubles of shared scratch.  Every
-// thread receives the result.  Contains two __syncthreads().
+// thread receives the result.  Contains two __syncthreads(); LEAD = false
+// drops the leading one when the caller knows `red` is not being read.
+template <bool LEAD = true>
 __device__ __forceinline__ double block_max(double v, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   v = warp_max(v);
-  __syncthreads();
+  if (LEAD) __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   double r = lane < nw ? red[lane] : 0.0;
@@ -387,10 +389,11 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
   b = warp_sum(lane < nw ? red[32 + lane] : 0.0);
   c = warp_sum(lane < nw ? red[64 + lane] : 0.0);
 }
+template <bool LEAD = true>
 __device__ __forceinline__ unsigned block_min_u(unsigned v, unsigned* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   v = warp_min_u(v);
-  __syncthreads();
+  if (LEAD) __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   unsigned r = lane < nw ? red[lane] : 0xffffffffu;

@@ -29,6 +29,7 @@ namespace {
 constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
 constexpr int OLOGP = 3;
 constexpr int LSG = 8;  // threads per row / column in the least-squares passes
+constexpr int LSU = 4;  // loads per thread issued together in those passes
 
 struct OmpK {
   DevOp op;
@@ -313,7 +314,9 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           }
         }
         // identification with the tie band (solvers.cpp:90-101, :362-367)
-        best = block_max(best, red);
+        // `red` was last read before the least-squares pass-2 barrier (or the
+        // transform's barriers at t = 1): no leading barrier needed
+        best = block_max<false>(best, red);
         mark(fast_row ? 1 : 0);
         if (best == 0.0) break;
         const double cut = best * (1.0 - kTieBandRel);
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           for (int k = tid; k < n; k += nth)
             if (msc[k] >= cut) { first = (unsigned)k; break; }
         }
-        const unsigned pick = block_min_u(first, redu);
+        const unsigned pick = block_min_u<false>(first, redu);  // redu: only used here
         // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
         if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
         // b_s = h0[pick], read early so its latency hides behind the row pass
@@ -347,10 +350,25 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           const int i = base + tid / LSG, q = tid % LSG;
           double ar = 0.0, ai = 0.0;
           if (i < s)
-            for (int j = q; j <= i; j += LSG) {
-              const double2 w = W[wofs(T, i, j)], v = gram_of(s_lam[j], pick);
-              ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
-              ai = fma(w.x, v.y, fma(w.y, v.x, ai));
+            for (int j0 = q; j0 <= i; j0 += LSG * LSU) {
+              // fixed-size predicated chunk: all loads issue before the FMAs
+              double2 w[LSU], v[LSU];
+#pragma unroll
+              for (int u = 0; u < LSU; ++u) {
+                const int j = j0 + LSG * u;
+                if (j <= i) {
+                  w[u] = W[wofs(T, i, j)];
+                  v[u] = gram_of(s_lam[j], pick);
+                } else {
+                  w[u] = make_double2(0.0, 0.0);
+                  v[u] = w[u];
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < LSU; ++u) {
+                ar = fma(w[u].x, v[u].x, fma(-w[u].y, v[u].y, ar));
+                ai = fma(w[u].x, v[u].y, fma(w[u].y, v[u].x, ai));
+              }
             }
 #pragma unroll
           for (int o = LSG / 2; o; o >>= 1) {
@@ -384,9 +402,11 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
         if (!(d2 > 1e-12 * gamma)) { aborted = 1; break; }
-        const double d = sqrt(d2);
+        // one reciprocal square root instead of a sqrt and per-element
+        // divisions (fp64 division / sqrt are long software sequences)
+        const double invd = rsqrt(d2);
         const double2 bnew = to_c128(bpre);
-        const double2 znew = make_double2((bnew.x - lzr) / d, (bnew.y - lzi) / d);
+        const double2 znew = make_double2((bnew.x - lzr) * invd, (bnew.y - lzi) * invd);
         // new row of W, one pass per column j < s (eight threads each; column
         // j of the packed W is contiguous): W_sj = -(1/d) sum_{i=j}^{s-1}
         // conj(l_i) W_ij.  Older rows never change, so x = W^H z only gains
@@ -396,10 +416,24 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           double ar = 0.0, ai = 0.0;
           if (j < s) {
             const double2* Wc = W + wofs(T, j, j);
-            for (int i = j + q; i < s; i += LSG) {
-              const double2 l = s_l[i], w = Wc[i - j];
-              ar = fma(l.x, w.x, fma(l.y, w.y, ar));  // conj(l) w
-              ai = fma(l.x, w.y, fma(-l.y, w.x, ai));
+            for (int i0 = j + q; i0 < s; i0 += LSG * LSU) {
+              double2 l[LSU], w[LSU];
+#pragma unroll
+              for (int u = 0; u < LSU; ++u) {
+                const int i = i0 + LSG * u;
+                if (i < s) {
+                  l[u] = s_l[i];
+                  w[u] = Wc[i - j];
+                } else {
+                  l[u] = make_double2(0.0, 0.0);
+                  w[u] = l[u];
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < LSU; ++u) {
+                ar = fma(l[u].x, w[u].x, fma(l[u].y, w[u].y, ar));  // conj(l) w
+                ai = fma(l[u].x, w[u].y, fma(-l[u].y, w[u].x, ai));
+              }
             }
           }
 #pragma unroll
@@ -408,7 +442,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
             ai += __shfl_xor_sync(0xffffffffu, ai, o);
           }
           if (j < s && q == 0) {
-            const double2 wn = make_double2(-ar / d, -ai / d);
+            const double2 wn = make_double2(-ar * invd, -ai * invd);
             W[wofs(T, s, j)] = wn;
             const double2 xo = s_x[j];
             const double xr = xo.x + wn.x * znew.x + wn.y * znew.y;
@@ -418,12 +452,12 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           }
         }
         if (tid == 0) {
-          W[wofs(T, s, s)] = make_double2(1.0 / d, 0.0);
+          W[wofs(T, s, s)] = make_double2(invd, 0.0);
           s_z[s] = znew;
           s_lam[s] = pick;
           s_sel[pick >> 5] |= 1u << (pick & 31);
           if (s_xmap) s_xmap[HAD ? (int)pick : (int)brev_n(pick, log2n)] = (int16_t)s;
-          const double2 xs = make_double2(znew.x / d, znew.y / d);
+          const double2 xs = make_double2(znew.x * invd, znew.y * invd);
           s_x[s] = xs;
           from_c128(make_double2(xs.x * xscale, xs.y * xscale), s_xn[s]);
         }
