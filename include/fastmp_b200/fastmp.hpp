@@ -176,6 +176,11 @@ struct ProblemInstance {
 };
 ProblemInstance make_instance(const SensingOperator& op, std::size_t k, double noise_stddev,
                               std::uint64_t seed);
+// text formats (sensing.hpp:84-87, solvers.hpp:115): the reference's layouts
+// and number formatting (%.17g pairs), so files are interchangeable
+SensingOperator make_operator(const ProblemInstance& inst);
+void save_instance(const ProblemInstance& inst, std::ostream& os);
+ProblemInstance load_instance(std::istream& is);
 
 // ----------------------------------------------------------------- kernel
 struct CorrelationKernel {
@@ -253,6 +258,8 @@ RecoveryResult cosamp_solve(const SensingOperator& op, const cvec& y, std::size_
 std::vector<RecoveryResult> cosamp_solve_batch(const SensingOperator& op,
                                                const std::vector<cvec>& ys, std::size_t k,
                                                const SolveConfig& cfg);
+
+void save_result(const RecoveryResult& result, std::ostream& os);
 
 cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
                    const cvec& y, LeastSquaresMethod method = LeastSquaresMethod::NormalEquations,

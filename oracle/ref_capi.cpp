@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <string>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -326,6 +328,57 @@ int fmpo_omp_solve_batch(int kind, uint64_t n, const uint64_t* omega,
     for (auto& th : pool) th.join();
     if (failed) throw std::runtime_error("batch solve failed");
   });
+}
+
+}  // extern "C"
+
+// ---- text formats (reference only: fixtures for the facade's I/O) --------
+namespace {
+int put_text(const std::string& t, char* buf, uint64_t cap, uint64_t* len) {
+  if (len) *len = t.size();
+  if (!buf || cap < t.size() + 1) return 3;
+  std::memcpy(buf, t.data(), t.size() + 1);
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+/* save_instance (sensing.cpp:160-168) of make_instance(op, k, noise, seed)
+ * with Omega = make_row_selection(n, m, derive_seed(seed, 1)) */
+int fmpo_ref_instance_text(int kind, uint64_t n, uint64_t m, uint64_t k, double noise,
+                           uint64_t seed, char* buf, uint64_t cap, uint64_t* len) {
+  int st = 0;
+  const int g = guard([&] {
+    const SensingOperator op(StructuredUnitary(kind == 0 ? TransformKind::Fourier
+                                                         : TransformKind::Hadamard, n),
+                             make_row_selection(n, m, derive_seed(seed, 1)));
+    std::ostringstream os;
+    save_instance(make_instance(op, k, noise, seed), os);
+    st = put_text(os.str(), buf, cap, len);
+  });
+  return g ? g : st;
+}
+
+/* load_instance -> omp_solve(default_config(k, |y|), mode) -> save_result
+ * (solvers.cpp:546-562) and costs.write_csv (cost_model.cpp:98-113) */
+int fmpo_ref_result_text(const char* instance, int mode, char* buf, uint64_t cap, uint64_t* len,
+                         char* csv, uint64_t csvcap, uint64_t* csvlen) {
+  int st = 0;
+  const int g = guard([&] {
+    std::istringstream is(instance);
+    const ProblemInstance inst = load_instance(is);
+    const SensingOperator op = make_operator(inst);
+    SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
+    cfg.correlation_mode = mode_of(mode);
+    const RecoveryResult res = omp_solve(op, inst.y, cfg);
+    std::ostringstream os, oc;
+    save_result(res, os);
+    res.costs.write_csv(oc);
+    st = put_text(os.str(), buf, cap, len);
+    if (!st) st = put_text(oc.str(), csv, csvcap, csvlen);
+  });
+  return g ? g : st;
 }
 
 }  // extern "C"

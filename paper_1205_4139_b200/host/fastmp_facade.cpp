@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <mutex>
+#include <istream>
 #include <ostream>
 
 #include "fmp.h"
@@ -293,6 +294,87 @@ ProblemInstance make_instance(const SensingOperator& op, std::size_t k, double n
   inst.y = op.apply(inst.x_true);
   for (std::size_t i = 0; i < inst.m; ++i) inst.y[i] += inst.noise[i];
   return inst;
+}
+
+// ------------------------------------------------------------ text formats
+namespace {
+void append_pairs(std::ostream& os, const cvec& v) {
+  char buf[64];
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    std::snprintf(buf, sizeof(buf), "%.17g %.17g", v[i].real(), v[i].imag());
+    if (i) os << ' ';
+    os << buf;
+  }
+  os << '\n';
+}
+
+cvec read_pairs(std::istream& is, std::size_t count, const char* what) {
+  cvec v(count);
+  for (auto& z : v) {
+    double re = 0.0, im = 0.0;
+    if (!(is >> re >> im)) throw std::runtime_error(std::string("instance parse: bad ") + what);
+    z = cplx(re, im);
+  }
+  return v;
+}
+}  // namespace
+
+SensingOperator make_operator(const ProblemInstance& inst) {
+  return SensingOperator(StructuredUnitary(inst.kind, inst.n), make_row_selection(inst.n, inst.omega));
+}
+
+// sensing.cpp:160-168: header "n m k seed kind", the 1-based rows, then x
+// and y as %.17g pairs, one line each
+void save_instance(const ProblemInstance& inst, std::ostream& os) {
+  os << inst.n << ' ' << inst.m << ' ' << inst.k << ' ' << inst.seed << ' ' << to_string(inst.kind)
+     << '\n';
+  for (std::size_t i = 0; i < inst.omega.size(); ++i) {
+    if (i) os << ' ';
+    os << inst.omega[i];
+  }
+  os << '\n';
+  append_pairs(os, inst.x_true);
+  append_pairs(os, inst.y);
+}
+
+// sensing.cpp:170-193; the noise is recovered as y - apply(x_true) (on the GPU)
+ProblemInstance load_instance(std::istream& is) {
+  ProblemInstance inst;
+  std::string kind;
+  if (!(is >> inst.n >> inst.m >> inst.k >> inst.seed >> kind))
+    throw std::runtime_error("instance parse: bad header");
+  inst.kind = parse_kind(kind);
+  if (inst.n == 0 || inst.m == 0 || inst.m > inst.n)
+    throw std::runtime_error("instance parse: bad dimensions");
+  inst.omega.resize(inst.m);
+  for (auto& w : inst.omega)
+    if (!(is >> w)) throw std::runtime_error("instance parse: bad row indices");
+  inst.x_true = read_pairs(is, inst.n, "x_true");
+  inst.y = read_pairs(is, inst.m, "y");
+  const cvec clean = make_operator(inst).apply(inst.x_true);
+  inst.noise.resize(inst.m);
+  for (std::size_t i = 0; i < inst.m; ++i) inst.noise[i] = inst.y[i] - clean[i];
+  return inst;
+}
+
+// solvers.cpp:546-562
+void save_result(const RecoveryResult& result, std::ostream& os) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.17g", result.residual_norm);
+  os << result.x_hat.size() << ' ' << result.support.size() << ' ' << result.iterations_run << ' '
+     << buf << ' ' << (result.rank_deficient_abort ? 1 : 0) << ' ' << to_string(result.costs.kind)
+     << '\n';
+  for (std::size_t i = 0; i < result.support.size(); ++i) {
+    if (i) os << ' ';
+    os << result.support[i];
+  }
+  os << '\n';
+  for (std::size_t i = 0; i < result.coeffs.size(); ++i) {
+    std::snprintf(buf, sizeof(buf), "%.17g %.17g", result.coeffs[i].real(), result.coeffs[i].imag());
+    if (i) os << ' ';
+    os << buf;
+  }
+  os << '\n';
 }
 
 // ----------------------------------------------------------------- kernel

@@ -8,7 +8,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
 #include <functional>
+#include <sstream>
 #include <string>
 
 #include "fastmp_b200/fastmp.hpp"
@@ -279,6 +281,89 @@ int main(int argc, char** argv) {
           CHECK(l2_distance(b.correlation_history[i], a.correlation_history[i]) <=
                 1e-10 * std::max(l2_norm(a.correlation_history[i]), 1e-300));
       }
+  }
+  // text formats against the reference's own files (tests/golden/*.txt, *.csv
+  // written by save_instance / save_result / write_csv, make_golden.py)
+  if (argc > 2) {
+    const std::string dir = argv[2];
+    auto slurp = [](const std::string& path) {
+      std::ifstream f(path, std::ios::binary);
+      std::ostringstream o;
+      o << f.rdbuf();
+      return o.str();
+    };
+    const char* stems[] = {"fourier_64_32_4_11", "hadamard_64_32_4_12", "fourier_256_64_8_13",
+                           "hadamard_1024_256_16_14"};
+    int files = 0;
+    for (const char* stem : stems) {
+      const std::string want = slurp(dir + "/instance_" + stem + ".txt");
+      if (want.empty()) continue;
+      ++files;
+      std::istringstream is(want);
+      const ProblemInstance inst = load_instance(is);
+      std::ostringstream os;
+      save_instance(inst, os);
+      CHECK(os.str() == want);  // byte-for-byte round trip
+      double nn = 0.0;
+      for (const cplx& z : inst.noise) nn += std::norm(z);
+      CHECK(std::sqrt(nn) < 0.2 * std::sqrt(double(inst.m)));  // noise recovered by apply()
+      const SensingOperator op = make_operator(inst);
+      for (const char* mode : {"conventional", "fast"}) {
+        SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
+        cfg.correlation_mode = parse_mode(mode);
+        const RecoveryResult res = omp_solve(op, inst.y, cfg);
+        std::ostringstream ro;
+        save_result(res, ro);
+        std::istringstream got(ro.str()), ref(slurp(dir + "/result_" + stem + "_" + mode + ".txt"));
+        std::size_t gn, gs, gi, rn_, rs, ri;
+        double gr, rr;
+        int ga, ra;
+        std::string gk, rk;
+        got >> gn >> gs >> gi >> gr >> ga >> gk;
+        ref >> rn_ >> rs >> ri >> rr >> ra >> rk;
+        CHECK(gn == rn_ && gs == rs && gi == ri && ga == ra && gk == rk);
+        CHECK(std::abs(gr - rr) <= 1e-10 * l2_norm(inst.y));
+        bool same = true;
+        for (std::size_t j = 0; j < rs; ++j) {
+          std::size_t a = 0, b = 0;
+          got >> a;
+          ref >> b;
+          same &= a == b;
+        }
+        CHECK(same);
+        double err = 0.0, nrm = 0.0;
+        for (std::size_t j = 0; j < 2 * rs; ++j) {
+          double a = 0.0, b = 0.0;
+          got >> a;
+          ref >> b;
+          err += (a - b) * (a - b);
+          nrm += b * b;
+        }
+        CHECK(std::sqrt(err) <= 1e-10 * std::sqrt(nrm));
+        // cost CSV: the same rows (t, mode, analytic flops, relative cost)
+        std::ostringstream co;
+        res.costs.write_csv(co);
+        std::istringstream gc(co.str()), rc(slurp(dir + "/costs_" + stem + "_" + mode + ".csv"));
+        std::string gl, rl;
+        bool rows_ok = true;
+        while (std::getline(rc, rl)) {
+          if (!std::getline(gc, gl)) { rows_ok = false; break; }
+          if (rl.rfind("#", 0) == 0) continue;  // counted totals: analytic here
+          auto cols = [](const std::string& l) {
+            std::vector<std::string> v;
+            std::stringstream ss(l);
+            std::string c;
+            while (std::getline(ss, c, ',')) v.push_back(c);
+            return v;
+          };
+          const auto a = cols(gl), b = cols(rl);
+          rows_ok &= a.size() == 5 && b.size() == 5 && a[0] == b[0] && a[1] == b[1] &&
+                     a[2] == b[2] && a[4] == b[4];
+        }
+        CHECK(rows_ok);
+      }
+    }
+    CHECK(files == 4);
   }
   std::printf("facade test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;

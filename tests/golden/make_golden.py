@@ -10,18 +10,19 @@ oracle/ref_capi.cpp; nothing here is computed by this repository's code.
 The recipes follow the reference's own tests (cited per block).
 """
 import os
+import subprocess
 import sys
-
-import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from oracle import Oracle  # noqa: E402
+if "--text" not in sys.argv:
+    from oracle import Oracle  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 
 def main():
+    import numpy as np
     R = Oracle("reference")
     assert R.impl() == "reference"
     g = {}
@@ -130,7 +131,47 @@ def main():
     g["cos_count"] = np.array([len(cos)])
     np.savez_compressed(os.path.join(OUT, "reference_golden.npz"), **g)
     print("wrote", os.path.join(OUT, "reference_golden.npz"))
+    # the reference library links libstdc++ statically (the image's $CXX);
+    # its iostreams must not meet the libstdc++ numpy loads: separate process
+    subprocess.run([sys.executable, os.path.abspath(__file__), "--text"], check=True)
+
+
+def text_fixtures():
+    """Instance / result / cost-CSV text written by the reference's
+    save_instance, save_result and CostReport::write_csv (SURVEY §8 f2)."""
+    import ctypes as C
+    L = C.CDLL(os.path.join(ROOT, "oracle", "_ref", "libfmp_ref.so"))
+    L.fmpo_ref_instance_text.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                         C.c_uint64, C.c_char_p, C.c_uint64,
+                                         C.POINTER(C.c_uint64)]
+    L.fmpo_ref_result_text.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_uint64,
+                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64,
+                                       C.POINTER(C.c_uint64)]
+    cases = [("fourier", 64, 32, 4, 0.0, 11), ("hadamard", 64, 32, 4, 0.05, 12),
+             ("fourier", 256, 64, 8, 0.05, 13), ("hadamard", 1024, 256, 16, 0.0, 14)]
+    for kind, n, m, k, noise, seed in cases:
+        buf = C.create_string_buffer(1 << 22)
+        ln = C.c_uint64()
+        assert L.fmpo_ref_instance_text(0 if kind == "fourier" else 1, n, m, k, noise, seed, buf,
+                                        len(buf), C.byref(ln)) == 0
+        inst = buf.value
+        stem = f"{kind}_{n}_{m}_{k}_{seed}"
+        with open(os.path.join(OUT, f"instance_{stem}.txt"), "wb") as f:
+            f.write(inst)
+        for mode, code in (("conventional", 0), ("fast", 1)):
+            rb = C.create_string_buffer(1 << 20)
+            cb = C.create_string_buffer(1 << 20)
+            assert L.fmpo_ref_result_text(inst, code, rb, len(rb), C.byref(ln), cb, len(cb),
+                                          C.byref(ln)) == 0
+            with open(os.path.join(OUT, f"result_{stem}_{mode}.txt"), "wb") as f:
+                f.write(rb.value)
+            with open(os.path.join(OUT, f"costs_{stem}_{mode}.csv"), "wb") as f:
+                f.write(cb.value)
+    print("wrote text fixtures")
 
 
 if __name__ == "__main__":
-    main()
+    if "--text" in sys.argv:
+        text_fixtures()
+    else:
+        main()

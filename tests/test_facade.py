@@ -25,14 +25,16 @@ def test_facade_builds_and_exports():
     out = subprocess.run(["nm", "-DC", "--defined-only", os.path.join(PKG, "libfastmp_b200.so")],
                          capture_output=True, text=True).stdout
     for sym in ("fastmp::omp_solve(", "fastmp::fast_update(", "fastmp::compute_kernel(",
-                "fastmp::least_squares(", "fastmp::cosamp_solve(", "fastmp::SensingOperator::apply_adjoint("):
+                "fastmp::least_squares(", "fastmp::cosamp_solve(",
+                "fastmp::save_instance(", "fastmp::load_instance(", "fastmp::save_result(", "fastmp::SensingOperator::apply_adjoint("):
         assert sym in out, sym
 
 
 @pytest.mark.gpu
 def test_facade_reference_recipes(oracle):
     exe = build_exe()
-    r = subprocess.run([exe, os.path.join(ROOT, "oracle", "_build", "libfmp_oracle.so")],
+    r = subprocess.run([exe, os.path.join(ROOT, "oracle", "_build", "libfmp_oracle.so"),
+                        os.path.join(ROOT, "tests", "golden")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
