@@ -108,65 +108,102 @@ extern "C" int fmp_make_batch(int kind, uint64_t n, const uint64_t* rows, uint64
       k >= m || noise_stddev < 0.0 || !rows || !y_out)
     return FMP_EINVAL;
   const double isn = 1.0 / std::sqrt(static_cast<double>(n));
+  unsigned w = threads > 0 ? unsigned(threads) : std::max(1u, std::thread::hardware_concurrency());
+  // run f(lo, hi) over [0, count) in w contiguous chunks
+  auto par = [&](uint64_t count, unsigned nt, auto&& f) {
+    nt = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(nt, count)));
+    std::vector<std::thread> pool;
+    const uint64_t chunk = (count + nt - 1) / nt;
+    for (unsigned t = 1; t < nt; ++t)
+      pool.emplace_back([&, t] { f(std::min(count, t * chunk), std::min(count, (t + 1) * chunk)); });
+    f(0, std::min(count, chunk));
+    for (auto& th : pool) th.join();
+  };
   std::vector<cplx> tw;
   if (kind == FMP_FOURIER) {
     tw.resize(n);
-    for (uint64_t e = 0; e < n; ++e) {
-      const double th = -kTwoPi * static_cast<double>(e) / static_cast<double>(n);
-      tw[e] = cplx(isn * std::cos(th), isn * std::sin(th));
-    }
+    par(n, w, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t e = lo; e < hi; ++e) {
+        const double th = -kTwoPi * static_cast<double>(e) / static_cast<double>(n);
+        tw[e] = cplx(isn * std::cos(th), isn * std::sin(th));
+      }
+    });
   }
-  auto one = [&](uint64_t b) {
+  // the draws of one signal, in make_instance's order (sensing.cpp:132-147)
+  struct Draw {
+    std::vector<uint64_t> sup;
+    std::vector<cplx> xs, noise;
+    double nn = 0.0;
+  };
+  auto draw = [&](uint64_t b) {
+    Draw d;
     Rng rng(fmp_derive_seed(base_seed, first + b));
-    const auto sup = rng.sample(n, k);
-    std::vector<cplx> xs(k);
+    d.sup = rng.sample(n, k);
+    d.xs.resize(k);
     for (uint64_t i = 0; i < k; ++i) {
       const cplx z = rng.cgauss();
-      xs[i] = real ? cplx(std::sqrt(2.0) * z.real(), 0.0) : z;
+      d.xs[i] = real ? cplx(std::sqrt(2.0) * z.real(), 0.0) : z;
     }
-    double* y = y_out + 2 * m * b;
-    double nn = 0.0;
-    std::vector<cplx> noise(m, cplx(0.0));
+    d.noise.assign(m, cplx(0.0));
     if (!real && noise_stddev > 0.0) {
       const double sc = noise_stddev * std::sqrt(2.0);
       for (uint64_t i = 0; i < m; ++i) {
-        noise[i] = rng.cgauss() * sc;
-        nn += std::norm(noise[i]);
+        d.noise[i] = rng.cgauss() * sc;
+        d.nn += std::norm(d.noise[i]);
       }
     }
-    for (uint64_t i = 0; i < m; ++i) {
+    return d;
+  };
+  // y rows [lo, hi) of signal b synthesised from its K nonzeros
+  auto synth = [&](const Draw& d, uint64_t b, uint64_t lo, uint64_t hi) {
+    double* y = y_out + 2 * m * b;
+    for (uint64_t i = lo; i < hi; ++i) {
       const uint64_t a = rows[i] - 1;
       cplx acc(0.0);
       for (uint64_t j = 0; j < k; ++j) {
-        const uint64_t c = sup[j] - 1;
+        const uint64_t c = d.sup[j] - 1;
         if (kind == FMP_FOURIER)
-          acc += xs[j] * tw[(a * c) % n];
+          acc += d.xs[j] * tw[(a * c) & (n - 1)];
         else
-          acc += xs[j] * ((__builtin_popcountll(a & c) & 1) ? -isn : isn);
+          acc += d.xs[j] * ((__builtin_popcountll(a & c) & 1) ? -isn : isn);
       }
-      acc += noise[i];
+      acc += d.noise[i];
       y[2 * i] = acc.real();
       y[2 * i + 1] = acc.imag();
     }
+  };
+  auto finish = [&](const Draw& d, uint64_t b) {
     if (x_out) {
       double* x = x_out + 2 * n * b;
       std::fill(x, x + 2 * n, 0.0);
       for (uint64_t j = 0; j < k; ++j) {
-        x[2 * (sup[j] - 1)] = xs[j].real();
-        x[2 * (sup[j] - 1) + 1] = xs[j].imag();
+        x[2 * (d.sup[j] - 1)] = d.xs[j].real();
+        x[2 * (d.sup[j] - 1) + 1] = d.xs[j].imag();
       }
     }
-    if (noise_norm_out) noise_norm_out[b] = std::sqrt(nn);
+    if (noise_norm_out) noise_norm_out[b] = std::sqrt(d.nn);
   };
-  unsigned w = threads > 0 ? unsigned(threads) : std::max(1u, std::thread::hardware_concurrency());
-  w = unsigned(std::min<uint64_t>(w, std::max<uint64_t>(batch, 1)));
-  std::atomic<uint64_t> next{0};
-  auto work = [&] {
-    for (uint64_t b; (b = next.fetch_add(1)) < batch;) one(b);
-  };
-  std::vector<std::thread> pool;
-  for (unsigned i = 1; i < w; ++i) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  if (batch >= w) {
+    // many signals: one signal per thread at a time
+    std::atomic<uint64_t> next{0};
+    auto work = [&] {
+      for (uint64_t b; (b = next.fetch_add(1)) < batch;) {
+        const Draw d = draw(b);
+        synth(d, b, 0, m);
+        finish(d, b);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned i = 1; i < w; ++i) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  } else {
+    // few (large) signals: the rows of each signal split over the threads
+    for (uint64_t b = 0; b < batch; ++b) {
+      const Draw d = draw(b);
+      par(m, w, [&](uint64_t lo, uint64_t hi) { synth(d, b, lo, hi); });
+      finish(d, b);
+    }
+  }
   return FMP_OK;
 }
