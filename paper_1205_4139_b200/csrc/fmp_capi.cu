@@ -297,6 +297,31 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
     while (k < m && spos[k] < i * 256) ++k;
     soff[i] = (uint32_t)k;
   }
+  // two-pass transform lists (n = N1 N2): Omega by column for the scatter,
+  // by output row for the gather (fmp_transform_4s.cu)
+  d.fs_l1 = fmp::fs_split(d.log2n);
+  std::vector<uint32_t> fa_off, fa_pos, fa_row, fb_off, fb_pos, fb_row;
+  if (d.fs_l1) {
+    const int L1 = d.fs_l1, L2 = d.log2n - L1;
+    const uint32_t N1 = 1u << L1, N2 = 1u << L2;
+    auto build = [&](auto key, uint32_t groups, std::vector<uint32_t>& off,
+                     std::vector<uint32_t>& pos, std::vector<uint32_t>& row) {
+      off.assign(groups + 1, 0);
+      for (uint64_t i = 0; i < m; ++i) off[key(om[i]) + 1]++;
+      for (uint32_t g = 0; g < groups; ++g) off[g + 1] += off[g];
+      std::vector<uint32_t> fill(off.begin(), off.end() - 1);
+      pos.resize(m);
+      row.resize(m);
+      for (uint64_t i = 0; i < m; ++i) {
+        const uint32_t q = fill[key(om[i])]++;
+        pos[q] = om[i];
+        row[q] = (uint32_t)i;
+      }
+    };
+    build([&](uint32_t p) { return p & (N2 - 1); }, N2, fa_off, fa_pos, fa_row);
+    if (kind == FMP_FOURIER) build([&](uint32_t p) { return p & (N1 - 1); }, N1, fb_off, fb_pos, fb_row);
+    else build([&](uint32_t p) { return p >> L2; }, N1, fb_off, fb_pos, fb_row);
+  }
   cudaError_t e = cudaSuccess;
 #define OPALLOC(p, bytes) \
   if ((e = cudaMalloc(&p, (bytes))) != cudaSuccess) return cleanup(fail(FMP_ENOMEM, "operator alloc: %s", cudaGetErrorString(e)))
@@ -313,8 +338,24 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
     OPALLOC(d.gr64, n * 8);
     if (m <= 32767) OPALLOC(d.glat, n * 2);
   }
+  if (d.fs_l1) {
+    OPALLOC(d.fs_aoff, fa_off.size() * 4);
+    OPALLOC(d.fs_apos, m * 4);
+    OPALLOC(d.fs_arow, m * 4);
+    OPALLOC(d.fs_boff, fb_off.size() * 4);
+    OPALLOC(d.fs_bpos, m * 4);
+    OPALLOC(d.fs_brow, m * 4);
+  }
 #undef OPALLOC
   cudaStream_t st = ctx->cur;
+  if (d.fs_l1 &&
+      ((e = cudaMemcpyAsync(d.fs_aoff, fa_off.data(), fa_off.size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+       (e = cudaMemcpyAsync(d.fs_apos, fa_pos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+       (e = cudaMemcpyAsync(d.fs_arow, fa_row.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+       (e = cudaMemcpyAsync(d.fs_boff, fb_off.data(), fb_off.size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+       (e = cudaMemcpyAsync(d.fs_bpos, fb_pos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+       (e = cudaMemcpyAsync(d.fs_brow, fb_row.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess))
+    return cleanup(fail(FMP_ECUDA, "two-pass lists: %s", cudaGetErrorString(e)));
   int launches = 0;
   if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(d.scat_pos, spos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
@@ -353,7 +394,8 @@ int fmp_operator_destroy(fmp_op op) {
   cudaStreamSynchronize(op->ctx->cur);
   DevOp& d = op->d;
   for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.scat_off, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
-                  (void*)d.gr64, (void*)d.glat})
+                  (void*)d.gr64, (void*)d.glat, (void*)d.fs_aoff, (void*)d.fs_apos, (void*)d.fs_arow,
+                  (void*)d.fs_boff, (void*)d.fs_bpos, (void*)d.fs_brow})
     if (p) cudaFree(p);
   delete op;
   return FMP_OK;
@@ -979,9 +1021,30 @@ int lg_local_best(fmp_large_s* lg, double* best) {
 // explicit residual r = y - Phi_Lambda x (replicated on every shard)
 int lg_residual(fmp_large_s* lg, double* rn) {
   cudaStream_t st = lg_stream(lg);
-  CU(cudaMemsetAsync(lg->xdense, 0, (size_t)lg->n * lg->eb, st));
-  CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, lg->s, st));
-  if (int e = run_transform(lg->op, lg->dtype, 0, 0, 1, lg->xdense, lg->ax, 1, nullptr, st)) return e;
+  if (lg->op->d.fs_l1) {
+    // two-pass forward transform straight from the sparse estimate, gathered
+    // at Omega (no dense scatter, fmp_transform_4s.cu)
+    fmp_ctx_s* ctx = lg->op->ctx;
+    void* w;
+    ALLOC(w, S_WORK, (size_t)lg->n * lg->eb);
+    fmp::FsTransform t{};
+    t.op = &lg->op->d;
+    t.dtype = lg->dtype;
+    t.inverse = 0;
+    t.in_mode = 2;
+    t.lam = lg->lam;
+    t.xs = lg->x;
+    t.cnt = lg->s;
+    t.mid = w;
+    t.out_mode = 1;
+    t.out = lg->ax;
+    t.batch = 1;
+    CU(fmp::launch_transform_fs(t, st));
+  } else {
+    CU(cudaMemsetAsync(lg->xdense, 0, (size_t)lg->n * lg->eb, st));
+    CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, lg->s, st));
+    if (int e = run_transform(lg->op, lg->dtype, 0, 0, 1, lg->xdense, lg->ax, 1, nullptr, st)) return e;
+  }
   CU(fmp::lg_launch_resid(lg->dtype, lg->y, lg->ax, lg->r, lg->m, lg->part, lg->dval, st));
   double r2 = 0;
   CU(cudaMemcpyAsync(&r2, lg->dval, 8, cudaMemcpyDeviceToHost, st));

@@ -33,6 +33,16 @@ struct DevOp {
   uint32_t* scat_pos = nullptr;  // m, ascending slots
   uint32_t* scat_row = nullptr;  // m, index into the m-vector for each slot
   uint32_t* scat_off = nullptr;  // n/256 + 1: number of slots below 256 i (n >= 256)
+  // two-pass transform (n = N1 N2, N1 = 2^fs_l1; fmp_transform_4s.cu), n >= 2^18:
+  // Omega sorted by column (pos mod N2) for the pass-A scatter and by output
+  // row k1 for the pass-B gather, each with per-column / per-row offsets
+  int fs_l1 = 0;
+  uint32_t* fs_aoff = nullptr;  // N2 + 1
+  uint32_t* fs_apos = nullptr;  // m
+  uint32_t* fs_arow = nullptr;  // m
+  uint32_t* fs_boff = nullptr;  // N1 + 1
+  uint32_t* fs_bpos = nullptr;  // m
+  uint32_t* fs_brow = nullptr;  // m
 };
 
 struct TransformArgs {
@@ -47,6 +57,22 @@ struct TransformArgs {
   uint64_t* argmax_out;  // optional: band argmax of |out|^2 per vector (dense out only)
   void* work;            // batch x n scratch, required when n > transform_max_n(dtype)
   int* sync;             // 32 + batch ints of scratch (job-queue path), optional
+};
+
+// two-pass transform of `batch` vectors (see fmp_transform_4s.cu)
+struct FsTransform {
+  const DevOp* op;
+  int dtype;
+  int inverse;
+  int in_mode;              // 0 dense n, 1 m values at Omega, 2 sparse (lam, xs; batch 1)
+  const void* in;
+  const uint32_t* lam;      // in_mode 2: 0-based positions
+  const double2* xs;        // in_mode 2: values (fp64)
+  int cnt;
+  void* mid;                // batch x n scratch
+  int out_mode;             // 0 dense n, 1 gathered at Omega (m)
+  void* out;
+  int64_t batch;
 };
 
 struct FastUpdateArgs {
@@ -125,6 +151,8 @@ struct CosArgs {
 
 // launchers (return cudaError_t); all async on `stream`
 cudaError_t launch_transform(const TransformArgs& a, cudaStream_t stream);
+cudaError_t launch_transform_fs(const FsTransform& t, cudaStream_t stream);
+int fs_split(int log2n);  // N1 = 2^fs_split rows of the two-pass transform, 0: not used
 cudaError_t launch_fast_update(const FastUpdateArgs& a, cudaStream_t stream);
 cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t stream);
 cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t stream);

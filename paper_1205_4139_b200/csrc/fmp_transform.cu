@@ -507,6 +507,27 @@ cudaError_t launch_tr_global(const TransformArgs& a, cudaStream_t st) {
 
 template <class V, bool HAD>
 cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
+  if (a.op->n > transform_max_n(a.dtype) && a.op->fs_l1 && a.work && a.out) {
+    // two passes over HBM (n >= 2^18; fmp_transform_4s.cu)
+    FsTransform t{};
+    t.op = a.op;
+    t.dtype = a.dtype;
+    t.inverse = a.inverse;
+    t.in_mode = a.in_omega ? 1 : 0;
+    t.in = a.in;
+    t.mid = a.work;
+    t.out_mode = a.out_omega ? 1 : 0;
+    t.out = a.out;
+    t.batch = a.batch;
+    cudaError_t e = launch_transform_fs(t, st);
+    if (e != cudaSuccess) return e;
+    if (a.argmax_out && !a.out_omega) {
+      const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+      k_argmax<V><<<g2, 512, 0, st>>>((const V*)a.out, a.op->n, a.batch, a.argmax_out);
+      ++g_launches;
+    }
+    return cudaGetLastError();
+  }
   if (a.op->n > transform_max_n(a.dtype)) {
     const int k = a.op->scat_pos ? cluster_k<V>(a.op->n, a.dtype) : 0;
     const int kq = a.op->scat_pos ? queue_k<V>(a.op->n, a.dtype) : 0;

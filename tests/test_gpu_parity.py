@@ -58,8 +58,10 @@ def test_kernel_golden(fmp, gold):
 # ------------------------------------------------------------- transforms
 @pytest.mark.parametrize("kind", ["fourier", "hadamard"])
 @pytest.mark.parametrize("n,m", [(1, 1), (2, 1), (8, 3), (64, 16), (1024, 256), (4096, 1024),
-                                 (8192, 2048), (16384, 4096), (65536, 8192), (1 << 18, 1 << 15)])
+                                 (8192, 2048), (16384, 4096), (65536, 8192), (1 << 18, 1 << 15),
+                                 (1 << 20, 1 << 17), (1 << 22, 1 << 19)])
 def test_apply_adjoint_matches_oracle(fmp, oracle, kind, n, m):
+    # n >= 2^18 runs the two-pass transform (fmp_transform_4s.cu)
     om = oracle.make_row_selection(n, m, 7 + n)
     op = fmp.SensingOperator(kind, n, om)
     B = 3 if n <= 65536 else 1
@@ -86,7 +88,7 @@ def test_apply_adjoint_other_dtypes(fmp, oracle, dtype, tol):
     n, m = 65536, 8192
     om = oracle.make_row_selection(n, m, 3)
     kind = "fourier" if dtype == np.complex64 else "hadamard"
-    for n_, m_ in ((1024, 256), (n, m)):
+    for n_, m_ in ((1024, 256), (n, m), (1 << 20, 1 << 17)):
         om = oracle.make_row_selection(n_, m_, 3)
         op = fmp.SensingOperator(kind, n_, om)
         r = oracle.rng_complex_gaussian(5, m_)
