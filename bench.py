@@ -361,6 +361,8 @@ def large_arm(args, ws, rank, local):
     cfg = fmp.SolveConfig(T, float(tol_h[0]), mname, fast_until=fu)
 
     def solve():
+        if ws == 1:  # one shard: the whole loop in C (fmp_large_solve)
+            return fmp.large_solve(op, y, cfg, dtype=NP_DT[CFG["dtype"]])
         shard = fmp.LargeShard(op, cfg, rank, ws, dtype=NP_DT[CFG["dtype"]])
         res = fmp.sharded_solve([shard], y, float(tol_h[0]), exchange)
         shard.close()

@@ -976,7 +976,12 @@ struct fmp_large_s {
   uint32_t* lam = nullptr;
   double *part = nullptr, *scal = nullptr, *blkmax = nullptr, *dval = nullptr;
   unsigned long long* dfirst = nullptr;
+  double* drec = nullptr;  // pick record (k_lg_pick)
   bool own_gcm = false;
+  // one shard (fmp_large_solve): the first-in-band pick rides along with the
+  // local best, cut on the device (fewer host round trips per iteration)
+  bool fused = false, first_ready = false;
+  double first_rec[4] = {0, 0, 0, 0};
   // host state (mirrors omp_solve's loop variables, solvers.cpp:306-403)
   int t = 0, s = 0, iters = 0, aborted = 0;
   double yy = 0, tol = 0, rn = 0;
@@ -1013,13 +1018,39 @@ int lg_local_best(fmp_large_s* lg, double* best) {
   lg_view(lg, &base, &off, &stride);
   if (lg->view == 1) CU(fmp::lg_launch_reduce_max(lg->blkmax, lg->dval, st));
   else CU(fmp::lg_launch_max(lg->dtype, base, off, stride, lg->np, lg->blkmax, lg->dval, st));
+  if (lg->fused) {
+    // one shard: the band pick (solvers.cpp:90-101) with the cut taken from
+    // the device best, and h0 there, in the same round trip
+    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval,
+                            lg->view == 1 ? nullptr : lg->blkmax, lg->dfirst, st));
+    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
+    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    lg->first_ready = true;
+    *best = lg->first_rec[0];
+    return FMP_OK;
+  }
   CU(cudaMemcpyAsync(best, lg->dval, 8, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return FMP_OK;
 }
 
-// explicit residual r = y - Phi_Lambda x (replicated on every shard)
+// explicit residual r = y - Phi_Lambda x (replicated on every shard);
+// enqueued only, ||r||^2 left in dval
+// cnt: atoms in the estimate (lg->s, or lg->s + 1 right after LS appended one)
+int lg_residual_launch(fmp_large_s* lg, int cnt);
+
 int lg_residual(fmp_large_s* lg, double* rn) {
+  if (int e = lg_residual_launch(lg, lg->s)) return e;
+  cudaStream_t st = lg_stream(lg);
+  double r2 = 0;
+  CU(cudaMemcpyAsync(&r2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *rn = std::sqrt(r2);
+  return FMP_OK;
+}
+
+int lg_residual_launch(fmp_large_s* lg, int cnt) {
   cudaStream_t st = lg_stream(lg);
   if (lg->op->d.fs_l1) {
     // two-pass forward transform straight from the sparse estimate, gathered
@@ -1034,7 +1065,7 @@ int lg_residual(fmp_large_s* lg, double* rn) {
     t.in_mode = 2;
     t.lam = lg->lam;
     t.xs = lg->x;
-    t.cnt = lg->s;
+    t.cnt = cnt;
     t.mid = w;
     t.out_mode = 1;
     t.out = lg->ax;
@@ -1042,14 +1073,10 @@ int lg_residual(fmp_large_s* lg, double* rn) {
     CU(fmp::launch_transform_fs(t, st));
   } else {
     CU(cudaMemsetAsync(lg->xdense, 0, (size_t)lg->n * lg->eb, st));
-    CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, lg->s, st));
+    CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, cnt, st));
     if (int e = run_transform(lg->op, lg->dtype, 0, 0, 1, lg->xdense, lg->ax, 1, nullptr, st)) return e;
   }
   CU(fmp::lg_launch_resid(lg->dtype, lg->y, lg->ax, lg->r, lg->m, lg->part, lg->dval, st));
-  double r2 = 0;
-  CU(cudaMemcpyAsync(&r2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  *rn = std::sqrt(r2);
   return FMP_OK;
 }
 
@@ -1109,6 +1136,7 @@ int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
   A((void**)&lg->blkmax, (size_t)grid * 8);
   A((void**)&lg->dval, 64);
   A((void**)&lg->dfirst, 64);
+  A((void**)&lg->drec, 64);
   if (!st && lg->P > 1) {
     A(&lg->gcm, lg->n * eb);
     lg->own_gcm = true;
@@ -1195,29 +1223,28 @@ int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0
   CU(cudaSetDevice(lg->op->ctx->device));
   std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
   cudaStream_t st = lg_stream(lg);
-  const double cut = global_best * (1.0 - 1e-9);  // kTieBandRel, solvers.cpp:40
-  const void* base;
-  int64_t off, stride;
-  lg_view(lg, &base, &off, &stride);
-  CU(cudaMemsetAsync(lg->dfirst, 0xff, 8, st));
-  CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, lg->dfirst, st));
-  unsigned long long kp = 0;
-  CU(cudaMemcpyAsync(&kp, lg->dfirst, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  if (kp == ~0ull) {
+  if (!(lg->first_ready && global_best == lg->first_rec[0])) {
+    const double cut = global_best * (1.0 - 1e-9);  // kTieBandRel, solvers.cpp:40
+    const void* base;
+    int64_t off, stride;
+    lg_view(lg, &base, &off, &stride);
+    // chunk maxima from k_lg_max (not the fast kernel's partition) let it skip chunks
+    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, nullptr,
+                            lg->view == 1 ? nullptr : lg->blkmax, lg->dfirst, st));
+    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
+    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  lg->first_ready = false;
+  if (lg->first_rec[1] < 0.0) {
     *atom = 0;
     h0_at[0] = h0_at[1] = 0.0;
     return FMP_OK;
   }
+  const uint64_t kp = (uint64_t)lg->first_rec[1];
   *atom = (uint64_t)lg->p + (uint64_t)lg->P * kp + 1;
-  if (lg->dtype == FMP_C128) {
-    CU(cudaMemcpy(h0_at, (const char*)lg->h0s + kp * 16, 16, cudaMemcpyDeviceToHost));
-  } else {
-    float v[2];
-    CU(cudaMemcpy(v, (const char*)lg->h0s + kp * 8, 8, cudaMemcpyDeviceToHost));
-    h0_at[0] = v[0];
-    h0_at[1] = v[1];
-  }
+  h0_at[0] = lg->first_rec[2];
+  h0_at[1] = lg->first_rec[3];
   return FMP_OK;
 }
 
@@ -1254,15 +1281,22 @@ int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* don
     // least squares (replicated)
     CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
                          lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
-    double sc[3];
+    // a conventional next row needs the explicit residual whatever LS gives:
+    // enqueue it now so one round trip returns zz, the abort flag and ||r||^2
+    // (on an abort LS leaves x alone, so r is the previous state's residual)
+    const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
+    if (next_conv)
+      if (int e = lg_residual_launch(lg, lg->s + 1)) return e;
+    double sc[3] = {0, 0, 0};
     CU(cudaMemcpyAsync(sc, lg->scal + 2, 8, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(sc + 1, lg->scal + 6, 8, cudaMemcpyDeviceToHost, st));
+    if (next_conv) CU(cudaMemcpyAsync(sc + 2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (sc[1] != 0.0) {  // rank deficient: keep the previous state (solvers.cpp:380-385)
       lg->aborted = 1;
       lg->done = true;
       *done = 1;
-      if (!lg->rn_explicit) {
+      if (next_conv || !lg->rn_explicit) {  // (the early residual counted the rejected atom)
         if (int e = lg_residual(lg, &lg->rn)) return e;
         lg->rn_explicit = true;
       }
@@ -1274,11 +1308,13 @@ int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* don
     lg->iters = lg->t;
     const double zz = sc[0];
     // residual and halting (solvers.cpp:388-402)
-    const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
     const double r2id = lg->yy - zz;
     const double margin = lg->dtype == FMP_C128 ? 1e-10 : 1e-5;
     const bool near = !(r2id > lg->tol * lg->tol + margin * lg->yy);
-    if (next_conv || near) {
+    if (next_conv) {
+      lg->rn = std::sqrt(sc[2]);
+      lg->rn_explicit = true;
+    } else if (near) {
       if (int e = lg_residual(lg, &lg->rn)) return e;
       lg->rn_explicit = true;
     } else {
@@ -1330,6 +1366,7 @@ int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* c
   if (!op || !y || !cfg || !out) return fail(FMP_EINVAL, "null argument");
   fmp_large lg = nullptr;
   if (int e = fmp_large_create(op, dtype, 0, 1, cfg, &lg)) return e;
+  lg->fused = true;
   double best = 0.0;
   int st = fmp_large_begin(lg, y, cfg->tolerances ? cfg->tolerances[0] : cfg->tolerance, &best);
   int done = best < 0.0;

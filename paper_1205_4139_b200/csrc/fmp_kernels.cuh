@@ -178,7 +178,10 @@ cudaError_t lg_launch_max(int dtype, const void* base, int64_t off, int64_t stri
                           double* blkmax, double* out, cudaStream_t st);
 cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st);
 cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
-                            double cut, unsigned long long* first, cudaStream_t st);
+                            double cut, const double* cut_best, const double* blkmax,
+                            unsigned long long* first, cudaStream_t st);
+cudaError_t lg_launch_pick(int dtype, const double* best, const unsigned long long* first,
+                           const void* h0s, double* rec, cudaStream_t st);
 cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, double2* z, double2* l,
                          uint32_t* lam, void* xn, double* part, double* scal, int T, int s,
                          unsigned pick, double2 bnew, cudaStream_t st);

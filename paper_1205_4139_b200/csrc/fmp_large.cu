@@ -86,10 +86,13 @@ template <class V>
 __global__ void __launch_bounds__(LG_THREADS) k_lg_max(const V* __restrict__ base, int64_t off,
                                                        int64_t stride, int64_t cnt,
                                                        double* __restrict__ blkmax) {
+  // block b owns the contiguous chunk [b chunk, (b + 1) chunk): k_lg_first
+  // skips the chunks whose maximum is below the cut
   __shared__ double red[32];
+  const int64_t chunk = (cnt + gridDim.x - 1) / gridDim.x;
+  const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(cnt, k0 + chunk);
   double best = 0.0;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
-       k += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
     best = fmax(best, mag2(base[off + stride * k]));
   best = block_max(best, red);
   if (threadIdx.x == 0) blkmax[blockIdx.x] = best;
@@ -103,11 +106,28 @@ __global__ void k_lg_reduce_max(const double* __restrict__ part, int cnt, double
   if (threadIdx.x == 0) *out = b;
 }
 
-// smallest shard position k' with |v|^2 >= cut (atomicMin over the grid)
+// smallest shard position k' with |v|^2 >= cut (atomicMin over the grid);
+// with blkmax (k_lg_max's chunk maxima) only chunks reaching the cut scan
 template <class V>
 __global__ void __launch_bounds__(LG_THREADS) k_lg_first(const V* __restrict__ base, int64_t off,
                                                          int64_t stride, int64_t cnt, double cut,
+                                                         const double* __restrict__ cut_best,
+                                                         const double* __restrict__ blkmax,
                                                          unsigned long long* __restrict__ first) {
+  // cut_best: the best |h|^2 on the device (one shard: no host round trip);
+  // same double arithmetic as the host's best * (1 - 1e-9)
+  if (cut_best) cut = *cut_best * (1.0 - 1e-9);
+  if (blkmax) {
+    if (blkmax[blockIdx.x] < cut) return;
+    const int64_t chunk = (cnt + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(cnt, k0 + chunk);
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+      if (mag2(base[off + stride * k]) >= cut) {
+        atomicMin(first, (unsigned long long)k);
+        break;
+      }
+    return;
+  }
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
        k += (int64_t)gridDim.x * blockDim.x) {
     if (mag2(base[off + stride * k]) >= cut) {
@@ -115,6 +135,19 @@ __global__ void __launch_bounds__(LG_THREADS) k_lg_first(const V* __restrict__ b
       break;  // later k of this thread are larger
     }
   }
+}
+
+// the pick record [best, first (as a double, exact below 2^53), h0 re, h0 im]
+template <class V>
+__global__ void k_lg_pick(const double* __restrict__ best, const unsigned long long* __restrict__ first,
+                          const V* __restrict__ h0s, double* __restrict__ rec) {
+  const unsigned long long k = *first;
+  rec[0] = *best;
+  rec[1] = k == ~0ull ? -1.0 : (double)k;
+  double2 h = make_double2(0.0, 0.0);
+  if (k != ~0ull) h = to_c128(h0s[k]);
+  rec[2] = h.x;
+  rec[3] = h.y;
 }
 
 // ---- replicated least squares (same arithmetic as k_omp, deterministic)
@@ -140,32 +173,47 @@ __device__ __forceinline__ double2 lg_gram(const DevOp& op, unsigned a, unsigned
   else return op.g64[(a - b) & (unsigned)(op.n - 1)];
 }
 
-// l = W a (a_j = G(lambda_j, pick)), per-block partials of |l|^2 and l^H z
+// l = W a (a_j = G(lambda_j, pick)), one warp per row (lanes over j),
+// per-block partials of |l|^2 and l^H z (fixed order: identical on every shard)
 template <bool HAD>
 __global__ void __launch_bounds__(LG_THREADS) k_lg_ls_a(DevOp op, LgLs L, int s, unsigned pick) {
-  __shared__ double red[32];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double red[3][LG_THREADS / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * (LG_THREADS / 32) + w;
   double ll = 0.0, lzr = 0.0, lzi = 0.0;
   if (i < s) {
     double ar = 0.0, ai = 0.0;
-    for (int j = 0; j <= i; ++j) {
-      const double2 w = L.W[lg_wofs(L.T, i, j)], v = lg_gram<HAD>(op, L.lam[j], pick);
-      ar = fma(w.x, v.x, fma(-w.y, v.y, ar));
-      ai = fma(w.x, v.y, fma(w.y, v.x, ai));
+    for (int j = lane; j <= i; j += 32) {
+      const double2 wv = L.W[lg_wofs(L.T, i, j)], v = lg_gram<HAD>(op, L.lam[j], pick);
+      ar = fma(wv.x, v.x, fma(-wv.y, v.y, ar));
+      ai = fma(wv.x, v.y, fma(wv.y, v.x, ai));
     }
-    L.l[i] = make_double2(ar, ai);
-    const double2 zc = L.z[i];
-    ll = ar * ar + ai * ai;
-    lzr = ar * zc.x + ai * zc.y;
-    lzi = ar * zc.y - ai * zc.x;
+    ar = warp_sum(ar);
+    ai = warp_sum(ai);
+    if (lane == 0) {
+      L.l[i] = make_double2(ar, ai);
+      const double2 zc = L.z[i];
+      ll = ar * ar + ai * ai;
+      lzr = ar * zc.x + ai * zc.y;
+      lzi = ar * zc.y - ai * zc.x;
+    }
   }
-  ll = block_sum(ll, red);
-  lzr = block_sum(lzr, red);
-  lzi = block_sum(lzi, red);
+  if (lane == 0) {
+    red[0][w] = ll;
+    red[1][w] = lzr;
+    red[2][w] = lzi;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    L.part[3 * blockIdx.x] = ll;
-    L.part[3 * blockIdx.x + 1] = lzr;
-    L.part[3 * blockIdx.x + 2] = lzi;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int q = 0; q < LG_THREADS / 32; ++q) {
+      a += red[0][q];
+      b += red[1][q];
+      c += red[2][q];
+    }
+    L.part[3 * blockIdx.x] = a;
+    L.part[3 * blockIdx.x + 1] = b;
+    L.part[3 * blockIdx.x + 2] = c;
   }
 }
 
@@ -257,11 +305,14 @@ __global__ void __launch_bounds__(LG_THREADS) k_lg_resid(const V* __restrict__ y
   if (threadIdx.x == 0) part[blockIdx.x] = r2;
 }
 
+// one block, fixed order (strided per-thread sums, then the shuffle tree):
+// identical on every shard
 __global__ void k_lg_sum(const double* __restrict__ part, int cnt, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double red[32];
   double s = 0.0;
-  for (int i = 0; i < cnt; ++i) s += part[i];  // fixed order
-  *out = s;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
 }
 
 // shard view of a full vector: dst[k'] = src[p + P k']
@@ -320,12 +371,16 @@ cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st) {
 }
 
 cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
-                            double cut, unsigned long long* first, cudaStream_t st) {
+                            double cut, const double* cut_best, const double* blkmax,
+                            unsigned long long* first, cudaStream_t st) {
   const int grid = lg_grid();
+  cudaMemsetAsync(first, 0xff, 8, st);
   if (dtype == C128)
-    k_lg_first<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)base, off, stride, cnt, cut, first);
+    k_lg_first<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)base, off, stride, cnt, cut,
+                                                     cut_best, blkmax, first);
   else
-    k_lg_first<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)base, off, stride, cnt, cut, first);
+    k_lg_first<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)base, off, stride, cnt, cut,
+                                                    cut_best, blkmax, first);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -334,7 +389,7 @@ cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, dou
                          uint32_t* lam, void* xn, double* part, double* scal, int T, int s,
                          unsigned pick, double2 bnew, cudaStream_t st) {
   LgLs L{W, x, z, l, lam, xn, part, scal, T};
-  const int nblk = std::max(1, (s + LG_THREADS - 1) / LG_THREADS);
+  const int nblk = std::max(1, (s + LG_THREADS / 32 - 1) / (LG_THREADS / 32));
   if (op.kind == HADAMARD) k_lg_ls_a<true><<<nblk, LG_THREADS, 0, st>>>(op, L, s, pick);
   else k_lg_ls_a<false><<<nblk, LG_THREADS, 0, st>>>(op, L, s, pick);
   k_lg_ls_b<<<1, 32, 0, st>>>(L, nblk, bnew);
@@ -343,6 +398,14 @@ cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, dou
   if (dtype == C128) k_lg_ls_c<double2><<<cblk, LG_THREADS, 0, st>>>(L, s, pick, xscale);
   else k_lg_ls_c<float2><<<cblk, LG_THREADS, 0, st>>>(L, s, pick, xscale);
   g_launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t lg_launch_pick(int dtype, const double* best, const unsigned long long* first,
+                           const void* h0s, double* rec, cudaStream_t st) {
+  if (dtype == C128) k_lg_pick<double2><<<1, 1, 0, st>>>(best, first, (const double2*)h0s, rec);
+  else k_lg_pick<float2><<<1, 1, 0, st>>>(best, first, (const float2*)h0s, rec);
+  ++g_launches;
   return cudaGetLastError();
 }
 
@@ -362,13 +425,13 @@ cudaError_t lg_launch_resid(int dtype, const void* y, const void* ax, void* r, i
     k_lg_resid<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)y, (const double2*)ax, (double2*)r, m, part);
   else
     k_lg_resid<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)y, (const float2*)ax, (float2*)r, m, part);
-  k_lg_sum<<<1, 32, 0, st>>>(part, grid, out);
+  k_lg_sum<<<1, 256, 0, st>>>(part, grid, out);
   g_launches += 2;
   return cudaGetLastError();
 }
 
 cudaError_t lg_launch_sum(const double* part, int cnt, double* out, cudaStream_t st) {
-  k_lg_sum<<<1, 32, 0, st>>>(part, cnt, out);
+  k_lg_sum<<<1, 256, 0, st>>>(part, cnt, out);
   ++g_launches;
   return cudaGetLastError();
 }

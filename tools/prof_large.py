@@ -19,6 +19,8 @@ def main():
     p.add_argument("--mode", default="adaptive")
     p.add_argument("--log2n", type=int, default=24)
     p.add_argument("--reps", type=int, default=1)
+    p.add_argument("--python-loop", action="store_true",
+                   help="drive the shard through sharded_solve (the multi-GPU protocol)")
     a = p.parse_args()
     import torch
     import paper_1205_4139_b200 as fmp
@@ -35,9 +37,12 @@ def main():
     for _ in range(a.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        shard = fmp.LargeShard(op, cfg, 0, 1, dtype=np.complex64)
-        sup, co, it, rn, ab = fmp.sharded_solve([shard], y, tol, None)
-        shard.close()
+        if a.python_loop:
+            shard = fmp.LargeShard(op, cfg, 0, 1, dtype=np.complex64)
+            sup, co, it, rn, ab = fmp.sharded_solve([shard], y, tol, None)
+            shard.close()
+        else:
+            sup, co, it, rn, ab = fmp.large_solve(op, y, cfg, dtype=np.complex64)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         print(f"{it} iterations in {dt * 1e3:.1f} ms = {dt * 1e3 / max(it, 1):.3f} ms/iteration",
