@@ -103,6 +103,26 @@ __device__ __forceinline__ void msub_conj(float2& acc, float2 xn, float2 g) {
 template <class V>
 __device__ __forceinline__ void msub_conj(V&, V, V) {}
 
+// acc[r] -= x gk[r ^ lr] for a warp-uniform lr < RPT (fixed register maps)
+template <int RPT, int LR, class V, class T>
+__device__ __forceinline__ void lattice_mac_fixed(V (&acc)[RPT], V x, const T (&gk)[RPT]) {
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) msub(acc[r], x, gk[r ^ LR]);
+}
+template <int RPT, class V, class T>
+__device__ __forceinline__ void lattice_mac(V (&acc)[RPT], V x, const T (&gk)[RPT], int lr) {
+  switch (lr) {
+    case 0: lattice_mac_fixed<RPT, 0>(acc, x, gk); break;
+    case 1: if constexpr (RPT > 1) lattice_mac_fixed<RPT, 1 % RPT>(acc, x, gk); break;
+    case 2: if constexpr (RPT > 2) lattice_mac_fixed<RPT, 2 % RPT>(acc, x, gk); break;
+    case 3: if constexpr (RPT > 3) lattice_mac_fixed<RPT, 3 % RPT>(acc, x, gk); break;
+    case 4: if constexpr (RPT > 4) lattice_mac_fixed<RPT, 4 % RPT>(acc, x, gk); break;
+    case 5: if constexpr (RPT > 5) lattice_mac_fixed<RPT, 5 % RPT>(acc, x, gk); break;
+    case 6: if constexpr (RPT > 6) lattice_mac_fixed<RPT, 6 % RPT>(acc, x, gk); break;
+    default: if constexpr (RPT > 7) lattice_mac_fixed<RPT, 7 % RPT>(acc, x, gk); break;
+  }
+}
+
 // HALFG: the Fourier kernel is stored as its conjugate-symmetric half,
 // c[0..n/2] (c[n-j] = conj(c[j]), kernel.cpp:35-45); windows that stay on one
 // side of n/2 read it forwards (lower) or mirrored and conjugated (upper).
@@ -173,13 +193,16 @@ __device__ __forceinline__ void fast_tile(V (&acc)[RPT], int i0, int lane, int n
         l_nx = (int)lam[tau + 1];
         x_nx = xn[tau + 1];
       }
-      const int base = (i0 ^ (l & ~(32 * RPT - 1))) + (lane ^ (l & 31));
+      // output i0 + lane + 32 r reads entry (i0 + lane + 32 r) XOR l: the 32
+      // RPT block is permuted row-wise by lr = (l >> 5) mod RPT, which is
+      // uniform over the warp, so the loads use compile-time offsets from
+      // one base and the permutation is a branch to a fixed register mapping
+      const uint16_t* pb = gH + (i0 ^ (l & ~(32 * RPT - 1))) + (lane ^ (l & 31));
       const int lr = (l >> 5) & (RPT - 1);
-      T gv[RPT];
+      T gk[RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) lat_to((unsigned)gH[base + 32 * (r ^ lr)], gv[r]);
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) msub(acc[r], x, gv[r]);
+      for (int k = 0; k < RPT; ++k) lat_to((unsigned)pb[32 * k], gk[k]);
+      lattice_mac<RPT>(acc, x, gk, lr);
     }
   }
 }
