@@ -458,6 +458,27 @@ def _config(cfg: SolveConfig, tolerances=None):
     return c
 
 
+_TORCH_OF = {np.dtype(np.uint64): "int64", np.dtype(np.int64): "int64", np.dtype(np.float64): "float64",
+             np.dtype(np.complex128): "complex128", np.dtype(np.complex64): "complex64",
+             np.dtype(np.float32): "float32", np.dtype(np.int32): "int32", np.dtype(np.uint8): "uint8"}
+
+
+def _host_out(shape, dtype, zero=False):
+    """Result buffers for the host-buffer entry points: page-locked (torch's
+    caching host allocator, so device->host copies run at full speed and
+    repeated calls reuse the pages) when torch and a GPU are present."""
+    dtype = np.dtype(dtype)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            tdt = getattr(torch, _TORCH_OF[dtype])
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=tdt, pin_memory=True)
+            return t.numpy().view(dtype)
+    except (ImportError, KeyError, RuntimeError):
+        pass
+    return np.zeros(shape, dtype)
+
+
 def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
                     dtype=None) -> BatchResult:
     """omp_solve over a batch of measurements Y (batch, m) sharing `op`."""
@@ -474,14 +495,15 @@ def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
     B, T, n = Y.shape[0], int(cfg.max_iterations), op.n
     if T < 1:
         raise InvalidArgument(1, "omp_solve: max_iterations must be >= 1")
-    sup = np.zeros((B, T), np.uint64)
-    co = np.zeros((B, T), np.complex128)
-    sz = np.zeros(B, np.uint64)
-    it = np.zeros(B, np.uint64)
-    rn = np.zeros(B)
-    ab = np.zeros(B, np.int32)
-    md = np.zeros((B, T), np.uint8)
-    hl = np.zeros(B, np.uint64)
+    # every entry of these is written by the solve (support / coeffs zero padded)
+    sup = _host_out((B, T), np.uint64)
+    co = _host_out((B, T), np.complex128)
+    sz = _host_out(B, np.uint64)
+    it = _host_out(B, np.uint64)
+    rn = _host_out(B, np.float64)
+    ab = _host_out(B, np.int32)
+    md = _host_out((B, T), np.uint8, zero=True)  # rows past the last iteration stay 0
+    hl = _host_out(B, np.uint64)
     hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
     tol = None
     if tolerances is not None:

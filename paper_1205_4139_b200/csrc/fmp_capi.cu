@@ -74,7 +74,8 @@ struct Workspace {
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
             S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
-            S_OHSUP };
+            S_OHSUP,
+            S_ALT = 64 };  // S_ALT + slot: the alternate per-CTA workspace set
 
 }  // namespace
 
@@ -82,6 +83,9 @@ struct fmp_ctx_s {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t cur = nullptr;
+  cudaStream_t copy = nullptr;        // host<->device copies overlapped with solves (lazy)
+  cudaStream_t alt = nullptr;         // second compute stream (lazy)
+  std::vector<cudaEvent_t> events;    // chunk hand-offs between the two streams (lazy)
   Workspace ws;
   std::mutex mu;
 };
@@ -218,6 +222,12 @@ int fmp_ctx_destroy(fmp_ctx ctx) {
   if (!ctx) return FMP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->cur);
+  for (cudaStream_t x : {ctx->copy, ctx->alt})
+    if (x) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
+  for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
   return FMP_OK;
@@ -675,9 +685,12 @@ static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg) {
   }
 }
 
+// wsset: which set of per-CTA workspaces (two launches may run concurrently
+// on different streams, each with its own set)
 static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
                           const fmp_omp_config* cfg, const double* dtol, fmp_omp_result* out,
-                          cudaStream_t st) {
+                          cudaStream_t st, int wsset = 0) {
+  const int wo = wsset ? S_ALT : 0;  // slot offset of the alternate set
   fmp_ctx_s* ctx = op->ctx;
   const int64_t T = (int64_t)cfg->max_iterations;
   const int64_t n = op->d.n, m = op->d.m;
@@ -701,24 +714,24 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   a.hist = cfg->record_correlations ? out->history : nullptr;
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
   double2* w;
-  ALLOC(w, S_W, (size_t)a.grid * (T * (T + 1) / 2) * 16);
+  ALLOC(w, wo + S_W, (size_t)a.grid * (T * (T + 1) / 2) * 16);
   a.w_ws = w;
   void* h0;
-  ALLOC(h0, S_H0, (size_t)a.grid * n * eb);
+  ALLOC(h0, wo + S_H0, (size_t)a.grid * n * eb);
   a.h0_ws = h0;
   double* mag;
-  ALLOC(mag, S_MAG, (size_t)a.grid * n * 8);
+  ALLOC(mag, wo + S_MAG, (size_t)a.grid * n * 8);
   a.mag_ws = mag;
   void* r;
-  ALLOC(r, S_R, (size_t)a.grid * m * eb);
+  ALLOC(r, wo + S_R, (size_t)a.grid * m * eb);
   a.r_ws = r;
   if (n > fmp::transform_max_n(dtype) / 2) {
     void* bw;
-    ALLOC(bw, S_BUF, (size_t)a.grid * (n + n / 8) * eb);
+    ALLOC(bw, wo + S_BUF, (size_t)a.grid * (n + n / 8) * eb);
     a.buf_ws = bw;
   }
   int* q;
-  ALLOC(q, S_Q, 64);
+  ALLOC(q, wo + S_Q, 64);
   a.queue = q;
   CU(cudaMemsetAsync(q, 0, 4, st));
   if (g_phase_prof) {
@@ -757,6 +770,94 @@ int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
   return omp_dev_locked(op, dtype, y, batch, cfg, dtol, out, st);
 }
 
+// host-buffer solve in chunks: the copy stream moves chunk c + 1 in (and
+// chunk c - 1's results out) while the context stream solves chunk c
+static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
+                            const fmp_omp_config* cfg, fmp_omp_result* out, uint64_t nchunk) {
+  fmp_ctx_s* ctx = op->ctx;
+  cudaStream_t st = ctx->cur;
+  if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  if (!ctx->alt) CU(cudaStreamCreateWithFlags(&ctx->alt, cudaStreamNonBlocking));
+  while (ctx->events.size() < 2 * nchunk + 2) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  cudaStream_t cp = ctx->copy;
+  cudaEvent_t* ev_in = ctx->events.data();
+  cudaEvent_t* ev_out = ev_in + nchunk;
+  cudaEvent_t ev_ready = ev_in[2 * nchunk], ev_alt = ev_in[2 * nchunk + 1];
+  // chunks alternate between the context stream and a second one, each with
+  // its own workspaces, so a chunk's CTAs backfill SMs while the previous
+  // chunk's last problems finish
+  cudaStream_t cs[2] = {st, ctx->alt};
+  const uint64_t T = cfg->max_iterations, m = (uint64_t)op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  // device buffers for the whole batch (results stay addressable per chunk)
+  void *dy, *dtol;
+  ALLOC(dy, S_IN, batch * m * eb);
+  ALLOC(dtol, S_TOL, batch * 8);
+  fmp_omp_result d{};
+  ALLOC(d.support, S_OSUP, batch * T * 8);
+  ALLOC(d.coeffs, S_OCO, batch * T * 16);
+  ALLOC(d.support_size, S_OSZ, batch * 8);
+  ALLOC(d.iterations, S_OIT, batch * 8);
+  ALLOC(d.residual, S_ORES, batch * 8);
+  ALLOC(d.aborted, S_OAB, batch * 4);
+  if (out->modes) ALLOC(d.modes, S_OMOD, batch * T);
+  if (out->history_len) ALLOC(d.history_len, S_OHL, batch * 8);
+  std::vector<double> tv;
+  if (!cfg->tolerances) tv.assign(batch, cfg->tolerance);
+  // the copy stream starts after everything already queued on the context stream
+  CU(cudaEventRecord(ev_ready, st));
+  CU(cudaStreamWaitEvent(cp, ev_ready, 0));
+  CU(cudaStreamWaitEvent(ctx->alt, ev_ready, 0));
+  CU(cudaMemcpyAsync(dtol, cfg->tolerances ? cfg->tolerances : tv.data(), batch * 8,
+                     cudaMemcpyHostToDevice, cp));
+  const uint64_t per = (batch + nchunk - 1) / nchunk;
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
+    CU(cudaMemcpyAsync((char*)dy + b0 * m * eb, (const char*)y + b0 * m * eb, nb * m * eb,
+                       cudaMemcpyHostToDevice, cp));
+    CU(cudaEventRecord(ev_in[c], cp));
+  }
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
+    cudaStream_t sc = cs[c & 1];
+    CU(cudaStreamWaitEvent(sc, ev_in[c], 0));
+    fmp_omp_result dc{};
+    dc.support = d.support + b0 * T;
+    dc.coeffs = d.coeffs + 2 * b0 * T;
+    dc.support_size = d.support_size + b0;
+    dc.iterations = d.iterations + b0;
+    dc.residual = d.residual + b0;
+    dc.aborted = d.aborted + b0;
+    dc.modes = d.modes ? d.modes + b0 * T : nullptr;
+    dc.history_len = d.history_len ? d.history_len + b0 : nullptr;
+    if (int e = omp_dev_locked(op, dtype, (const char*)dy + b0 * m * eb, nb, cfg,
+                               (const double*)dtol + b0, &dc, sc, (int)(c & 1)))
+      return e;
+    CU(cudaEventRecord(ev_out[c], sc));
+    CU(cudaStreamWaitEvent(cp, ev_out[c], 0));
+    CU(cudaMemcpyAsync(out->support + b0 * T, dc.support, nb * T * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(out->coeffs + 2 * b0 * T, dc.coeffs, nb * T * 16, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(out->support_size + b0, dc.support_size, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(out->iterations + b0, dc.iterations, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(out->residual + b0, dc.residual, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(out->aborted + b0, dc.aborted, nb * 4, cudaMemcpyDeviceToHost, cp));
+    if (out->modes) CU(cudaMemcpyAsync(out->modes + b0 * T, dc.modes, nb * T, cudaMemcpyDeviceToHost, cp));
+    if (out->history_len)
+      CU(cudaMemcpyAsync(out->history_len + b0, dc.history_len, nb * 8, cudaMemcpyDeviceToHost, cp));
+  }
+  // the context stream owns the end of the call (later work queued on it
+  // sees every chunk)
+  CU(cudaEventRecord(ev_alt, ctx->alt));
+  CU(cudaStreamWaitEvent(st, ev_alt, 0));
+  CU(cudaStreamSynchronize(cp));
+  CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
 int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp_omp_config* cfg,
                   fmp_omp_result* out) {
   if (int s = omp_validate(op, dtype, cfg)) return s;
@@ -774,6 +875,11 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
   cudaStream_t st = ctx->cur;
   const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
   const size_t eb = fmp::elem_bytes(dtype);
+  // large batches: copies overlapped with the solve, chunk by chunk (each
+  // chunk still fills the GPU several times over)
+  const uint64_t grid = (uint64_t)fmp::omp_grid(op->d, dtype, (int64_t)batch, (int64_t)T);
+  if (!cfg->record_correlations && !g_phase_prof && batch >= 8 * grid)
+    return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(4, batch / (2 * grid)));
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
   std::vector<double> tv;

@@ -377,3 +377,27 @@ def test_omp_config4_c64_support_agreement_at_scale(fmp, oracle):
     out = subprocess.run([sys.executable, os.path.join(root, "tools", "fp32_agreement.py"), "16"],
                          capture_output=True, text=True, timeout=900).stdout
     assert "c64 support agreement 16 / 16" in out, out
+
+
+def test_omp_host_chunked_equals_device(fmp, oracle):
+    # batches >= 8 x grid take the copy/compute-overlapped host path
+    # (fmp_capi.cu omp_host_chunked): results must equal the device path bitwise
+    import torch
+    n, m, k, B = 1024, 256, 16, 1600
+    rows = fmp.make_row_selection(n, m, 31)
+    op = fmp.SensingOperator("fourier", n, rows)
+    Y, _, _ = fmp.make_batch("fourier", n, rows, k, B, base_seed=31)
+    tol = 1e-9 * np.linalg.norm(Y, axis=1)
+    cfg = fmp.SolveConfig(k, 0.0, "fast")
+    host = fmp.omp_solve_batch(op, Y, cfg, tolerances=tol)
+    out = fmp.alloc_dev_result(B, k)
+    fmp.omp_solve_dev(op, torch.from_numpy(Y).cuda(), cfg, out,
+                      tolerances=torch.from_numpy(tol).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(host.support.astype(np.int64), out["support"].cpu().numpy())
+    assert np.array_equal(host.coeffs, out["coeffs"].cpu().numpy())
+    assert np.array_equal(host.iterations.astype(np.int64), out["iterations"].cpu().numpy())
+    for b in range(0, B, 397):
+        r = oracle.omp_solve("fourier", n, rows, Y[b], k, tol[b], "fast")
+        assert [int(v) for v in host.support[b, :int(host.support_size[b])]] == \
+            [int(v) for v in r.support]
