@@ -526,10 +526,11 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
                        al(4 * (size_t)((n + 31) / 32));
   const size_t cap = (size_t)smem_optin() - 2048;
   size_t tot = tw + small;
-  // the transform buffer lives in smem unless even it does not fit with the
-  // kernel table (then it is an L2-resident per-CTA global buffer)
+  // the transform buffer has first claim on smem (a global-memory buffer
+  // sends every transform pass through L2); the kernel table follows and
+  // falls back to global memory (GMODE 0) when it does not fit beside it
   const size_t gmin = HAD ? gfull : ghalf;
-  p.bufg = tot + buf + gmin > cap;
+  p.bufg = tot + buf > cap;
   if (!p.bufg) tot += buf;
   p.wsm = tot + w + gmin <= cap;  // W next: the least-squares phase is latency bound
   if (p.wsm) tot += w;
