@@ -392,12 +392,14 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           red[64 + warp] = lzi;
         }
         __syncthreads();  // publishes s_l and the partials
-        ll = lzr = lzi = 0.0;
-        for (int w = 0; w < nw; ++w) {  // fixed order: every thread the same value
-          ll += red[w];
-          lzr += red[32 + w];
-          lzi += red[64 + w];
-        }
+        // every warp reduces the nw partials with the same shuffle tree, so
+        // every thread holds the bitwise-same sums
+        ll = lane < nw ? red[lane] : 0.0;
+        lzr = lane < nw ? red[32 + lane] : 0.0;
+        lzi = lane < nw ? red[64 + lane] : 0.0;
+        ll = warp_sum(ll);
+        lzr = warp_sum(lzr);
+        lzi = warp_sum(lzi);
         const double d2 = gamma - ll;
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
