@@ -316,24 +316,29 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
         // identification with the tie band (solvers.cpp:90-101, :362-367)
         // `red` was last read before the least-squares pass-2 barrier (or the
         // transform's barriers at t = 1): no leading barrier needed
+        const double my_best = best;  // this thread's own maximum
         best = block_max<false>(best, red);
         mark(fast_row ? 1 : 0);
         if (best == 0.0) break;
         const double cut = best * (1.0 - kTieBandRel);
         unsigned first = 0xffffffffu;
         if (!fast_row) {
+          // only a thread whose own maximum (over these same indices k) reaches
+          // the band can hold the pick
           const double scv = t == 1 ? 1.0 : sc;
-          for (int k = tid; k < n; k += nth)
-            if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
+          if (my_best >= cut)
+            for (int k = tid; k < n; k += nth)
+              if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
         } else if (regs_only) {
 #pragma unroll
           for (int r = RPT - 1; r >= 0; --r)
             if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
-        } else {
+        } else {  // (tile ownership differs from this scan's indices: no skip here)
           for (int k = tid; k < n; k += nth)
             if (msc[k] >= cut) { first = (unsigned)k; break; }
         }
         const unsigned pick = block_min_u<false>(first, redu);  // redu: only used here
+        if (pick >= (unsigned)n) break;  // no candidate (cannot happen: the maximum is in band)
         // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
         if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
         // b_s = h0[pick], read early so its latency hides behind the row pass
