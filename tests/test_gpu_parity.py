@@ -64,7 +64,7 @@ def test_apply_adjoint_matches_oracle(fmp, oracle, kind, n, m):
     # n >= 2^18 runs the two-pass transform (fmp_transform_4s.cu)
     om = oracle.make_row_selection(n, m, 7 + n)
     op = fmp.SensingOperator(kind, n, om)
-    B = 3 if n <= 65536 else 1
+    B = 3 if n <= 65536 else (2 if n <= (1 << 20) else 1)  # batch > 1 through the two-pass tiles too
     R = np.stack([oracle.rng_complex_gaussian(oracle.derive_seed(n, b), m) for b in range(B)])
     H, idx = op.apply_adjoint(R, argmax=True)
     for b in range(B):
@@ -401,3 +401,21 @@ def test_omp_host_chunked_equals_device(fmp, oracle):
         r = oracle.omp_solve("fourier", n, rows, Y[b], k, tol[b], "fast")
         assert [int(v) for v in host.support[b, :int(host.support_size[b])]] == \
             [int(v) for v in r.support]
+
+
+def test_omp_config1_shape_f32(fmp, oracle):
+    # config-1 shape in f32 (Hadamard lattice fast tile, FP32 path): identical
+    # supports to the oracle on the fp32-rounded measurements, x within 1e-4
+    n, m, k = 1024, 256, 16
+    om = oracle.make_row_selection(n, m, oracle.derive_seed(1, 1 << 40))
+    op = fmp.SensingOperator("hadamard", n, om)
+    for b in range(6):
+        x, y = oracle.make_real_instance("hadamard", n, om, k, oracle.derive_seed(1, b))
+        y32 = y.real.astype(np.float32)
+        tol = 1e-5 * np.linalg.norm(y32)
+        for mode in ("fast", "conventional"):
+            g = fmp.omp_solve(op, y32, fmp.SolveConfig(k, tol, mode), dtype=np.float32)
+            r = oracle.omp_solve("hadamard", n, om, y32.astype(np.complex128), k, tol, mode)
+            assert g.support == [int(v) for v in r.support]
+            assert rel(g.coeffs, r.coeffs) < 1e-4
+            assert sorted(g.support) == list(np.flatnonzero(x) + 1)
