@@ -879,7 +879,7 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
   // chunk still fills the GPU several times over)
   const uint64_t grid = (uint64_t)fmp::omp_grid(op->d, dtype, (int64_t)batch, (int64_t)T);
   if (!cfg->record_correlations && !g_phase_prof && batch >= 8 * grid)
-    return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(4, batch / (2 * grid)));
+    return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(8, batch / (2 * grid)));
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
   std::vector<double> tv;
