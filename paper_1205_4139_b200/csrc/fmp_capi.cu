@@ -1227,7 +1227,7 @@ int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
   A(&lg->h0s, lg->np * eb);
   A(&lg->hs, lg->np * eb);
   A(&lg->hfull, lg->n * eb);
-  A(&lg->xdense, lg->n * eb);
+  if (!op->d.fs_l1) A(&lg->xdense, lg->n * eb);  // (the two-pass transform reads the sparse estimate)
   A(&lg->ax, lg->m * eb);
   A(&lg->r, lg->m * eb);
   A(&lg->y, lg->m * eb);

@@ -177,7 +177,6 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
   __shared__ int s_hist[256];
   __shared__ unsigned long long s_ctl[4];
   __shared__ int s_prob;
-  __shared__ double s_piv;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T, K = a.K;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;

@@ -131,8 +131,7 @@ struct FsArgs {
 };
 
 template <class V>
-struct TwSel {
-  static constexpr bool kPowers = true;
+struct TwSel {  // the staged two-level table, or the global one
   TwTwoLevel<V> s;
   TwTable<V> g;
   bool sm;
