@@ -261,6 +261,23 @@ std::vector<RecoveryResult> cosamp_solve_batch(const SensingOperator& op,
 
 void save_result(const RecoveryResult& result, std::ostream& os);
 
+// Thin QR of a growing column set (solvers.hpp:90-109); Q lives on the
+// device.  push_column is false (and changes nothing) when the column's
+// remainder after two Gram-Schmidt passes is at most 1e-10 of its norm.
+// FlopCounter receives the reference's analytic counts.
+class IncrementalQR {
+ public:
+  explicit IncrementalQR(std::size_t rows);
+  std::size_t rows() const noexcept { return rows_; }
+  std::size_t cols() const noexcept;
+  bool push_column(const cvec& col, FlopCounter* fc = nullptr);
+  cvec solve(const cvec& rhs, FlopCounter* fc = nullptr) const;
+
+ private:
+  std::size_t rows_;
+  std::shared_ptr<void> h_;  // fmp_qr
+};
+
 cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
                    const cvec& y, LeastSquaresMethod method = LeastSquaresMethod::NormalEquations,
                    FlopCounter* fc = nullptr);

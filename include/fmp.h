@@ -191,6 +191,19 @@ int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64
 int fmp_cosamp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
                          const fmp_omp_config* cfg, fmp_cosamp_result* out, void* stream);
 
+/* ------------------------------------------------------------ IncrementalQR */
+/* IncrementalQR (solvers.hpp:90-109): thin QR of a growing column set, Q
+ * resident on the device.  push_column returns *accepted = 0 (and leaves the
+ * factorisation unchanged) when the column's remainder after two
+ * Gram-Schmidt passes is at most 1e-10 of its norm (solvers.cpp:244).
+ * Columns / rhs / x are host arrays of interleaved complex fp64. */
+typedef struct fmp_qr_s* fmp_qr;
+int fmp_qr_create(fmp_ctx ctx, uint64_t rows, uint64_t capacity, fmp_qr* out);
+int fmp_qr_destroy(fmp_qr qr);
+int fmp_qr_push_column(fmp_qr qr, const double* col, int* accepted);
+int fmp_qr_solve(fmp_qr qr, const double* rhs, double* x_out);
+uint64_t fmp_qr_cols(fmp_qr qr);
+
 /* profiling aid: when enabled, each fused solve accumulates SM cycles per
  * phase (conventional correlation, fast correlation, identification, least
  * squares, residual, other), summed over CTAs, readable afterwards */

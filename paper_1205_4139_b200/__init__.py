@@ -111,6 +111,11 @@ _sig("fmp_cosamp_solve", C.c_int, _vp, C.c_int, _vp, _u64, _u64, C.POINTER(OmpCo
      C.POINTER(CosampResult))
 _sig("fmp_cosamp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, _u64, C.POINTER(OmpConfig),
      C.POINTER(CosampResult), _vp)
+_sig("fmp_qr_create", C.c_int, _vp, _u64, _u64, C.POINTER(_vp))
+_sig("fmp_qr_destroy", C.c_int, _vp)
+_sig("fmp_qr_push_column", C.c_int, _vp, _vp, C.POINTER(C.c_int))
+_sig("fmp_qr_solve", C.c_int, _vp, _vp, _vp)
+_sig("fmp_qr_cols", _u64, _vp)
 _sig("fmp_large_create", C.c_int, _vp, C.c_int, _u64, _u64, C.POINTER(OmpConfig), C.POINTER(_vp))
 _sig("fmp_large_destroy", C.c_int, _vp)
 _sig("fmp_large_begin", C.c_int, _vp, _vp, C.c_double, C.POINTER(C.c_double))
@@ -650,6 +655,42 @@ def adaptive_cosamp_uses_fast(kind, n: int, k: int) -> bool:
     return (6 if kind == FOURIER else 2) * n * k <= (5 if kind == FOURIER else 2) * n * logn
 
 
+class IncrementalQR:
+    """IncrementalQR (solvers.hpp:90-109): thin QR of a growing column set,
+    Q resident on the device (fmp_qr_*)."""
+
+    def __init__(self, rows: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.rows = int(rows)
+        h = _vp()
+        _check(_lib.fmp_qr_create(self.ctx.handle, self.rows, 64, C.byref(h)))
+        self.handle = h
+
+    def cols(self) -> int:
+        return int(_lib.fmp_qr_cols(self.handle))
+
+    def push_column(self, col) -> bool:
+        col = np.ascontiguousarray(np.asarray(col, np.complex128))
+        if col.shape != (self.rows,):
+            raise InvalidArgument(1, "qr: column length mismatch")
+        ok = C.c_int(0)
+        _check(_lib.fmp_qr_push_column(self.handle, _ptr(col), C.byref(ok)))
+        return bool(ok.value)
+
+    def solve(self, rhs) -> np.ndarray:
+        rhs = np.ascontiguousarray(np.asarray(rhs, np.complex128))
+        if rhs.shape != (self.rows,):
+            raise InvalidArgument(1, "qr: rhs length mismatch")
+        x = np.zeros(self.cols(), np.complex128)
+        _check(_lib.fmp_qr_solve(self.handle, _ptr(rhs), _ptr(x) if x.size else None))
+        return x
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.fmp_qr_destroy(self.handle)
+            self.handle = None
+
+
 # ------------------------------------------- sharded single-signal solver
 class LargeShard:
     """Shard p of P of the config-5 solver (fmp_large_*): correlation entries
@@ -834,6 +875,6 @@ __all__ = [
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
     "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
-    "least_squares", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
+    "least_squares", "IncrementalQR", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
     "LargeShard", "LocalExchange", "sharded_solve", "large_solve",
 ]

@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <complex>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 #include <string>
@@ -1061,6 +1063,142 @@ int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64
   if (cfg->record_correlations)
     CU(cudaMemcpyAsync(out->history, d.history, batch * T * n * eb, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ IncrementalQR
+struct fmp_qr_s {
+  fmp_ctx_s* ctx = nullptr;
+  int64_t rows = 0;
+  int t = 0, cap = 0;
+  double2 *Q = nullptr, *v = nullptr, *part = nullptr, *s = nullptr, *acc = nullptr;
+  double *npart = nullptr, *dval = nullptr;
+  std::vector<std::vector<std::complex<double>>> R;  // column j: R(0..j, j)
+};
+
+namespace {
+void qr_free(fmp_qr_s* q) {
+  for (void* p : {(void*)q->Q, (void*)q->v, (void*)q->part, (void*)q->s, (void*)q->acc,
+                  (void*)q->npart, (void*)q->dval})
+    if (p) cudaFree(p);
+}
+
+int qr_reserve(fmp_qr_s* q, int cap) {
+  if (cap <= q->cap) return FMP_OK;
+  const int nc = std::max(cap, 2 * q->cap);
+  const int nb = fmp::qr_dot_blocks(q->rows);
+  double2 *Q2 = nullptr, *p2 = nullptr, *s2 = nullptr, *a2 = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&Q2, (size_t)nc * q->rows * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&p2, (size_t)nc * nb * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&s2, (size_t)nc * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&a2, (size_t)nc * 16)) != cudaSuccess) {
+    for (void* p : {(void*)Q2, (void*)p2, (void*)s2, (void*)a2}) if (p) cudaFree(p);
+    return fail(FMP_ENOMEM, "qr capacity %d: %s", nc, cudaGetErrorString(e));
+  }
+  if (q->t) CU(cudaMemcpyAsync(Q2, q->Q, (size_t)q->t * q->rows * 16, cudaMemcpyDeviceToDevice, q->ctx->cur));
+  CU(cudaStreamSynchronize(q->ctx->cur));
+  for (void* p : {(void*)q->Q, (void*)q->part, (void*)q->s, (void*)q->acc}) if (p) cudaFree(p);
+  q->Q = Q2;
+  q->part = p2;
+  q->s = s2;
+  q->acc = a2;
+  q->cap = nc;
+  return FMP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fmp_qr_create(fmp_ctx ctx, uint64_t rows, uint64_t capacity, fmp_qr* out) {
+  if (!ctx || !out) return fail(FMP_EINVAL, "null argument");
+  if (rows == 0) return fail(FMP_EINVAL, "qr: rows must be positive");
+  CU(cudaSetDevice(ctx->device));
+  fmp_qr_s* q = new fmp_qr_s;
+  q->ctx = ctx;
+  q->rows = (int64_t)rows;
+  cudaError_t e;
+  if ((e = cudaMalloc(&q->v, rows * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&q->npart, 4096 * 8)) != cudaSuccess ||  // >= the norm kernel grid
+      (e = cudaMalloc(&q->dval, 64)) != cudaSuccess) {
+    qr_free(q);
+    delete q;
+    return fail(FMP_ENOMEM, "qr: %s", cudaGetErrorString(e));
+  }
+  if (int st = qr_reserve(q, (int)std::max<uint64_t>(capacity, 8))) {
+    qr_free(q);
+    delete q;
+    return st;
+  }
+  *out = q;
+  return FMP_OK;
+}
+
+int fmp_qr_destroy(fmp_qr q) {
+  if (!q) return FMP_OK;
+  cudaSetDevice(q->ctx->device);
+  cudaStreamSynchronize(q->ctx->cur);
+  qr_free(q);
+  delete q;
+  return FMP_OK;
+}
+
+uint64_t fmp_qr_cols(fmp_qr q) { return q ? (uint64_t)q->t : 0; }
+
+// solvers.cpp:222-251
+int fmp_qr_push_column(fmp_qr q, const double* col, int* accepted) {
+  if (!q || !col || !accepted) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(q->ctx->device));
+  std::lock_guard<std::mutex> lk(q->ctx->mu);
+  cudaStream_t st = q->ctx->cur;
+  double o2 = 0.0;  // l2_norm(col) in the reference's order (types.cpp:32-36)
+  for (int64_t i = 0; i < 2 * q->rows; ++i) o2 += col[i] * col[i];
+  const double orig = std::sqrt(o2);
+  if (int e = qr_reserve(q, q->t + 1)) return e;
+  CU(cudaMemcpyAsync(q->v, col, (size_t)q->rows * 16, cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(q->acc, 0, (size_t)std::max(q->t, 1) * 16, st));
+  for (int pass = 0; pass < 2; ++pass)  // the second mops up the first's rounding
+    CU(fmp::launch_qr_project(q->Q, q->rows, q->t, q->v, q->part, q->s, q->acc, st));
+  CU(fmp::launch_qr_norm(q->v, q->rows, q->npart, q->dval, st));
+  std::vector<std::complex<double>> rcol((size_t)q->t + 1);
+  double r2 = 0.0;
+  if (q->t) CU(cudaMemcpyAsync(rcol.data(), q->acc, (size_t)q->t * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&r2, q->dval, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const double rho = std::sqrt(r2);
+  if (rho <= 1e-10 * orig) {  // nothing left outside the span
+    *accepted = 0;
+    return FMP_OK;
+  }
+  rcol[(size_t)q->t] = rho;
+  CU(fmp::launch_qr_store(q->Q + (size_t)q->t * q->rows, q->v, q->rows, 1.0 / rho, st));
+  q->R.push_back(std::move(rcol));
+  q->t += 1;
+  *accepted = 1;
+  return FMP_OK;
+}
+
+// solvers.cpp:253-274: z = Q^H rhs on the device, back substitution on the host
+int fmp_qr_solve(fmp_qr q, const double* rhs, double* x_out) {
+  if (!q || !rhs || (!x_out && q->t)) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(q->ctx->device));
+  std::lock_guard<std::mutex> lk(q->ctx->mu);
+  cudaStream_t st = q->ctx->cur;
+  const int t = q->t;
+  if (t == 0) return FMP_OK;
+  CU(cudaMemcpyAsync(q->v, rhs, (size_t)q->rows * 16, cudaMemcpyHostToDevice, st));
+  CU(fmp::launch_qr_dots(q->Q, q->rows, t, q->v, q->part, q->s, q->acc, st));
+  std::vector<std::complex<double>> z((size_t)t), x((size_t)t);
+  CU(cudaMemcpyAsync(z.data(), q->s, (size_t)t * 16, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int jj = t; jj-- > 0;) {
+    std::complex<double> v = z[(size_t)jj];
+    for (int k = jj + 1; k < t; ++k) v -= q->R[(size_t)k][(size_t)jj] * x[(size_t)k];
+    x[(size_t)jj] = v / q->R[(size_t)jj][(size_t)jj];
+  }
+  std::memcpy(x_out, x.data(), (size_t)t * 16);
   return FMP_OK;
 }
 

@@ -197,5 +197,13 @@ cudaError_t lg_launch_classmajor(int dtype, const void* g, void* gcm, int64_t n,
 cudaError_t fma_peak(int is_double, double* fma_per_s);
 // number of kernel launches issued by the last launch_* call on this thread
 int last_launch_count();
+// IncrementalQR helpers (fmp_qr.cu): Q column-major rows x t, fp64 complex
+int qr_dot_blocks(int64_t rows);
+cudaError_t launch_qr_project(const double2* Q, int64_t rows, int t, double2* v, double2* part,
+                              double2* s, double2* acc, cudaStream_t st);
+cudaError_t launch_qr_norm(const double2* v, int64_t rows, double* part, double* out, cudaStream_t st);
+cudaError_t launch_qr_store(double2* qnew, const double2* v, int64_t rows, double inv, cudaStream_t st);
+cudaError_t launch_qr_dots(const double2* Q, int64_t rows, int t, const double2* rhs, double2* part,
+                           double2* z, double2* scratch, cudaStream_t st);
 
 }  // namespace fmp

@@ -513,6 +513,49 @@ RecoveryResult omp_solve(const SensingOperator& op, const cvec& y, const SolveCo
   return std::move(omp_solve_batch(op, std::vector<cvec>{y}, cfg)[0]);
 }
 
+// ------------------------------------------------------------ IncrementalQR
+IncrementalQR::IncrementalQR(std::size_t rows) : rows_(rows) {
+  auto dev = Device::default_device();
+  fmp_qr q = nullptr;
+  check(fmp_qr_create(static_cast<fmp_ctx>(dev->handle()), rows, 64, &q));
+  // the deleter holds the device: its context outlives the factorisation
+  h_ = std::shared_ptr<void>(q, [dev](void* p) { fmp_qr_destroy(static_cast<fmp_qr>(p)); });
+}
+
+std::size_t IncrementalQR::cols() const noexcept {
+  return static_cast<std::size_t>(fmp_qr_cols(static_cast<fmp_qr>(h_.get())));
+}
+
+bool IncrementalQR::push_column(const cvec& col, FlopCounter* fc) {
+  if (col.size() != rows_) throw std::invalid_argument("qr: column length mismatch");
+  const std::size_t t = cols();
+  int accepted = 0;
+  check(fmp_qr_push_column(static_cast<fmp_qr>(h_.get()), raw(col), &accepted));
+  if (fc) {  // solvers.cpp:231-240 bookkeeping
+    fc->complex_mul += 2 * t * 2 * rows_;
+    fc->complex_add += 2 * t * (2 * rows_ - 1);
+    fc->real_mul += 2 * rows_;
+    fc->real_add += rows_;
+  }
+  return accepted != 0;
+}
+
+cvec IncrementalQR::solve(const cvec& rhs, FlopCounter* fc) const {
+  if (rhs.size() != rows_) throw std::invalid_argument("qr: rhs length mismatch");
+  const std::size_t t = cols();
+  cvec x(t);
+  check(fmp_qr_solve(static_cast<fmp_qr>(h_.get()), raw(rhs), t ? raw(x) : nullptr));
+  if (fc) {  // solvers.cpp:256-272 bookkeeping
+    fc->complex_mul += t * rows_;
+    fc->complex_add += t * (rows_ - 1);
+    if (t > 0) {
+      fc->complex_mul += std::uint64_t(t) * (t + 1) / 2;
+      fc->complex_add += std::uint64_t(t) * (t - 1) / 2;
+    }
+  }
+  return x;
+}
+
 std::uint64_t cosamp_fast_iteration_flops(TransformKind kind, std::size_t n, std::size_t k,
                                           std::size_t t) {
   if (t == 0) throw std::invalid_argument("flops: t must be positive");

@@ -12,6 +12,7 @@
 #include <functional>
 #include <sstream>
 #include <string>
+#include <tuple>
 
 #include "fastmp_b200/fastmp.hpp"
 
@@ -38,6 +39,8 @@ struct OSolveResult {
 };
 using omp_fn = int (*)(int, uint64_t, const uint64_t*, uint64_t, const double*, const OSolveConfig*,
                        OSolveResult*);
+using ls_fn = int (*)(int, uint64_t, const uint64_t*, uint64_t, const uint64_t*, uint64_t, const double*,
+                      int, double*, uint64_t*);
 
 static cvec gaussian(std::size_t n, std::uint64_t seed) {
   // deterministic test data (not the reference RNG): Box-Muller on splitmix
@@ -58,6 +61,7 @@ int main(int argc, char** argv) {
   void* orc = dlopen(oracle_path, RTLD_NOW | RTLD_LOCAL);
   omp_fn oracle_omp = orc ? reinterpret_cast<omp_fn>(dlsym(orc, "fmpo_omp_solve")) : nullptr;
   if (!oracle_omp) std::fprintf(stderr, "oracle not loaded: %s\n", dlerror());
+  ls_fn oracle_ls = orc ? reinterpret_cast<ls_fn>(dlsym(orc, "fmpo_least_squares")) : nullptr;
 
   // kernel invariants (test_kernel.cpp:65-107)
   {
@@ -229,6 +233,44 @@ int main(int argc, char** argv) {
     const RecoveryResult zero = omp_solve(op, cvec(8, cplx(0.0)), default_config(2, 0.0));
     CHECK(zero.iterations_run == 0 && zero.support.empty() && zero.residual_norm == 0.0);
     CHECK_THROWS_AS(omp_solve(op, cvec(7), default_config(1, 1.0)), std::invalid_argument);
+  }
+  // IncrementalQR (test_solvers.cpp:65-86 recipe; agreement with the oracle's
+  // two-pass MGS least squares, solvers.cpp:222-274)
+  {
+    SensingOperator op(StructuredUnitary(TransformKind::Hadamard, 32), make_row_selection(32, 8, 5));
+    IncrementalQR qr(8);
+    const cvec col = op.column(3);
+    CHECK(qr.push_column(col));
+    CHECK(!qr.push_column(col));
+    CHECK(qr.cols() == 1);
+    for (auto [kind, n, m, s] : {std::tuple{TransformKind::Fourier, std::size_t(256), std::size_t(64), 12},
+                                 std::tuple{TransformKind::Hadamard, std::size_t(1024), std::size_t(256), 24},
+                                 std::tuple{TransformKind::Fourier, std::size_t(65536), std::size_t(16384), 40}}) {
+      SensingOperator o2(StructuredUnitary(kind, n), make_row_selection(n, m, 77 + s));
+      const ProblemInstance in2 = make_instance(o2, 8, 0.05, 78 + s);
+      IncrementalQR q2(m);
+      std::vector<std::uint64_t> sup;
+      for (int j = 0; j < s; ++j) {
+        const std::size_t atom = 1 + (std::size_t(j) * 7919 + 13) % n;
+        CHECK(q2.push_column(o2.column(atom)));
+        sup.push_back(atom);
+      }
+      const cvec x = q2.solve(in2.y);
+      CHECK(x.size() == sup.size());
+      if (oracle_ls) {
+        std::vector<uint64_t> om(o2.selection().omega.begin(), o2.selection().omega.end());
+        std::vector<double> ox(2 * sup.size());
+        uint64_t aux = 0;
+        CHECK(oracle_ls(kind == TransformKind::Fourier ? 0 : 1, n, om.data(), m, sup.data(), sup.size(),
+                        reinterpret_cast<const double*>(in2.y.data()), 0, ox.data(), &aux) == 0);
+        double err = 0.0, nrm = 0.0;
+        for (std::size_t j = 0; j < x.size(); ++j) {
+          err += std::norm(x[j] - cplx(ox[2 * j], ox[2 * j + 1]));
+          nrm += std::norm(cplx(ox[2 * j], ox[2 * j + 1]));
+        }
+        CHECK(std::sqrt(err) <= 1e-10 * std::sqrt(nrm));
+      }
+    }
   }
   // CoSaMP (test_solvers.cpp:236-305, test_cost_model.cpp:93-108)
   {

@@ -26,7 +26,8 @@ def test_facade_builds_and_exports():
                          capture_output=True, text=True).stdout
     for sym in ("fastmp::omp_solve(", "fastmp::fast_update(", "fastmp::compute_kernel(",
                 "fastmp::least_squares(", "fastmp::cosamp_solve(",
-                "fastmp::save_instance(", "fastmp::load_instance(", "fastmp::save_result(", "fastmp::SensingOperator::apply_adjoint("):
+                "fastmp::save_instance(", "fastmp::load_instance(", "fastmp::save_result(",
+                "fastmp::IncrementalQR::push_column(", "fastmp::IncrementalQR::solve(", "fastmp::SensingOperator::apply_adjoint("):
         assert sym in out, sym
 
 
