@@ -660,8 +660,18 @@ RecoveryResult cosamp_solve(const SensingOperator& op, const cvec& y, std::size_
 }
 
 cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& support,
-                   const cvec& y, LeastSquaresMethod, FlopCounter*) {
+                   const cvec& y, LeastSquaresMethod method, FlopCounter* fc) {
   if (y.size() != op.m()) throw std::invalid_argument("least_squares: rhs length mismatch");
+  if (method == LeastSquaresMethod::IncrementalQR) {
+    // solvers.cpp:276-294: columns pushed in support order, the first
+    // dependent one raises with its position
+    IncrementalQR qr(op.m());
+    for (std::size_t j = 0; j < support.size(); ++j)
+      if (!qr.push_column(op.column(support[j]), fc))
+        throw RankDeficientError(j, "qr: dependent column at support position " +
+                                        std::to_string(j));
+    return qr.solve(y, fc);
+  }
   std::vector<std::uint64_t> sup(support.begin(), support.end());
   cvec x(support.size());
   std::int64_t pos = 0;

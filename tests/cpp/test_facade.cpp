@@ -234,6 +234,43 @@ int main(int argc, char** argv) {
     CHECK(zero.iterations_run == 0 && zero.support.empty() && zero.residual_norm == 0.0);
     CHECK_THROWS_AS(omp_solve(op, cvec(7), default_config(1, 1.0)), std::invalid_argument);
   }
+  // least squares in both methods (test_solvers.cpp:39-86)
+  {
+    SensingOperator op(StructuredUnitary(TransformKind::Fourier, 64), make_row_selection(64, 16, 3));
+    const ProblemInstance inst = make_instance(op, 5, 0.1, 4);
+    const std::vector<std::size_t> support{3, 17, 29, 40, 61};
+    const cvec a = least_squares(op, support, inst.y, LeastSquaresMethod::IncrementalQR);
+    const cvec b = least_squares(op, support, inst.y, LeastSquaresMethod::NormalEquations);
+    CHECK(a.size() == 5);
+    bool close = a.size() == b.size();
+    for (std::size_t i = 0; close && i < a.size(); ++i) close = std::abs(a[i] - b[i]) < 1e-8;
+    CHECK(close);
+    cvec r = inst.y;
+    for (std::size_t j = 0; j < support.size(); ++j) {
+      const cvec col = op.column(support[j]);
+      for (std::size_t i = 0; i < r.size(); ++i) r[i] -= a[j] * col[i];
+    }
+    bool orth = true;
+    for (std::size_t atom : support) {
+      const cvec col = op.column(atom);
+      cplx g = 0.0;
+      for (std::size_t i = 0; i < r.size(); ++i) g += std::conj(col[i]) * r[i];
+      orth &= std::abs(g) < 1e-10 * l2_norm(inst.y);
+    }
+    CHECK(orth);
+    SensingOperator oh(StructuredUnitary(TransformKind::Hadamard, 32), make_row_selection(32, 8, 5));
+    const ProblemInstance ih = make_instance(oh, 2, 0.0, 6);
+    const std::vector<std::size_t> dup{7, 7};
+    for (LeastSquaresMethod mth : {LeastSquaresMethod::IncrementalQR, LeastSquaresMethod::NormalEquations}) {
+      std::size_t pos = 99;
+      try {
+        least_squares(oh, dup, ih.y, mth);
+      } catch (const RankDeficientError& e) {
+        pos = e.position();
+      }
+      CHECK(pos == 1);
+    }
+  }
   // IncrementalQR (test_solvers.cpp:65-86 recipe; agreement with the oracle's
   // two-pass MGS least squares, solvers.cpp:222-274)
   {
