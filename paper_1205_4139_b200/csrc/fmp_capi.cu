@@ -87,6 +87,8 @@ struct fmp_ctx_s {
   cudaStream_t cur = nullptr;
   cudaStream_t copy = nullptr;        // host<->device copies overlapped with solves (lazy)
   cudaStream_t alt = nullptr;         // second compute stream (lazy)
+  void* pinned = nullptr;             // page-locked staging for pageable host buffers (lazy)
+  size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;    // chunk hand-offs between the two streams (lazy)
   Workspace ws;
   std::mutex mu;
@@ -230,6 +232,7 @@ int fmp_ctx_destroy(fmp_ctx ctx) {
       cudaStreamDestroy(x);
     }
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
   return FMP_OK;
@@ -772,6 +775,26 @@ int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
   return omp_dev_locked(op, dtype, y, batch, cfg, dtol, out, st);
 }
 
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+static int pinned_reserve(fmp_ctx_s* ctx, size_t bytes) {
+  if (ctx->pinned_bytes >= bytes) return FMP_OK;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  ctx->pinned_bytes = 0;
+  cudaError_t e = cudaHostAlloc(&ctx->pinned, bytes, cudaHostAllocDefault);
+  if (e != cudaSuccess) return fail(FMP_ENOMEM, "page-locked staging (%zu bytes): %s", bytes, cudaGetErrorString(e));
+  ctx->pinned_bytes = bytes;
+  return FMP_OK;
+}
+
 // host-buffer solve in chunks: the copy stream moves chunk c + 1 in (and
 // chunk c - 1's results out) while the context stream solves chunk c
 static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
@@ -780,15 +803,29 @@ static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
   cudaStream_t st = ctx->cur;
   if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
   if (!ctx->alt) CU(cudaStreamCreateWithFlags(&ctx->alt, cudaStreamNonBlocking));
-  while (ctx->events.size() < 2 * nchunk + 2) {
+  cudaStream_t cp = ctx->copy;
+  // pageable host buffers go through a page-locked staging area (a host
+  // memcpy per chunk that overlaps the device work of the other chunks)
+  // instead of the driver's synchronous staged copies
+  const uint64_t T_ = cfg->max_iterations, m_ = (uint64_t)op->d.m;
+  const size_t eb_ = fmp::elem_bytes(dtype);
+  const bool stage_in = !host_pinned(y), stage_out = !host_pinned(out->support);
+  const size_t in_bytes = stage_in ? batch * m_ * eb_ : 0;
+  const size_t out_row = T_ * 8 + T_ * 16 + 8 + 8 + 8 + 4;  // support, coeffs, size, iters, resid, aborted
+  const size_t out_bytes = stage_out ? batch * out_row : 0;
+  if (stage_in || stage_out)
+    if (int e = pinned_reserve(ctx, in_bytes + out_bytes)) return e;
+  char* pin_in = (char*)ctx->pinned;
+  char* pin_out = (char*)ctx->pinned + in_bytes;
+  while (ctx->events.size() < 3 * nchunk + 2) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->events.push_back(e);
   }
-  cudaStream_t cp = ctx->copy;
   cudaEvent_t* ev_in = ctx->events.data();
   cudaEvent_t* ev_out = ev_in + nchunk;
   cudaEvent_t ev_ready = ev_in[2 * nchunk], ev_alt = ev_in[2 * nchunk + 1];
+  cudaEvent_t* ev_d2h = ev_in + 2 * nchunk + 2;
   // chunks alternate between the context stream and a second one, each with
   // its own workspaces, so a chunk's CTAs backfill SMs while the previous
   // chunk's last problems finish
@@ -819,8 +856,12 @@ static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
   const uint64_t per = (batch + nchunk - 1) / nchunk;
   for (uint64_t c = 0; c < nchunk; ++c) {
     const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
-    CU(cudaMemcpyAsync((char*)dy + b0 * m * eb, (const char*)y + b0 * m * eb, nb * m * eb,
-                       cudaMemcpyHostToDevice, cp));
+    const char* src = (const char*)y + b0 * m * eb;
+    if (stage_in) {  // (the host copy of chunk c overlaps the transfer of chunk c - 1)
+      std::memcpy(pin_in + b0 * m * eb, src, nb * m * eb);
+      src = pin_in + b0 * m * eb;
+    }
+    CU(cudaMemcpyAsync((char*)dy + b0 * m * eb, src, nb * m * eb, cudaMemcpyHostToDevice, cp));
     CU(cudaEventRecord(ev_in[c], cp));
   }
   for (uint64_t c = 0; c < nchunk; ++c) {
@@ -841,16 +882,47 @@ static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
       return e;
     CU(cudaEventRecord(ev_out[c], sc));
     CU(cudaStreamWaitEvent(cp, ev_out[c], 0));
-    CU(cudaMemcpyAsync(out->support + b0 * T, dc.support, nb * T * 8, cudaMemcpyDeviceToHost, cp));
-    CU(cudaMemcpyAsync(out->coeffs + 2 * b0 * T, dc.coeffs, nb * T * 16, cudaMemcpyDeviceToHost, cp));
-    CU(cudaMemcpyAsync(out->support_size + b0, dc.support_size, nb * 8, cudaMemcpyDeviceToHost, cp));
-    CU(cudaMemcpyAsync(out->iterations + b0, dc.iterations, nb * 8, cudaMemcpyDeviceToHost, cp));
-    CU(cudaMemcpyAsync(out->residual + b0, dc.residual, nb * 8, cudaMemcpyDeviceToHost, cp));
-    CU(cudaMemcpyAsync(out->aborted + b0, dc.aborted, nb * 4, cudaMemcpyDeviceToHost, cp));
+    // results of chunk c: straight into page-locked user buffers, or into
+    // the staging area (copied out below, chunk by chunk)
+    uint64_t* o_sup = out->support + b0 * T;
+    double* o_co = out->coeffs + 2 * b0 * T;
+    uint64_t* o_sz = out->support_size + b0;
+    uint64_t* o_it = out->iterations + b0;
+    double* o_rn = out->residual + b0;
+    int32_t* o_ab = out->aborted + b0;
+    if (stage_out) {
+      char* base = pin_out + b0 * out_row;
+      o_sup = (uint64_t*)base;
+      o_co = (double*)(base + nb * T * 8);
+      o_sz = (uint64_t*)(base + nb * (T * 24));
+      o_it = o_sz + nb;
+      o_rn = (double*)(o_it + nb);
+      o_ab = (int32_t*)(o_rn + nb);
+    }
+    CU(cudaMemcpyAsync(o_sup, dc.support, nb * T * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(o_co, dc.coeffs, nb * T * 16, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(o_sz, dc.support_size, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(o_it, dc.iterations, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(o_rn, dc.residual, nb * 8, cudaMemcpyDeviceToHost, cp));
+    CU(cudaMemcpyAsync(o_ab, dc.aborted, nb * 4, cudaMemcpyDeviceToHost, cp));
+    CU(cudaEventRecord(ev_d2h[c], cp));
     if (out->modes) CU(cudaMemcpyAsync(out->modes + b0 * T, dc.modes, nb * T, cudaMemcpyDeviceToHost, cp));
     if (out->history_len)
       CU(cudaMemcpyAsync(out->history_len + b0, dc.history_len, nb * 8, cudaMemcpyDeviceToHost, cp));
   }
+  if (stage_out)
+    for (uint64_t c = 0; c < nchunk; ++c) {  // overlaps the device work of later chunks
+      const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
+      CU(cudaEventSynchronize(ev_d2h[c]));
+      const char* base = pin_out + b0 * out_row;
+      std::memcpy(out->support + b0 * T, base, nb * T * 8);
+      std::memcpy(out->coeffs + 2 * b0 * T, base + nb * T * 8, nb * T * 16);
+      const char* tail = base + nb * T * 24;
+      std::memcpy(out->support_size + b0, tail, nb * 8);
+      std::memcpy(out->iterations + b0, tail + nb * 8, nb * 8);
+      std::memcpy(out->residual + b0, tail + nb * 16, nb * 8);
+      std::memcpy(out->aborted + b0, tail + nb * 24, nb * 4);
+    }
   // the context stream owns the end of the call (later work queued on it
   // sees every chunk)
   CU(cudaEventRecord(ev_alt, ctx->alt));

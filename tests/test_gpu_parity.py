@@ -419,3 +419,31 @@ def test_omp_config1_shape_f32(fmp, oracle):
             assert g.support == [int(v) for v in r.support]
             assert rel(g.coeffs, r.coeffs) < 1e-4
             assert sorted(g.support) == list(np.flatnonzero(x) + 1)
+
+
+def test_omp_host_chunked_pageable_buffers(fmp):
+    # pageable (non-page-locked) input and result buffers take the staging
+    # path of the chunked host call; results must equal the wrapper's bitwise
+    import ctypes as C
+    n, m, k, B = 1024, 256, 16, 1600
+    rows = fmp.make_row_selection(n, m, 32)
+    op = fmp.SensingOperator("hadamard", n, rows)
+    Y, _, _ = fmp.make_batch("hadamard", n, rows, k, B, base_seed=32)
+    Y = np.ascontiguousarray(Y.real)
+    tol = np.ascontiguousarray(1e-9 * np.linalg.norm(Y, axis=1))
+    cfg = fmp.SolveConfig(k, 0.0, "fast")
+    ref = fmp.omp_solve_batch(op, Y, cfg, tolerances=tol)
+    sup = np.zeros((B, k), np.uint64)
+    co = np.zeros((B, k), np.complex128)
+    sz = np.zeros(B, np.uint64)
+    it = np.zeros(B, np.uint64)
+    rn = np.zeros(B)
+    ab = np.zeros(B, np.int32)
+    res = fmp.OmpResult(sup.ctypes.data, co.ctypes.data, sz.ctypes.data, it.ctypes.data,
+                        rn.ctypes.data, ab.ctypes.data, None, None, None)
+    c = fmp._config(cfg, tol.ctypes.data_as(C.POINTER(C.c_double)))
+    assert fmp._lib.fmp_omp_solve(op.handle, fmp.DTYPES[Y.dtype], Y.ctypes.data, B, C.byref(c),
+                                  C.byref(res)) == 0
+    assert np.array_equal(sup, ref.support) and np.array_equal(co, ref.coeffs)
+    assert np.array_equal(sz, ref.support_size) and np.array_equal(it, ref.iterations)
+    assert np.array_equal(rn, ref.residual) and np.array_equal(ab.astype(bool), ref.aborted)

@@ -20,7 +20,9 @@ def main():
     tol = 1e-9 * np.linalg.norm(Y, axis=1)
     op = fmp.SensingOperator("fourier", n, rows)
     Yp = torch.from_numpy(Y).pin_memory().numpy()
-    cfg = fmp.SolveConfig(k, 0.0, "gpu")
+    mode = sys.argv[1] if len(sys.argv) > 1 else "gpu"
+    cfg = fmp.SolveConfig(k, 0.0, mode)
+    print("mode", mode)
 
     def timed(fn, reps=5):
         fn()
