@@ -311,6 +311,30 @@ __device__ __forceinline__ void first_pass_loaded(V* buf, int log2n, const LOAD&
   }
 }
 
+// first pass driven by a slot map (int16, -1 = zero slot): each thread
+// fetches its R = 8 map entries with one 16-byte load (consecutive threads,
+// consecutive 16-byte words: no bank conflicts), then the values it maps to
+template <int LOGP, bool INV, bool HAD, class V, class VAL>
+__device__ __forceinline__ void first_pass_map8(V* buf, int log2n, const int16_t* map, const VAL& val,
+                                                int tid, int nth) {
+  const int nsub = 1 << (log2n - 3);
+  const int4* m4 = reinterpret_cast<const int4*>(map);
+  for (int u = tid; u < nsub; u += nth) {
+    const int4 w = m4[u];
+    const int packed[4] = {w.x, w.y, w.z, w.w};
+    V v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = (int)(int16_t)((packed[j >> 1] >> (16 * (j & 1))) & 0xFFFF);
+      v[j] = val(q);
+    }
+    if constexpr (HAD) wht_reg<8>(v);
+    else dft_reg<8, INV>(v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) buf[padx<LOGP>(u * 8 + j)] = v[j];
+  }
+}
+
 // log2tab: size of the twiddle table (defaults to the vector); a block that
 // runs the first stages of a longer transform passes the full length.
 template <int RMAX, bool INV, bool HAD, class V, class TW>

@@ -199,10 +199,9 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
     auto residual_explicit = [&](int cnt) -> double {
       if (s_xmap && log2n >= OLOGP) {
         __syncthreads();
-        first_pass_loaded<ORMAX, OLOGP, false, HAD>(
-            buf, log2n,
-            [&](int slot) {
-              const int q = s_xmap[slot];
+        first_pass_map8<OLOGP, false, HAD>(
+            buf, log2n, s_xmap,
+            [&](int q) {
               V xv = zv;
               if (q >= 0) from_c128(s_x[q], xv);
               return xv;
@@ -248,9 +247,8 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           const V* r = t == 1 ? y : rs;
           if (s_map && log2n >= OLOGP) {
             __syncthreads();  // buf may still be read (previous argmax / h0)
-            first_pass_loaded<ORMAX, OLOGP, true, HAD>(
-                buf, log2n, [&](int slot) { const int q = s_map[slot]; return q >= 0 ? r[q] : zv; },
-                tid, nth);
+            first_pass_map8<OLOGP, true, HAD>(
+                buf, log2n, s_map, [&](int q) { return q >= 0 ? r[q] : zv; }, tid, nth);
             __syncthreads();
             block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth, -1, OLOGP);
           } else {
