@@ -361,8 +361,39 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
     OPALLOC(d.fs_bpos, m * 4);
     OPALLOC(d.fs_brow, m * 4);
   }
+  // one-pass large Hadamard adjoint: per block size, rows ordered by (row of
+  // 32, position, input block) (fmp_transform_fold.cu)
+  std::vector<uint32_t> fold_tab[4], fold_off[4];
+  if (kind == FMP_HADAMARD && m < (1u << 20)) {
+    for (int q = 3; q < 4; ++q) {  // block sizes in use: 2^14 (f32)
+      const int lb = 11 + q, s = d.log2n - lb;
+      if (s < 1 || s > 6) continue;
+      const uint32_t rows_per_block = 1u << (lb - 5);
+      std::vector<std::pair<uint64_t, uint32_t>> key(m);
+      for (uint64_t i = 0; i < m; ++i) {
+        const uint32_t p = om[i], ih = p >> lb, lo = p & ((1u << lb) - 1);
+        key[i] = {((uint64_t)(lo >> 5) << 16) | ((lo & 31u) << 8) | ih, (uint32_t)i};
+      }
+      std::sort(key.begin(), key.end());
+      fold_tab[q].resize(m);
+      fold_off[q].assign(rows_per_block + 1, 0);
+      for (uint64_t i = 0; i < m; ++i) {
+        const uint32_t mi = key[i].second, p = om[mi], lo = p & ((1u << lb) - 1);
+        fold_tab[q][i] = mi | ((p >> lb) << 20) | ((lo & 31u) << 26);
+        fold_off[q][(lo >> 5) + 1]++;
+      }
+      for (uint32_t g = 0; g < rows_per_block; ++g) fold_off[q][g + 1] += fold_off[q][g];
+      OPALLOC(d.fold_tab[q], m * 4);
+      OPALLOC(d.fold_off[q], (rows_per_block + 1) * 4);
+    }
+  }
 #undef OPALLOC
   cudaStream_t st = ctx->cur;
+  for (int q = 0; q < 4; ++q)
+    if (d.fold_tab[q] &&
+        ((e = cudaMemcpyAsync(d.fold_tab[q], fold_tab[q].data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+         (e = cudaMemcpyAsync(d.fold_off[q], fold_off[q].data(), fold_off[q].size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess))
+      return cleanup(fail(FMP_ECUDA, "fold tables: %s", cudaGetErrorString(e)));
   if (d.fs_l1 &&
       ((e = cudaMemcpyAsync(d.fs_aoff, fa_off.data(), fa_off.size() * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
        (e = cudaMemcpyAsync(d.fs_apos, fa_pos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
@@ -412,6 +443,10 @@ int fmp_operator_destroy(fmp_op op) {
                   (void*)d.gr64, (void*)d.glat, (void*)d.fs_aoff, (void*)d.fs_apos, (void*)d.fs_arow,
                   (void*)d.fs_boff, (void*)d.fs_bpos, (void*)d.fs_brow})
     if (p) cudaFree(p);
+  for (int q = 0; q < 4; ++q) {
+    if (d.fold_tab[q]) cudaFree(d.fold_tab[q]);
+    if (d.fold_off[q]) cudaFree(d.fold_off[q]);
+  }
   delete op;
   return FMP_OK;
 }

@@ -4,6 +4,131 @@
 
 namespace fmp {
 namespace {
+// --------------------------------------- real Hadamard: quad-lane lattice
+// Each lane owns 4 consecutive outputs per 128-output group, so one 8-byte
+// shared-memory load brings the 4 lattice entries it needs for an atom: for
+// output i = i0 + 128 r + 4 lane + q the entry i XOR l sits in group r ^ lr,
+// lane slot lane ^ ll, position q ^ lq (lr, ll, lq fields of l, uniform over
+// the warp).  The group permutation lives in the load addresses, the
+// position permutation lq is a branch to a fixed register mapping; each entry becomes an exact float / double by one byte permute
+// (PRMT) into a magic-number pattern and one bias subtraction, and the
+// multiply-adds run packed (FFMA2 / FADD2) for f32.  Same operations and
+// order per output as fast_point / fast_tile, so results are unchanged.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+// entry s (0..3) of the 4-entry group held in w as an exact lattice value k
+template <int S>
+__device__ __forceinline__ float quad_f(uint2 w) {
+  const uint32_t word = (S >> 1) ? w.y : w.x;
+  return __uint_as_float(prmt(word, 0x4B000000u, (S & 1) ? 0x7632u : 0x7610u));  // 2^23 + u
+}
+template <int S>
+__device__ __forceinline__ double quad_d(uint2 w) {
+  const uint32_t word = (S >> 1) ? w.y : w.x;
+  const uint32_t u = prmt(word, 0u, (S & 1) ? 0x4432u : 0x4410u);
+  return __hiloint2double(0x43300000, (int)u) - 4503599627403264.0;  // 2^52 + 2^15
+}
+
+template <int RPT, int LQ>
+__device__ __forceinline__ void quad_mac(float2 (&acc)[RPT][2], float x, const uint2 (&w)[RPT]) {
+  const float2 xx = make_float2(x, x);
+  const float2 bias = make_float2(-8421376.0f, -8421376.0f);  // -(2^23 + 2^15)
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const uint2 ww = w[r];
+    const float2 g01 = __fadd2_rn(make_float2(quad_f<0 ^ LQ>(ww), quad_f<1 ^ LQ>(ww)), bias);
+    const float2 g23 = __fadd2_rn(make_float2(quad_f<2 ^ LQ>(ww), quad_f<3 ^ LQ>(ww)), bias);
+    acc[r][0] = __ffma2_rn(xx, g01, acc[r][0]);
+    acc[r][1] = __ffma2_rn(xx, g23, acc[r][1]);
+  }
+}
+template <int RPT, int LQ>
+__device__ __forceinline__ void quad_mac(double (&acc)[RPT][4], double x, const uint2 (&w)[RPT]) {
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const uint2 ww = w[r];
+    acc[r][0] = fma(x, quad_d<0 ^ LQ>(ww), acc[r][0]);
+    acc[r][1] = fma(x, quad_d<1 ^ LQ>(ww), acc[r][1]);
+    acc[r][2] = fma(x, quad_d<2 ^ LQ>(ww), acc[r][2]);
+    acc[r][3] = fma(x, quad_d<3 ^ LQ>(ww), acc[r][3]);
+  }
+}
+template <int RPT, class A, class T>
+__device__ __forceinline__ void quad_mac_q(A& acc, T x, const uint2 (&w)[RPT], int lq) {
+  switch (lq) {
+    case 0: quad_mac<RPT, 0>(acc, x, w); break;
+    case 1: quad_mac<RPT, 1>(acc, x, w); break;
+    case 2: quad_mac<RPT, 2>(acc, x, w); break;
+    default: quad_mac<RPT, 3>(acc, x, w); break;
+  }
+}
+
+// accumulator tile of one lane: RPT groups of 4 consecutive outputs
+template <class T, int RPT> struct QuadAcc;
+template <int RPT> struct QuadAcc<float, RPT> {
+  float2 a[RPT][2];
+  __device__ __forceinline__ void load(const float* p) {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const float4 v = *reinterpret_cast<const float4*>(p + 128 * r);
+      a[r][0] = make_float2(v.x, v.y);
+      a[r][1] = make_float2(v.z, v.w);
+    }
+  }
+  __device__ __forceinline__ float get(int r, int q) const { return (q & 1) ? a[r][q >> 1].y : a[r][q >> 1].x; }
+  __device__ __forceinline__ void store(float* p) const {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      *reinterpret_cast<float4*>(p + 128 * r) = make_float4(a[r][0].x, a[r][0].y, a[r][1].x, a[r][1].y);
+  }
+};
+template <int RPT> struct QuadAcc<double, RPT> {
+  double a[RPT][4];
+  __device__ __forceinline__ void load(const double* p) {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const double2 v0 = *reinterpret_cast<const double2*>(p + 128 * r);
+      const double2 v1 = *reinterpret_cast<const double2*>(p + 128 * r + 2);
+      a[r][0] = v0.x; a[r][1] = v0.y; a[r][2] = v1.x; a[r][3] = v1.y;
+    }
+  }
+  __device__ __forceinline__ double get(int r, int q) const { return a[r][q]; }
+  __device__ __forceinline__ void store(double* p) const {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      *reinterpret_cast<double2*>(p + 128 * r) = make_double2(a[r][0], a[r][1]);
+      *reinterpret_cast<double2*>(p + 128 * r + 2) = make_double2(a[r][2], a[r][3]);
+    }
+  }
+};
+
+template <class T, int RPT>
+__device__ __forceinline__ void fast_tile_quad(QuadAcc<T, RPT>& acc, int i0, int lane,
+                                               const uint16_t* __restrict__ gH,
+                                               const unsigned* lam, const T* xn, int t) {
+  if (t <= 0) return;
+  int l_nx = (int)lam[0];
+  T x_nx = xn[0];
+  for (int tau = 0; tau < t; ++tau) {
+    const int l = l_nx;
+    const T x = x_nx;
+    if (tau + 1 < t) {
+      l_nx = (int)lam[tau + 1];
+      x_nx = xn[tau + 1];
+    }
+    // group k of the tile reads entry group ((i0 + 128 k) ^ l) >> 7
+    const uint16_t* pb = gH + 4 * (lane ^ ((l >> 2) & 31));
+    const int gx = (i0 ^ l) & ~127;
+    uint2 w[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) w[k] = *reinterpret_cast<const uint2*>(pb + (gx ^ (128 * k)));
+    quad_mac_q<RPT>(acc.a, x, w, l & 3);
+  }
+}
+
 // ----------------------------------------------------------- fast update
 template <class V, bool HAD, int RPT, bool GSM>
 __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
@@ -47,6 +172,10 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
     double best = 0.0;
     // outputs are produced tile by tile; the atom list is consumed in chunks
     const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
+    // real Hadamard with a staged lattice: quad-lane tiles of 128 RPT/4 outputs
+    constexpr bool QUAD = HAD && GSM && (sizeof(V) == 4 || sizeof(V) == 8) && RPT >= 4;
+    constexpr int QR = 8;  // 1024 outputs per warp tile, 32 per lane
+    const int qtiles = n / (128 * QR);
     for (int c0 = 0; c0 < t || c0 == 0; c0 += chunk) {
       const int cn = min(chunk, t - c0);
       __syncthreads();
@@ -57,7 +186,27 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
       __syncthreads();
       const bool first = c0 == 0, last = c0 + chunk >= t;
       const V* src = first ? hb : ob;  // later chunks continue from the partial h
-      if (ntiles) {
+      if constexpr (QUAD) {
+        using T = typename scal<V>::T;
+        for (int tile = warp; tile < qtiles; tile += nw) {
+          const int i0 = tile * 128 * QR;
+          QuadAcc<T, QR> acc;
+          acc.load(reinterpret_cast<const T*>(src) + i0 + 4 * lane);
+          fast_tile_quad<T, QR>(acc, i0, lane, gH, s_lam, reinterpret_cast<const T*>(s_xn), cn);
+          if (ob) acc.store(reinterpret_cast<T*>(ob) + i0 + 4 * lane);
+          if (last) {
+#pragma unroll
+            for (int r = 0; r < QR; ++r)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int i = i0 + 128 * r + 4 * lane + q;
+                const double mm = mag2(acc.get(r, q));
+                msc[i] = mm;
+                best = fmax(best, mm);
+              }
+          }
+        }
+      } else if (ntiles) {
         for (int tile = warp; tile < ntiles; tile += nw) {
           const int i0 = tile * 32 * RPT;
           V acc[RPT];

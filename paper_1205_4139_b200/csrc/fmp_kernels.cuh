@@ -43,6 +43,12 @@ struct DevOp {
   uint32_t* fs_boff = nullptr;  // N1 + 1
   uint32_t* fs_bpos = nullptr;  // m
   uint32_t* fs_brow = nullptr;  // m
+  // one-pass Hadamard adjoint for n beyond one CTA (fmp_transform_fold.cu):
+  // for block size B = 2^(11+q), Omega's rows ordered by (row g of 32 within
+  // the block, position j in the row, input block ih), packed
+  // m | ih << 20 | j << 26, with B/32 + 1 per-row offsets; null if unused
+  uint32_t* fold_tab[4] = {};
+  uint32_t* fold_off[4] = {};
 };
 
 struct TransformArgs {
@@ -152,6 +158,9 @@ struct CosArgs {
 // launchers (return cudaError_t); all async on `stream`
 cudaError_t launch_transform(const TransformArgs& a, cudaStream_t stream);
 cudaError_t launch_transform_fs(const FsTransform& t, cudaStream_t stream);
+// Hadamard adjoint of m values at Omega, n beyond one CTA: one pass, no
+// intermediate (fmp_transform_fold.cu); cudaErrorNotSupported if not applicable
+cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t stream);
 int fs_split(int log2n);  // N1 = 2^fs_split rows of the two-pass transform, 0: not used
 cudaError_t launch_fast_update(const FastUpdateArgs& a, cudaStream_t stream);
 cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t stream);

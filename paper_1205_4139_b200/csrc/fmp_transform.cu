@@ -538,6 +538,19 @@ cudaError_t launch_tr_v(const TransformArgs& a, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (a.op->n > transform_max_n(a.dtype)) {
+    if constexpr (HAD) {
+      // one pass over HBM: sparse input folded at load time (fmp_transform_fold.cu)
+      cudaError_t e = launch_wht_fold(a, st);
+      if (e == cudaSuccess) {
+        if (a.argmax_out) {
+          const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(a.batch, 4 * num_sms()));
+          k_argmax<V><<<g2, 512, 0, st>>>((const V*)a.out, a.op->n, a.batch, a.argmax_out);
+          ++g_launches;
+        }
+        return cudaGetLastError();
+      }
+      if (e != cudaErrorNotSupported) return e;
+    }
     const int k = a.op->scat_pos ? cluster_k<V>(a.op->n, a.dtype) : 0;
     const int kq = a.op->scat_pos ? queue_k<V>(a.op->n, a.dtype) : 0;
     // distributed-shared-memory cluster for 4-byte elements (config 3 f32:

@@ -1,0 +1,258 @@
+// Conventional Hadamard correlation Phi^H r for vectors larger than one CTA's
+// shared memory (config 3: N = 65536, M = 8192), in ONE pass over HBM with no
+// intermediate vector.
+//
+// Reference: SensingOperator::apply_adjoint (sensing.cpp:102-109) = scatter r
+// at Omega into zeros, StructuredUnitary::fht (transform.cpp:86-100), scale by
+// 1/sqrt(N) (transform.cpp:132).
+//
+// Factorisation.  Write i = i_hi B + i_lo, k = k_hi B + k_lo (B = N / S).
+// H_N = H_S (x) H_B, so
+//     h[k_hi B + k_lo] = sum_{i_lo} H_B[k_lo, i_lo] z_{k_hi}[i_lo],
+//     z_{k_hi}[i_lo]   = sum_{i_hi} (-1)^{popc(k_hi & i_hi)} x[i_hi B + i_lo].
+// Output block k_hi therefore needs only a fold of the sparse input into a
+// B-point buffer z (the S-point high-bit stages, done at load time: x is only
+// M nonzeros, the rows of Omega), a B-point transform of z in shared memory
+// and a contiguous store.  Each persistent CTA stages a vector's r in shared
+// memory once (one bulk copy) and produces its S output blocks in turn, so
+// HBM traffic is exactly the algorithmic (M + N) * sizeof(V) per vector and
+// nothing intermediate leaves the SM.
+//
+// Register-tile passes: pass p transforms index bits [lo_p, lo_p + R_p) of z;
+// each thread holds 2^R_p elements of one group.  z is stored with one pad
+// element per row of 32 (the first pass's rows), which makes every pass
+// conflict-free: in pass 1 the lanes' rows are 33 elements apart, in later
+// passes consecutive lanes own consecutive low indices.
+#include "fmp_kcommon.cuh"
+
+namespace fmp {
+namespace {
+
+template <int R, class V>
+__device__ __forceinline__ void wht_regs(V* v) {
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) {
+      if (j & (1 << s)) continue;
+      const V a = v[j], b = v[j + (1 << s)];
+      v[j] = add(a, b);
+      v[j + (1 << s)] = sub(a, b);
+    }
+  }
+}
+
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
+
+// one register-tile pass over bits [LO, LO + R) of the padded buffer z; the
+// last pass scales and streams its block to global memory instead
+template <class V, int LOGB, int R1, int LO, int R, int NTH, bool LAST>
+__device__ __forceinline__ void fold_pass(V* z, V* __restrict__ out, double sc, int tid) {
+  constexpr int G = 1 << (LOGB - R);
+#pragma unroll 1
+  for (int g = tid; g < G; g += NTH) {
+    const int gl = g & ((1 << LO) - 1), gh = g >> LO;
+    const int base = (gh << (LO + R)) + gl;
+    V v[1 << R];
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) {
+      const int i = base + (j << LO);
+      v[j] = z[i + (i >> R1)];
+    }
+    wht_regs<R>(v);
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) {
+      const int i = base + (j << LO);
+      if constexpr (LAST) st_stream(out + i, scale(v[j], sc));
+      else z[i + (i >> R1)] = v[j];
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(mb)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// one bulk (TMA) copy global -> shared, completion counted on `mb`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(mb))
+      : "memory");
+}
+
+// Persistent: CTA c takes vectors c, c + grid, ...  Per vector, r is staged
+// in shared memory once (bulk copy; the next vector's copy is issued while
+// the last output block's passes 2-3 still run) and the S output blocks are
+// produced one after the other.  Thread g owns row g (32 consecutive i_lo)
+// during the fold: its rows of Omega come from the operator's fold table in
+// (position, input block) order, so every position's sum is formed in a
+// register in ascending i_hi order (deterministic) and the first register
+// pass (bits 0-4) follows without touching shared memory.
+template <class V, int LOGB, int R2, int R3, int NTH>
+__global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict__ tab,
+                                                     const uint32_t* __restrict__ roff, int m,
+                                                     int log2n, const V* __restrict__ in,
+                                                     V* __restrict__ out, int64_t batch, double sc,
+                                                     int use_bulk) {
+  constexpr int R1 = 5;
+  static_assert(R1 + R2 + R3 == LOGB && NTH == (1 << (LOGB - R1)), "pass widths");
+  constexpr int B = 1 << LOGB;
+  constexpr int ZN = B + (B >> R1);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar;
+  V* z = reinterpret_cast<V*>(smem_raw);
+  V* rb = z + ZN;                                                   // m values
+  uint32_t* tb = reinterpret_cast<uint32_t*>(rb + ((m + 3) & ~3));  // m entries
+  const int tid = threadIdx.x;
+  const int S = 1 << (log2n - LOGB);
+  const uint32_t rbytes = (uint32_t)m * (uint32_t)sizeof(V);
+  int64_t b = blockIdx.x;
+  if (b >= batch) return;
+  if (tid == 0 && use_bulk) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = tid; k < m; k += NTH) tb[k] = tab[k];
+  const uint32_t e0 = roff[tid], e1 = roff[tid + 1];
+  __syncthreads();
+  if (use_bulk) {
+    if (tid == 0) bulk_load(rb, in + b * m, rbytes, &mbar);
+  } else {
+    for (int k = tid; k < m; k += NTH) rb[k] = in[b * m + k];
+    __syncthreads();
+  }
+  const V zero = zero_of(V{});
+  for (uint32_t it = 0; b < batch; b += gridDim.x, ++it) {
+    if (use_bulk) mbar_wait(&mbar, it & 1);
+    V* ob = out + b * ((int64_t)S << LOGB);
+    for (int khi = 0; khi < S; ++khi) {
+      // entries of row tid in (position, input block) order: one running sum
+      // per position, stored when the position changes; positions without
+      // rows read as zero through `seen` (no zero fill)
+      V* row = z + tid * 33;
+      uint32_t seen = 0, jc = 32;
+      V acc = zero;
+      const uint32_t neg_mask = (uint32_t)khi;
+      for (uint32_t e = e0; e < e1; e += 4) {
+        uint32_t u[4];
+        V x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = e + q < e1 ? tb[e + q] : 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = u[q] != 0xffffffffu ? rb[u[q] & 0xfffffu] : zero;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (u[q] == 0xffffffffu) break;
+          const uint32_t j = u[q] >> 26;
+          if (j != jc) {
+            if (jc < 32) row[jc] = acc;
+            acc = zero;
+            jc = j;
+            seen |= 1u << j;
+          }
+          acc = (__popc((u[q] >> 20) & neg_mask) & 1) ? sub(acc, x[q]) : add(acc, x[q]);
+        }
+      }
+      if (jc < 32) row[jc] = acc;
+      V v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = (seen >> j) & 1 ? row[j] : zero;
+      wht_regs<R1>(v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) row[j] = v[j];
+      __syncthreads();
+      if (khi == S - 1) {
+        // every read of this vector's r is done: stage the next one
+        const int64_t nb = b + gridDim.x;
+        if (nb < batch) {
+          if (use_bulk) {
+            if (tid == 0) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              bulk_load(rb, in + nb * m, rbytes, &mbar);
+            }
+          }
+        }
+      }
+      V* o = ob + ((int64_t)khi << LOGB);
+      if constexpr (R3 == 0) {
+        fold_pass<V, LOGB, R1, R1, R2, NTH, true>(z, o, sc, tid);
+      } else {
+        fold_pass<V, LOGB, R1, R1, R2, NTH, false>(z, o, sc, tid);
+        __syncthreads();
+        fold_pass<V, LOGB, R1, R1 + R2, R3, NTH, true>(z, o, sc, tid);
+      }
+      __syncthreads();
+    }
+    if (!use_bulk) {
+      const int64_t nb = b + gridDim.x;
+      if (nb < batch) {
+        for (int k = tid; k < m; k += NTH) rb[k] = in[nb * m + k];
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <class V, int LOGB, int R2, int R3>
+cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  constexpr int B = 1 << LOGB, NTH = B >> 5;
+  const int q = LOGB - 11;
+  if (q < 0 || q > 3 || !op.fold_tab[q]) return cudaErrorNotSupported;
+  // one persistent CTA per vector in flight: small batches keep the job queue
+  if (a.batch < 64) return cudaErrorNotSupported;
+  const int64_t m = op.m;
+  const size_t smem = (size_t)(B + (B >> 5)) * sizeof(V) + (size_t)((m + 3) & ~3) * sizeof(V) + (size_t)m * 4;
+  if (smem + 1024 > (size_t)smem_optin()) return cudaErrorNotSupported;
+  auto kern = k_wht_fold<V, LOGB, R2, R3, NTH>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTH, smem);
+  const int64_t grid = std::min<int64_t>(a.batch, (int64_t)std::max(1, occ) * num_sms());
+  const bool bulk = ((uintptr_t)a.in % 16 == 0) && ((m * (int64_t)sizeof(V)) % 16 == 0);
+  kern<<<(unsigned)grid, NTH, smem, st>>>(op.fold_tab[q], op.fold_off[q], (int)m, op.log2n,
+                                          (const V*)a.in, (V*)a.out, a.batch,
+                                          1.0 / sqrt((double)op.n), bulk ? 1 : 0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// f32: 2^14-point blocks (smem: z 66 KB + r + the fold table), passes 5 + 5 + 4.
+// 8-byte and wider elements stay on the job queue: measured on config 3
+// (f64 0.375 ms fold vs 0.340 ms queue, c64 0.388 vs 0.338; f32 0.160 vs
+// 0.203), the wider fold is bound by shared-memory wavefronts and bank
+// conflicts of the r gathers.
+}  // namespace
+
+cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  if (op.kind != HADAMARD || !a.in_omega || a.out_omega || !a.out) return cudaErrorNotSupported;
+  const char* e = getenv("FMP_FOLD");  // FMP_FOLD=-1: job queue instead (timing tools)
+  if (e && atoi(e) < 0) return cudaErrorNotSupported;
+  if (a.dtype == F32) return launch_fold_k<float, 14, 5, 4>(a, st);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace fmp

@@ -100,6 +100,23 @@ def test_apply_adjoint_other_dtypes(fmp, oracle, dtype, tol):
         assert rel(h, want) < tol
 
 
+@pytest.mark.parametrize("n,m", [(65536, 8192), (65536, 8191), (1 << 17, 12345)])
+def test_apply_adjoint_fold_path(fmp, oracle, n, m):
+    """Batched f32 Hadamard adjoint beyond one CTA (batch >= 64): the one-pass
+    fold kernel (fmp_transform_fold.cu); m * 4 bytes not a multiple of 16
+    takes its plain-load staging instead of the bulk copy."""
+    om = oracle.make_row_selection(n, m, 11 + m)
+    op = fmp.SensingOperator("hadamard", n, om)
+    B = 70
+    R = np.stack([oracle.rng_complex_gaussian(oracle.derive_seed(m, b), m).real for b in range(B)])
+    R = R.astype(np.float32)
+    H, idx = op.apply_adjoint(R, argmax=True)
+    for b in (0, 1, 37, B - 1):
+        want = oracle.apply_adjoint("hadamard", n, om, R[b].astype(np.complex128))
+        assert rel(H[b], want) < 1e-6
+        assert idx[b] == oracle.argmax_magnitude(H[b].astype(np.complex128)) + 1
+
+
 # ------------------------------------------------------------ fast update
 def test_fast_update_campaign(fmp, oracle):
     # test_kernel.cpp:178-219 recipe: fast = Phi^H (y - Phi_Lambda x) within 1e-10
