@@ -15,8 +15,10 @@
 //     identical (the reference's own 1e-9 identification tie band absorbs the
 //     last-bit differences); rank deficiency uses the normal-equations pivot
 //     floor (solvers.cpp:32,144)
-//   - FlopCounter / CostReport carry the analytic Table-I counts (the GPU does
-//     not count executed operations)
+//   - FlopCounter / CostReport carry the reference's bookkeeping for the same
+//     operation sequence (transforms, fast updates, identification, the
+//     configured least-squares method), booked host-side: the GPU does not
+//     count the operations it executes
 //   - non-power-of-two Fourier sizes (the reference's dense fallback) throw
 //     std::invalid_argument
 //   - the batched overload omp_solve_batch is an addition

@@ -23,6 +23,8 @@
 
 using namespace fastmp;
 
+#include "../tests/cpp/counts_recipe.inc"
+
 namespace {
 
 TransformKind kind_of(int kind) {
@@ -378,6 +380,14 @@ int fmpo_ref_result_text(const char* instance, int mode, char* buf, uint64_t cap
     st = put_text(os.str(), buf, cap, len);
     if (!st) st = put_text(oc.str(), csv, csvcap, csvlen);
   });
+  return g ? g : st;
+}
+
+/* the FlopCounter bookkeeping recipe (tests/cpp/counts_recipe.inc) on an
+ * instance text */
+int fmpo_ref_counts_text(const char* instance, char* buf, uint64_t cap, uint64_t* len) {
+  int st = 0;
+  const int g = guard([&] { st = put_text(flop_counts_text(instance), buf, cap, len); });
   return g ? g : st;
 }
 

@@ -17,13 +17,17 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libfmp_cuda.so")
+# FMP_BUILD_DEFS / FMP_BUILD_OUT: an experimental variant (extra -D flags)
+# built into its own object directory and library, e.g. _variants/x.so
+DEFS = os.environ.get("FMP_BUILD_DEFS", "").split()
+_VOUT = os.environ.get("FMP_BUILD_OUT")
+OBJ = os.path.join(PKG, "_build") if not _VOUT else os.path.abspath(_VOUT) + "_obj"
+LIB = os.path.join(PKG, "libfmp_cuda.so") if not _VOUT else os.path.abspath(_VOUT) + ".so"
 FACADE = os.path.join(PKG, "libfastmp_b200.so")
 CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), *DEFS]
 SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_cosamp.cu", "fmp_large.cu", "fmp_fast_update.cu", "fmp_qr.cu", "fmp_transform.cu", "fmp_transform_4s.cu", "fmp_transform_fold.cu", "fmp_capi.cu", "fmp_host_gen.cpp"]
 HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh"]
 
@@ -56,6 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    if _VOUT:
+        return LIB
     # the C++ drop-in facade over the C ABI
     src = os.path.join(PKG, "host", "fastmp_facade.cpp")
     if force or not os.path.exists(FACADE) or os.path.getmtime(FACADE) < max(

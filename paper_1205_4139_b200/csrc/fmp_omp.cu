@@ -9,7 +9,7 @@ cudaError_t launch_omp_f64(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_f32(const OmpArgs& a, cudaStream_t st);
 
 int omp_grid(const DevOp&, int, int64_t batch, int64_t) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(batch, num_sms()));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)OMP_CTAS * num_sms()));
 }
 
 cudaError_t launch_omp(const OmpArgs& a, cudaStream_t st) {

@@ -27,7 +27,10 @@ namespace {
 
 
 constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
-constexpr int OLOGP = 3;
+#ifndef FMP_OLOGP
+#define FMP_OLOGP 3
+#endif
+constexpr int OLOGP = FMP_OLOGP;  // transform-buffer padding period 2^OLOGP
 constexpr int LSG = 8;  // threads per row / column in the least-squares passes
 constexpr int LSU = 4;  // loads per thread issued together in those passes
 
@@ -74,9 +77,10 @@ __device__ __forceinline__ int wofs(int T, int i, int j) {
 }
 
 // GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
+// 3 conjugate half read from global memory through L1;
 // Fourier only); BUFG: transform buffer in global memory (n beyond smem)
 template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
-__global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
+__global__ void __launch_bounds__(OMP_THREADS, OMP_CTAS) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[96];
   __shared__ unsigned redu[32];
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
                 : reinterpret_cast<V*>(sm);
   const V* gF = fourier_table<V>(op);
   const uint16_t* gH = op.glat;
-  if constexpr (GMODE > 0) {
+  if constexpr (GMODE == 1 || GMODE == 2) {
     if constexpr (!HAD) {
       V* s = reinterpret_cast<V*>(sm + a.off_g);
       const int cnt = GMODE == 2 ? n / 2 + 1 : n;
@@ -147,11 +151,11 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
   // Gram entry (Phi^H Phi)_{ab}: from the staged kernel when it is exact fp64
   // (c128 table, or the Hadamard integer lattice), else the fp64 table
   auto gram_of = [&](unsigned ga, unsigned gb) -> double2 {
-    if constexpr (GMODE > 0 && HAD) {
+    if constexpr ((GMODE == 1 || GMODE == 2) && HAD) {
       return make_double2((double)((int)gH[ga ^ gb] - 32768) / (double)n, 0.0);
     } else if constexpr (GMODE == 1 && sizeof(V) == 16) {
       return to_c128(gF[(ga - gb) & (unsigned)(n - 1)]);
-    } else if constexpr (GMODE == 2 && sizeof(V) == 16) {
+    } else if constexpr ((GMODE == 2 || GMODE == 3) && sizeof(V) == 16) {
       const unsigned j = (ga - gb) & (unsigned)(n - 1);
       return j <= (unsigned)(n >> 1) ? to_c128(gF[j]) : to_c128(conj(gF[n - j]));
     } else {
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
               V acc[RPT];
 #pragma unroll
               for (int r = 0; r < RPT; ++r) acc[r] = buf[padx<OLOGP>(i0 + lane + 32 * r)];
-              fast_tile<V, HAD, RPT, GMODE == 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
+              fast_tile<V, HAD, RPT, GMODE >= 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
                 const int i = i0 + lane + 32 * r;
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(OMP_THREADS, 1) k_omp(OmpK a) {
           } else {
             for (int i = tid; i < n; i += nth) {
               V acc = buf[padx<OLOGP>(i)];
-              fast_point<V, HAD, GMODE == 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
+              fast_point<V, HAD, GMODE >= 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
               const double mm = mag2(acc);
               msc[i] = mm;
               best = fmax(best, mm);
@@ -529,7 +533,9 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   const size_t tw = HAD ? 0 : al(2 * (((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) + 4) * sizeof(V);
   const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
                        al(4 * (size_t)((n + 31) / 32));
-  const size_t cap = (size_t)smem_optin() - 2048;
+  // OMP_CTAS > 1: the SM's shared memory (optin + 1 KB) split between CTAs
+  const size_t cap = OMP_CTAS == 1 ? (size_t)smem_optin() - 2048
+                                   : ((size_t)smem_optin() + 1024) / OMP_CTAS - 1024 - 2048;
   size_t tot = tw + small;
   // the transform buffer has first claim on smem (a global-memory buffer
   // sends every transform pass through L2); the kernel table follows and
@@ -543,6 +549,9 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   if (!(HAD && !op.glat)) {
     if (tot + gfull <= cap) { p.gmode = 1; tot += gfull; }
     else if (!HAD && tot + ghalf <= cap) { p.gmode = 2; tot += ghalf; }
+    // several CTAs per SM: the conjugate half stays in global memory, where
+    // the L1 left beside the CTAs' shared memory keeps it resident
+    else if (!HAD && OMP_CTAS > 1) p.gmode = 3;
   }
   p.rsm = tot + r <= cap;
   if (p.rsm) tot += r;
@@ -564,6 +573,12 @@ template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
 void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
   auto f = k_omp<V, HAD, RPT, GMODE, BUFG>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (OMP_CTAS > 1) {
+    // smallest carveout that holds the resident CTAs: the rest is L1
+    const int pct = (int)std::min<size_t>(100, (OMP_CTAS * (smem + 3072) * 100 + (size_t)smem_optin()) /
+                                                   ((size_t)smem_optin() + 1024) + 1);
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  }
   f<<<grid, OMP_THREADS, smem, st>>>(k);
 }
 
@@ -571,6 +586,7 @@ template <class V, bool HAD, int RPT, bool BUFG>
 void launch_g(const OmpK& k, int gmode, int grid, size_t smem, cudaStream_t st) {
   if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG>(k, grid, smem, st);
   else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG>(k, grid, smem, st);
+  else if (!HAD && gmode == 3) launch_k<V, HAD, RPT, 3, BUFG>(k, grid, smem, st);
   else launch_k<V, HAD, RPT, 0, BUFG>(k, grid, smem, st);
 }
 

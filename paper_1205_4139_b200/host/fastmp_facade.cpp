@@ -53,6 +53,87 @@ void validate_unitary(TransformKind kind, std::size_t n) {
     throw std::invalid_argument("non power-of-two Fourier sizes are not implemented on the GPU path");
 }
 
+
+// ------------------------------------------- FlopCounter bookkeeping (f4)
+// The reference books flops per operation (cost_model.hpp:19-31); the device
+// work is organised differently, so the facade books the counts a reference
+// caller would read from the same operation sequence.
+unsigned log2_size(std::size_t n) {
+  unsigned l = 0;
+  while ((std::size_t{1} << l) < n) ++l;
+  return l;
+}
+// fft_pow2 / fht (transform.cpp:60-100) and the 1/sqrt(N) scaling of
+// forward / adjoint (transform.cpp:133,150); apply / apply_adjoint book the
+// transform they run (sensing.cpp:93-109)
+void book_transform(FlopCounter* fc, TransformKind kind, std::size_t n) {
+  if (!fc) return;
+  const std::uint64_t lg = log2_size(n);
+  if (kind == TransformKind::Fourier) fc->complex_mul += std::uint64_t(n) / 2 * lg;
+  fc->complex_add += std::uint64_t(n) * lg;
+  fc->real_mul += 2 * std::uint64_t(n);
+}
+// fast_update (kernel.cpp:209-303): d = number of distinct Hadamard values
+void book_fast_update(FlopCounter* fc, TransformKind kind, std::size_t n, std::size_t atoms,
+                      std::size_t d, bool symmetry) {
+  if (!fc || atoms == 0) return;
+  const std::uint64_t s = atoms;
+  if (kind == TransformKind::Hadamard) {
+    fc->real_mul += 2 * std::uint64_t(d) * s;
+  } else if (!symmetry) {
+    fc->complex_mul += std::uint64_t(n) * s;
+  } else {
+    const std::uint64_t pairs = n >= 1 ? (n - 1) / 2 : 0;  // j >= 1 with 2 j < n
+    fc->complex_mul += pairs * s;
+    fc->real_add += 2 * pairs * s;
+    fc->real_mul += (2 + (n % 2 == 0 && n > 1 ? 2 : 0)) * s;
+  }
+  fc->complex_add += std::uint64_t(n) * s;
+}
+// dot_conj bookkeeping (solvers.cpp:48-53)
+void book_dot(FlopCounter& fc, std::size_t len, std::uint64_t count = 1) {
+  if (len == 0) return;
+  fc.complex_mul += count * len;
+  fc.complex_add += count * (len - 1);
+}
+// normal_equations_solve on s columns (solvers.cpp:120-177); `done` pivots
+// completed (s unless it raised at pivot `done`)
+void book_normal(FlopCounter& fc, std::size_t rows, std::size_t s, std::size_t done) {
+  const std::uint64_t S = s;
+  book_dot(fc, rows, S * (S + 1) / 2 + S);
+  for (std::uint64_t j = 0; j < done; ++j) {
+    fc.complex_mul += S - j;
+    fc.complex_add += (S - j) * (j + 1);
+  }
+  if (done < s) return;
+  fc.complex_mul += S * S;
+  fc.complex_add += S * S;
+}
+// one least-squares step of omp_solve with s columns (solvers.cpp:370-388):
+// IncrementalQR push + solve (solvers.cpp:223-274) or the normal equations,
+// then update_residual (solvers.cpp:180-192); `ok` false: the step ended rank
+// deficient at its new column
+void book_ls_step(FlopCounter& fc, LeastSquaresMethod method, std::size_t rows, std::size_t s,
+                  bool ok) {
+  const std::uint64_t S = s;
+  if (method == LeastSquaresMethod::IncrementalQR) {
+    const std::uint64_t q = S - 1;
+    book_dot(fc, rows, 2 * q);
+    fc.complex_mul += 2 * q * rows;
+    fc.complex_add += 2 * q * rows;
+    fc.real_mul += 2 * std::uint64_t(rows);
+    fc.real_add += rows;
+    if (!ok) return;
+    book_dot(fc, rows, S);
+    fc.complex_mul += S * (S + 1) / 2;
+    fc.complex_add += S * (S - 1) / 2;
+  } else {
+    book_normal(fc, rows, s, ok ? s : s - 1);
+    if (!ok) return;
+  }
+  fc.complex_mul += S * rows;
+  fc.complex_add += (S + 1) * rows;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ types
@@ -174,7 +255,7 @@ cvec StructuredUnitary::forward(const cvec& v, FlopCounter* fc) const {
   if (v.size() != n_) throw std::invalid_argument("forward: length mismatch");
   cvec out(n_);
   check(fmp_unitary_forward(static_cast<fmp_op>(unit_op()), FMP_C128, raw(v), 1, raw(out)));
-  if (fc) fc->real_mul += 2 * std::uint64_t(n_);
+  book_transform(fc, kind_, n_);
   return out;
 }
 
@@ -182,7 +263,7 @@ cvec StructuredUnitary::adjoint(const cvec& v, FlopCounter* fc) const {
   if (v.size() != n_) throw std::invalid_argument("adjoint: length mismatch");
   cvec out(n_);
   check(fmp_unitary_adjoint(static_cast<fmp_op>(unit_op()), FMP_C128, raw(v), 1, raw(out)));
-  if (fc) fc->real_mul += 2 * std::uint64_t(n_);
+  book_transform(fc, kind_, n_);
   return out;
 }
 
@@ -258,7 +339,7 @@ cvec SensingOperator::apply(const cvec& x, FlopCounter* fc) const {
   if (x.size() != n()) throw std::invalid_argument("apply: length mismatch");
   cvec out(m());
   check(fmp_apply(static_cast<fmp_op>(op_.get()), FMP_C128, raw(x), 1, raw(out)));
-  if (fc) fc->real_mul += 2 * std::uint64_t(n());
+  book_transform(fc, unitary_.kind(), n());
   return out;
 }
 
@@ -266,7 +347,7 @@ cvec SensingOperator::apply_adjoint(const cvec& r, FlopCounter* fc) const {
   if (r.size() != m()) throw std::invalid_argument("apply_adjoint: length mismatch");
   cvec out(n());
   check(fmp_apply_adjoint(static_cast<fmp_op>(op_.get()), FMP_C128, raw(r), 1, raw(out), nullptr));
-  if (fc) fc->real_mul += 2 * std::uint64_t(n());
+  book_transform(fc, unitary_.kind(), n());
   return out;
 }
 
@@ -396,9 +477,9 @@ CorrelationKernel compute_kernel(const SensingOperator& op, FlopCounter* fc) {
   }
   // keep the operator alive with the kernel (fast_update runs on it)
   k.device_op = op.device_handle();
-  if (fc) {
-    fc->real_mul += 4 * std::uint64_t(k.n);  // two scaled transforms (kernel.cpp:33)
-  }
+  // apply_adjoint(apply(e1)) (kernel.cpp:33)
+  book_transform(fc, k.kind, k.n);
+  book_transform(fc, k.kind, k.n);
   return k;
 }
 
@@ -413,7 +494,7 @@ std::size_t PermutationAction::map_index(std::size_t i) const {
 
 cvec fast_update(const cvec& h0, const CorrelationKernel& kernel,
                  const std::vector<std::size_t>& support, const cvec& coeffs,
-                 const FastUpdateOptions&, FlopCounter* fc) {
+                 const FastUpdateOptions& opts, FlopCounter* fc) {
   if (h0.size() != kernel.n) throw std::invalid_argument("fast_update: h0 length");
   if (support.size() != coeffs.size())
     throw std::invalid_argument("fast_update: support/coefficient mismatch");
@@ -424,10 +505,8 @@ cvec fast_update(const cvec& h0, const CorrelationKernel& kernel,
   check(fmp_fast_update(static_cast<fmp_op>(kernel.device_op.get()), FMP_C128, raw(h0),
                         sup.empty() ? nullptr : sup.data(), coeffs.empty() ? nullptr : raw(coeffs),
                         sup.size(), 1, raw(h), nullptr));
-  if (fc) {
-    fc->complex_mul += std::uint64_t(kernel.n) * support.size();
-    fc->complex_add += std::uint64_t(kernel.n) * support.size();
-  }
+  book_fast_update(fc, kernel.kind, kernel.n, support.size(), kernel.values.size(),
+                   opts.fourier_symmetry);
   return h;
 }
 
@@ -476,6 +555,14 @@ std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std
   r.history = cfg.record_correlations ? raw(hist) : nullptr;
   check(fmp_omp_solve(static_cast<fmp_op>(op.handle()), FMP_C128, raw(y), B, &c, &r));
   const TransformKind kind = op.unitary().kind();
+  // distinct Hadamard kernel values (the fast rows' bookkeeping), read once
+  std::size_t nvalues = 0;
+  if (kind == TransformKind::Hadamard) {
+    bool any_fast = false;
+    for (std::size_t b = 0; b < B && !any_fast; ++b)
+      for (std::size_t t = 2; t <= hlen[b] && !any_fast; ++t) any_fast = modes[b * T + t - 1] != 0;
+    if (any_fast) nvalues = compute_kernel(op).values.size();
+  }
   for (std::size_t b = 0; b < B; ++b) {
     RecoveryResult& res = results[b];
     res.x_hat.assign(n, cplx(0.0));
@@ -491,6 +578,9 @@ std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std
       res.support_history.emplace_back(res.support.begin(), res.support.begin() + t);
     res.costs.kind = kind;
     res.costs.n = n;
+    // counted flops as omp_solve books them (solvers.cpp:343-395)
+    FlopCounter kernel_fc, ls_fc, id_fc;
+    bool kernel_built = false;
     for (std::size_t t = 1; t <= hlen[b]; ++t) {
       IterationCost row;
       row.t = t;
@@ -498,12 +588,29 @@ std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std
       row.mode_used = fast ? CorrelationMode::Fast : CorrelationMode::Conventional;
       row.analytic_flops = fast ? fast_iteration_flops(kind, n, t)
                                 : conventional_iteration_flops(kind, n);
-      row.counted.complex_add = row.analytic_flops / kComplexAddFlops;
+      if (fast && t >= 2) {
+        if (!kernel_built) {
+          book_transform(&kernel_fc, kind, n);
+          book_transform(&kernel_fc, kind, n);
+          kernel_built = true;
+        }
+        book_fast_update(&row.counted, kind, n, t - 1, nvalues, cfg.fourier_symmetry);
+      } else {
+        book_transform(&row.counted, kind, n);
+      }
+      id_fc.real_mul += 2 * std::uint64_t(n);  // argmax_magnitude (solvers.cpp:90-96)
+      id_fc.real_add += n;
       res.costs.iterations.push_back(row);
       if (cfg.record_correlations)
         res.correlation_history.emplace_back(hist.begin() + (b * T + t - 1) * n,
                                              hist.begin() + (b * T + t) * n);
     }
+    const std::size_t steps = size[b] + (res.rank_deficient_abort ? 1 : 0);
+    for (std::size_t s = 1; s <= steps; ++s)
+      book_ls_step(ls_fc, cfg.ls_method, m, s, s <= size[b]);
+    res.costs.kernel_precompute_flops = kernel_fc.flops();
+    res.costs.least_squares_flops = ls_fc.flops();
+    res.costs.identification_flops = id_fc.flops();
   }
   return results;
 }
@@ -678,6 +785,8 @@ cvec least_squares(const SensingOperator& op, const std::vector<std::size_t>& su
   const int st = fmp_least_squares(static_cast<fmp_op>(op.handle()), FMP_C128, raw(y),
                                    sup.empty() ? nullptr : sup.data(), sup.size(), 1,
                                    x.empty() ? nullptr : raw(x), &pos);
+  if (fc && (st == FMP_OK || st == FMP_ERANK))
+    book_normal(*fc, op.m(), support.size(), st == FMP_OK ? support.size() : (std::size_t)pos);
   if (st != FMP_OK) raise(st, pos);
   return x;
 }

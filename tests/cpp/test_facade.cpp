@@ -18,6 +18,8 @@
 
 using namespace fastmp;
 
+#include "counts_recipe.inc"
+
 static int g_fail = 0, g_pass = 0;
 #define CHECK(cond)                                                                 \
   do {                                                                              \
@@ -386,6 +388,12 @@ int main(int argc, char** argv) {
       double nn = 0.0;
       for (const cplx& z : inst.noise) nn += std::norm(z);
       CHECK(std::sqrt(nn) < 0.2 * std::sqrt(double(inst.m)));  // noise recovered by apply()
+      // FlopCounter bookkeeping: the reference's counts_*.txt line for line
+      {
+        const std::string got = flop_counts_text(want), ref = slurp(dir + "/counts_" + stem + ".txt");
+        CHECK(!ref.empty() && got == ref);
+        if (got != ref) std::fprintf(stderr, "counts %s:\n%s\nreference:\n%s\n", stem, got.c_str(), ref.c_str());
+      }
       const SensingOperator op = make_operator(inst);
       for (const char* mode : {"conventional", "fast"}) {
         SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
@@ -419,7 +427,8 @@ int main(int argc, char** argv) {
           nrm += b * b;
         }
         CHECK(std::sqrt(err) <= 1e-10 * std::sqrt(nrm));
-        // cost CSV: the same rows (t, mode, analytic flops, relative cost)
+        // cost CSV: the reference's file line for line (t, mode, analytic and
+        // counted flops, relative cost; counted totals)
         std::ostringstream co;
         res.costs.write_csv(co);
         std::istringstream gc(co.str()), rc(slurp(dir + "/costs_" + stem + "_" + mode + ".csv"));
@@ -427,7 +436,10 @@ int main(int argc, char** argv) {
         bool rows_ok = true;
         while (std::getline(rc, rl)) {
           if (!std::getline(gc, gl)) { rows_ok = false; break; }
-          if (rl.rfind("#", 0) == 0) continue;  // counted totals: analytic here
+          if (rl.rfind("#", 0) == 0) {  // counted totals (kernel, least squares, identification)
+            rows_ok &= gl == rl;
+            continue;
+          }
           auto cols = [](const std::string& l) {
             std::vector<std::string> v;
             std::stringstream ss(l);
@@ -437,7 +449,7 @@ int main(int argc, char** argv) {
           };
           const auto a = cols(gl), b = cols(rl);
           rows_ok &= a.size() == 5 && b.size() == 5 && a[0] == b[0] && a[1] == b[1] &&
-                     a[2] == b[2] && a[4] == b[4];
+                     a[2] == b[2] && a[3] == b[3] && a[4] == b[4];
         }
         CHECK(rows_ok);
       }

@@ -147,6 +147,7 @@ def text_fixtures():
     L.fmpo_ref_result_text.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_uint64,
                                        C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64,
                                        C.POINTER(C.c_uint64)]
+    L.fmpo_ref_counts_text.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
     cases = [("fourier", 64, 32, 4, 0.0, 11), ("hadamard", 64, 32, 4, 0.05, 12),
              ("fourier", 256, 64, 8, 0.05, 13), ("hadamard", 1024, 256, 16, 0.0, 14)]
     for kind, n, m, k, noise, seed in cases:
@@ -158,6 +159,10 @@ def text_fixtures():
         stem = f"{kind}_{n}_{m}_{k}_{seed}"
         with open(os.path.join(OUT, f"instance_{stem}.txt"), "wb") as f:
             f.write(inst)
+        cbuf = C.create_string_buffer(1 << 20)
+        assert L.fmpo_ref_counts_text(inst, cbuf, len(cbuf), C.byref(ln)) == 0
+        with open(os.path.join(OUT, f"counts_{stem}.txt"), "wb") as f:
+            f.write(cbuf.value)
         for mode, code in (("conventional", 0), ("fast", 1)):
             rb = C.create_string_buffer(1 << 20)
             cb = C.create_string_buffer(1 << 20)
