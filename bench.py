@@ -270,14 +270,16 @@ def reference_arm(args, ws, rank):
 
 
 # --------------------------------------------------------------- our arm
-def parse_mode(mode, n, kind):
+def parse_mode(mode, n, kind, gpu_fu=None):
+    """(mode name, fast_until); gpu_fu: the switch point mode "gpu" takes for
+    this batched solve (fmp.gpu_crossover_for), else the one-CTA value."""
     import paper_1205_4139_b200 as fmp
     if mode.startswith("custom:"):
         return "custom", int(mode.split(":")[1])
     if mode == "adaptive":
         return "adaptive", fmp.crossover_iteration(kind, n)
     if mode == "gpu":
-        return "custom", fmp.gpu_crossover(kind, n)
+        return "custom", gpu_fu if gpu_fu is not None else fmp.gpu_crossover(kind, n)
     if mode == "fast":
         return "fast", 1 << 62
     if mode == "conventional":
@@ -452,15 +454,16 @@ def our_arm(args, ws, rank, local):
     # one untimed solve first so one-time costs (workspace allocation, first
     # launches) do not land on whichever candidate is probed first
     cands = ["gpu", "fast", "adaptive", "conventional"] if args.mode == "auto" else [args.mode]
-    step(*parse_mode(cands[0], n, CFG["kind"]))
+    gfu = fmp.gpu_crossover_for(op, Y.dtype, B, T)
+    step(*parse_mode(cands[0], n, CFG["kind"], gfu))
     torch.cuda.synchronize()
     per = {}
     for c in cands:
-        mname, fu = parse_mode(c, n, CFG["kind"])
+        mname, fu = parse_mode(c, n, CFG["kind"], gfu)
         tot, _ = timed(mname, fu, 3, 1)
         per[c] = allreduce_max(tot / 3, ws)
     best = min(per, key=per.get)
-    mname, fu = parse_mode(best, n, CFG["kind"])
+    mname, fu = parse_mode(best, n, CFG["kind"], gfu)
 
     with Clocks(local) as clk:
         tot_ms, launches = timed(mname, fu, args.steps, args.warmup)

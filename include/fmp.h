@@ -95,8 +95,13 @@ int fmp_operator_kernel(fmp_op op, double* c_out, double* values_out,
 /* crossover_iteration (cost_model.hpp:76): the Adaptive switch point */
 uint64_t fmp_crossover_iteration(int kind, uint64_t n);
 /* the same switch point measured for this GPU path (FMP_MODE_GPU): fast
- * updates while t <= this, transforms afterwards */
+ * updates while t <= this, transforms afterwards — for the one-CTA-per-SM
+ * solver (small batches, the sharded config-5 solver) */
 uint64_t fmp_gpu_crossover(int kind, uint64_t n);
+/* the switch point FMP_MODE_GPU uses for a batched solve of `batch` problems
+ * of `dtype` with max_iterations T on op (the solver's configuration depends
+ * on the batch: two CTAs per SM when both fit) */
+uint64_t fmp_gpu_crossover_for(fmp_op op, int dtype, uint64_t batch, uint64_t max_iterations);
 
 /* ------------------------------------------------------ transforms (batched) */
 /* SensingOperator::apply, Phi x (sensing.cpp:93-100): x batch x n -> y batch x m */

@@ -95,6 +95,7 @@ _sig("fmp_operator_info", C.c_int, _vp, C.POINTER(C.c_int), C.POINTER(_u64), C.P
 _sig("fmp_operator_kernel", C.c_int, _vp, _vp, _vp, _vp, C.POINTER(_u64))
 _sig("fmp_crossover_iteration", _u64, C.c_int, _u64)
 _sig("fmp_gpu_crossover", _u64, C.c_int, _u64)
+_sig("fmp_gpu_crossover_for", _u64, _vp, C.c_int, _u64, _u64)
 _sig("fmp_apply", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
 _sig("fmp_apply_dev", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
 _sig("fmp_apply_adjoint", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
@@ -243,9 +244,16 @@ def crossover_iteration(kind, n: int) -> int:
 
 
 def gpu_crossover(kind, n: int) -> int:
-    """Switch point of the GPU-calibrated Adaptive mode ("gpu")."""
+    """Switch point of the GPU-calibrated Adaptive mode ("gpu") for the
+    one-CTA-per-SM solver (small batches)."""
     kind = KINDS.get(kind, kind)
     return int(_lib.fmp_gpu_crossover(kind, n))
+
+
+def gpu_crossover_for(op: "SensingOperator", dtype, batch: int, max_iterations: int) -> int:
+    """Switch point mode "gpu" uses for this batched solve (the solver runs two
+    CTAs per SM when the batch and shared memory allow, which moves it)."""
+    return int(_lib.fmp_gpu_crossover_for(op.handle, DTYPES[np.dtype(dtype)], batch, max_iterations))
 
 
 def make_row_selection(n: int, m: int, seed: int) -> np.ndarray:
@@ -873,7 +881,7 @@ def apply_adjoint_dev(op: SensingOperator, r, h_out=None, argmax_out=None,
 __all__ = [
     "Context", "SensingOperator", "CorrelationKernel", "compute_kernel", "fast_update",
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
-    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "make_row_selection", "make_batch", "derive_seed",
+    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "gpu_crossover_for", "make_row_selection", "make_batch", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
     "least_squares", "IncrementalQR", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
     "LargeShard", "LocalExchange", "sharded_solve", "large_solve",

@@ -204,6 +204,12 @@ uint64_t fmp_gpu_crossover(int kind, uint64_t n) {
   return kind == FMP_FOURIER ? (8 * logn) / 3 : 2 * logn;
 }
 
+uint64_t fmp_gpu_crossover_for(fmp_op op, int dtype, uint64_t batch, uint64_t max_iterations) {
+  if (!op || dtype < 0 || dtype > 3) return 0;
+  cudaSetDevice(op->ctx->device);
+  return (uint64_t)fmp::omp_gpu_fast_until(op->d, dtype, (int64_t)batch, (int64_t)max_iterations);
+}
+
 int fmp_ctx_create(int device, fmp_ctx* out) {
   if (!out) return fail(FMP_EINVAL, "null output handle");
   int count = 0;
@@ -715,12 +721,13 @@ static int omp_validate(fmp_op op, int dtype, const fmp_omp_config* cfg) {
   return FMP_OK;
 }
 
-static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg) {
+static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg, int dtype, uint64_t batch) {
   switch (cfg->mode) {
     case FMP_MODE_CONVENTIONAL: return 0;
     case FMP_MODE_FAST: return std::numeric_limits<int64_t>::max();
     case FMP_MODE_ADAPTIVE: return (int64_t)fmp_crossover_iteration(op->d.kind, (uint64_t)op->d.n);
-    case FMP_MODE_GPU: return (int64_t)fmp_gpu_crossover(op->d.kind, (uint64_t)op->d.n);
+    case FMP_MODE_GPU:
+      return fmp::omp_gpu_fast_until(op->d, dtype, (int64_t)batch, (int64_t)cfg->max_iterations);
     default: return (int64_t)std::min<uint64_t>(cfg->fast_until, (uint64_t)INT64_MAX);
   }
 }
@@ -742,7 +749,7 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   a.tol = dtol;
   a.batch = (int64_t)batch;
   a.max_iter = T;
-  a.fast_until = fast_until_of(op, cfg);
+  a.fast_until = fast_until_of(op, cfg, dtype, batch);
   a.support = out->support;
   a.coeffs = (double2*)out->coeffs;
   a.size = out->support_size;

@@ -62,10 +62,6 @@ constexpr int LOGP = 4;
 #define FMP_OMP_THREADS 512
 #endif
 constexpr int OMP_THREADS = FMP_OMP_THREADS;
-#ifndef FMP_OMP_CTAS
-#define FMP_OMP_CTAS 1
-#endif
-constexpr int OMP_CTAS = FMP_OMP_CTAS;  // resident fused-solver CTAs per SM
 constexpr int FU_THREADS = 512;
 
 __device__ __forceinline__ double inv_sqrt_n(int n) { return 1.0 / sqrt((double)n); }

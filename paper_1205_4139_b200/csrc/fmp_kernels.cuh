@@ -170,6 +170,10 @@ cudaError_t launch_omp(const OmpArgs& a, cudaStream_t stream);
 cudaError_t launch_cosamp(const CosArgs& a, cudaStream_t stream);
 // resident CTA count the OMP launcher will use (sizes the workspaces)
 int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
+// resident fused-solver CTAs per SM for this launch (1 or 2) and the switch
+// point of FMP_MODE_GPU for it
+int omp_ctas(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
+int omp_gpu_fast_until(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 int fast_update_grid(const DevOp& op, int dtype, int64_t batch);
 // largest n the smem-resident transform handles for this element size
 int64_t transform_max_n(int dtype);

@@ -7,9 +7,30 @@ cudaError_t launch_omp_c128(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_c64(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_f64(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_f32(const OmpArgs& a, cudaStream_t st);
+int omp_ctas_c128(const DevOp& op, int64_t batch, int64_t T);
+int omp_ctas_c64(const DevOp& op, int64_t batch, int64_t T);
 
-int omp_grid(const DevOp&, int, int64_t batch, int64_t) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)OMP_CTAS * num_sms()));
+int omp_ctas(const DevOp& op, int dtype, int64_t batch, int64_t T) {
+  switch (dtype) {
+    case C128: return omp_ctas_c128(op, batch, T);
+    case C64: return omp_ctas_c64(op, batch, T);
+  }
+  return 1;
+}
+
+int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t T) {
+  const int64_t slots = (int64_t)omp_ctas(op, dtype, batch, T) * num_sms();
+  return (int)std::max<int64_t>(1, std::min<int64_t>(batch, slots));
+}
+
+int omp_gpu_fast_until(const DevOp& op, int dtype, int64_t batch, int64_t T) {
+  // measured on B200 (bench.py --mode custom:T sweeps): a Fourier transform
+  // iteration of the one-CTA solver costs about as much as 8 log2(N) / 3
+  // fast-update atoms, of the two-CTA solver (kernel table read through L1)
+  // 4 log2(N) / 3; the Hadamard FWHT needs no twiddles
+  const int64_t logn = op.log2n;
+  if (op.kind == HADAMARD) return (int)(2 * logn);
+  return (int)((omp_ctas(op, dtype, batch, T) == 2 ? 4 : 8) * logn / 3);
 }
 
 cudaError_t launch_omp(const OmpArgs& a, cudaStream_t st) {

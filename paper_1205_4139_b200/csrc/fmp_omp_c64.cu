@@ -5,4 +5,7 @@ namespace fmp {
 cudaError_t launch_omp_c64(const OmpArgs& a, cudaStream_t st) {
   return a.op->kind == HADAMARD ? launch_omp_v<float2, true>(a, st) : launch_omp_v<float2, false>(a, st);
 }
+int omp_ctas_c64(const DevOp& op, int64_t batch, int64_t T) {
+  return op.kind == HADAMARD ? 1 : omp_ctas_v<float2, false>(op, batch, T);
+}
 }  // namespace fmp

@@ -77,10 +77,10 @@ __device__ __forceinline__ int wofs(int T, int i, int j) {
 }
 
 // GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
-// 3 conjugate half read from global memory through L1;
-// Fourier only); BUFG: transform buffer in global memory (n beyond smem)
-template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
-__global__ void __launch_bounds__(OMP_THREADS, OMP_CTAS) k_omp(OmpK a) {
+// Fourier only); BUFG: transform buffer in global memory (n beyond smem);
+// NT threads per CTA, CT CTAs resident per SM (launch bounds)
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT>
+__global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[96];
   __shared__ unsigned redu[32];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(OMP_THREADS, OMP_CTAS) k_omp(OmpK a) {
       return make_double2((double)((int)gH[ga ^ gb] - 32768) / (double)n, 0.0);
     } else if constexpr (GMODE == 1 && sizeof(V) == 16) {
       return to_c128(gF[(ga - gb) & (unsigned)(n - 1)]);
-    } else if constexpr ((GMODE == 2 || GMODE == 3) && sizeof(V) == 16) {
+    } else if constexpr (GMODE == 2 && sizeof(V) == 16) {
       const unsigned j = (ga - gb) & (unsigned)(n - 1);
       return j <= (unsigned)(n >> 1) ? to_c128(gF[j]) : to_c128(conj(gF[n - j]));
     } else {
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(OMP_THREADS, OMP_CTAS) k_omp(OmpK a) {
               V acc[RPT];
 #pragma unroll
               for (int r = 0; r < RPT; ++r) acc[r] = buf[padx<OLOGP>(i0 + lane + 32 * r)];
-              fast_tile<V, HAD, RPT, GMODE >= 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
+              fast_tile<V, HAD, RPT, GMODE == 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
                 const int i = i0 + lane + 32 * r;
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(OMP_THREADS, OMP_CTAS) k_omp(OmpK a) {
           } else {
             for (int i = tid; i < n; i += nth) {
               V acc = buf[padx<OLOGP>(i)];
-              fast_point<V, HAD, GMODE >= 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
+              fast_point<V, HAD, GMODE == 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
               const double mm = mag2(acc);
               msc[i] = mm;
               best = fmax(best, mm);
@@ -520,7 +520,7 @@ struct OmpPlan {
 };
 
 template <class V, bool HAD>
-OmpPlan omp_plan(const DevOp& op, int64_t T) {
+OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
   OmpPlan p{};
   const int64_t n = op.n, m = op.m;
   auto al = [](size_t b) { return ((b + 15) / 16) * 16; };
@@ -533,9 +533,9 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   const size_t tw = HAD ? 0 : al(2 * (((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) + 4) * sizeof(V);
   const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
                        al(4 * (size_t)((n + 31) / 32));
-  // OMP_CTAS > 1: the SM's shared memory (optin + 1 KB) split between CTAs
-  const size_t cap = OMP_CTAS == 1 ? (size_t)smem_optin() - 2048
-                                   : ((size_t)smem_optin() + 1024) / OMP_CTAS - 1024 - 2048;
+  // ctas > 1: the SM's shared memory (optin + 1 KB) split between the CTAs
+  const size_t cap = ctas == 1 ? (size_t)smem_optin() - 2048
+                               : ((size_t)smem_optin() + 1024) / ctas - 1024 - 2048;
   size_t tot = tw + small;
   // the transform buffer has first claim on smem (a global-memory buffer
   // sends every transform pass through L2); the kernel table follows and
@@ -551,7 +551,6 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
     else if (!HAD && tot + ghalf <= cap) { p.gmode = 2; tot += ghalf; }
     // several CTAs per SM: the conjugate half stays in global memory, where
     // the L1 left beside the CTAs' shared memory keeps it resident
-    else if (!HAD && OMP_CTAS > 1) p.gmode = 3;
   }
   p.rsm = tot + r <= cap;
   if (p.rsm) tot += r;
@@ -569,31 +568,24 @@ OmpPlan omp_plan(const DevOp& op, int64_t T) {
   return p;
 }
 
-template <class V, bool HAD, int RPT, int GMODE, bool BUFG>
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT>
 void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
-  auto f = k_omp<V, HAD, RPT, GMODE, BUFG>;
+  auto f = k_omp<V, HAD, RPT, GMODE, BUFG, NT, CT>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (OMP_CTAS > 1) {
-    // smallest carveout that holds the resident CTAs: the rest is L1
-    const int pct = (int)std::min<size_t>(100, (OMP_CTAS * (smem + 3072) * 100 + (size_t)smem_optin()) /
-                                                   ((size_t)smem_optin() + 1024) + 1);
-    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-  }
-  f<<<grid, OMP_THREADS, smem, st>>>(k);
+  f<<<grid, NT, smem, st>>>(k);
 }
 
-template <class V, bool HAD, int RPT, bool BUFG>
+template <class V, bool HAD, int RPT, bool BUFG, int NT, int CT>
 void launch_g(const OmpK& k, int gmode, int grid, size_t smem, cudaStream_t st) {
-  if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG>(k, grid, smem, st);
-  else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG>(k, grid, smem, st);
-  else if (!HAD && gmode == 3) launch_k<V, HAD, RPT, 3, BUFG>(k, grid, smem, st);
-  else launch_k<V, HAD, RPT, 0, BUFG>(k, grid, smem, st);
+  if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG, NT, CT>(k, grid, smem, st);
+  else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG, NT, CT>(k, grid, smem, st);
+  else launch_k<V, HAD, RPT, 0, BUFG, NT, CT>(k, grid, smem, st);
 }
 
-template <class V, bool HAD, int RPT>
+template <class V, bool HAD, int RPT, int NT, int CT>
 cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   const DevOp& op = *a.op;
-  const OmpPlan p = omp_plan<V, HAD>(op, a.max_iter);
+  const OmpPlan p = omp_plan<V, HAD>(op, a.max_iter, CT);
   if (p.total > (size_t)smem_optin() - 2048) return cudaErrorInvalidConfiguration;
   OmpK k{};
   k.op = op;
@@ -631,19 +623,43 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.margin = is_double(a.dtype) ? 1e-10 : 1e-5;
   k.phase_ws = a.phase_ws;
   const int grid = std::max(1, a.grid);
-  if (p.bufg) launch_g<V, HAD, RPT, true>(k, p.gmode, grid, p.total, st);
-  else launch_g<V, HAD, RPT, false>(k, p.gmode, grid, p.total, st);
+  if constexpr (CT == 1) {
+    if (p.bufg) launch_g<V, HAD, RPT, true, NT, CT>(k, p.gmode, grid, p.total, st);
+    else launch_g<V, HAD, RPT, false, NT, CT>(k, p.gmode, grid, p.total, st);
+  } else {
+    if (p.bufg) return cudaErrorInvalidConfiguration;
+    launch_g<V, HAD, RPT, false, NT, CT>(k, p.gmode, grid, p.total, st);
+  }
   ++g_launches;
   return cudaGetLastError();
 }
 
+// Two resident CTAs of 256 threads per SM (two problems in flight: one's
+// latency-bound identification / least-squares phases overlap the other's
+// transforms) when both transform buffers fit in shared memory and the batch
+// fills them; measured on config 2 (B200): 239 k against 227 k recoveries/s at
+// the best switch point of each.  Fourier only (the Hadamard lattice path
+// keeps its kernel table in shared memory).
+template <class V, bool HAD>
+int omp_ctas_v(const DevOp& op, int64_t batch, int64_t T) {
+  const char* e = getenv("FMP_OMP_CTAS");
+  if (e && atoi(e) == 1) return 1;
+  if (HAD || sizeof(V) < 8 || op.n < 32 * 8 * 8) return 1;
+  if (batch < 2 * (int64_t)num_sms()) return 1;
+  const OmpPlan p = omp_plan<V, HAD>(op, T, 2);
+  return p.bufg || p.total > (size_t)smem_optin() - 2048 ? 1 : 2;
+}
+
 template <class V, bool HAD>
 cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
+  if constexpr (!HAD && sizeof(V) >= 8) {
+    if (omp_ctas_v<V, HAD>(*a.op, a.batch, a.max_iter) == 2) return launch_omp_t<V, HAD, 8, 256, 2>(a, st);
+  }
   // lanes own RPT outputs; pick RPT so that one tile per warp covers n
   constexpr int NW = OMP_THREADS / 32;
-  if (a.op->n >= 32 * 8 * NW && OMP_THREADS <= 512) return launch_omp_t<V, HAD, 8>(a, st);
-  if (a.op->n >= 32 * 4 * NW) return launch_omp_t<V, HAD, 4>(a, st);
-  return launch_omp_t<V, HAD, 2>(a, st);
+  if (a.op->n >= 32 * 8 * NW && OMP_THREADS <= 512) return launch_omp_t<V, HAD, 8, OMP_THREADS, 1>(a, st);
+  if (a.op->n >= 32 * 4 * NW) return launch_omp_t<V, HAD, 4, OMP_THREADS, 1>(a, st);
+  return launch_omp_t<V, HAD, 2, OMP_THREADS, 1>(a, st);
 }
 
 }  // namespace

@@ -361,6 +361,37 @@ def test_omp_config2_shape(fmp, oracle, mode):
         assert sorted(res.support[b, :s]) == list(np.flatnonzero(X[b]) + 1)
 
 
+@pytest.mark.parametrize("mode,dtype", [("gpu", np.complex128), ("fast", np.complex128),
+                                        ("conventional", np.complex128), ("gpu", np.complex64)])
+def test_omp_two_ctas_per_sm_batch(fmp, oracle, mode, dtype):
+    """Batches of at least two problems per SM run the two-CTA-per-SM solver
+    (256 threads each, kernel table through L1): every problem of a 320-signal
+    batch against the oracle, and the same supports as the one-CTA solver."""
+    n, m, k, B = 2048, 512, 24, 320
+    om = oracle.make_row_selection(n, m, oracle.derive_seed(7, 1 << 40))
+    op = fmp.SensingOperator("fourier", n, om)
+    Y, X, _ = fmp.make_batch("fourier", n, om, k, B, base_seed=7, want_x=True)
+    tol = 1e-9 * np.linalg.norm(Y, axis=1)
+    Yd = Y.astype(dtype)
+    res = fmp.omp_solve_batch(op, Yd, fmp.SolveConfig(k, 0.0, mode), tolerances=tol)
+    os.environ["FMP_OMP_CTAS"] = "1"
+    try:
+        one = fmp.omp_solve_batch(op, Yd, fmp.SolveConfig(k, 0.0, mode), tolerances=tol)
+    finally:
+        del os.environ["FMP_OMP_CTAS"]
+    assert np.array_equal(res.support, one.support)
+    assert np.array_equal(res.iterations, one.iterations)
+    omode = "fast" if mode == "gpu" else mode
+    Yo = Yd.astype(np.complex128)
+    for b in range(B):
+        s = int(res.support_size[b])
+        assert sorted(res.support[b, :s]) == list(np.flatnonzero(X[b]) + 1)
+        if dtype == np.complex128 and (mode != "gpu" or b % 8 == 0):
+            r = oracle.omp_solve("fourier", n, om, Yo[b], k, tol[b], omode)
+            assert list(res.support[b, :s]) == list(r.support)
+            assert rel(res.coeffs[b, :s], r.coeffs) < 1e-10
+
+
 @pytest.mark.parametrize("dtype,tol", [(np.complex64, 1e-4), (np.complex128, 1e-10)])
 def test_omp_config4_shape(fmp, oracle, dtype, tol):
     # config 4 shape (reduced batch): Fourier N=16384, M=4096, K=128, c64 and c128,
