@@ -128,7 +128,6 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   unsigned char* p = sm + a.off_small;
   double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   double2* s_z = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
-  double2* s_a = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   double2* s_l = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)T + 15) / 16) * 16;
   unsigned* s_lam = reinterpret_cast<unsigned*>(p); p += ((4 * (size_t)T + 15) / 16) * 16;
@@ -530,12 +529,17 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
   const size_t r = al((size_t)m * sizeof(V));
   const size_t w = al((size_t)T * (T + 1) / 2 * 16);
   p.tw_a = (op.log2n + 1) / 2;
-  const size_t tw = HAD ? 0 : al(2 * (((size_t)1 << p.tw_a) + ((size_t)n >> p.tw_a)) + 4) * sizeof(V);
-  const size_t small = al(4 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
+  // two-level twiddle tables, each padded i + i/8 (TwTwoLevel)
+  const size_t lo_n = ((size_t)1 << p.tw_a) + ((size_t)1 << p.tw_a) / 8 + 1;
+  const size_t hi_n = ((size_t)n >> p.tw_a) + ((size_t)n >> p.tw_a) / 8 + 1;
+  const size_t tw = HAD ? 0 : al((lo_n + hi_n) * sizeof(V));
+  const size_t small = al(3 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
                        al(4 * (size_t)((n + 31) / 32));
-  // ctas > 1: the SM's shared memory (optin + 1 KB) split between the CTAs
+  // ctas > 1: the SM's shared memory (optin + 1 KB) split between the CTAs,
+  // less each CTA's 1 KB reservation and the kernel's static shared memory
+  // (1936 bytes; omp_ctas_v confirms the residency with the occupancy API)
   const size_t cap = ctas == 1 ? (size_t)smem_optin() - 2048
-                               : ((size_t)smem_optin() + 1024) / ctas - 1024 - 2048;
+                               : ((size_t)smem_optin() + 1024) / ctas - 1024 - 1952;
   size_t tot = tw + small;
   // the transform buffer has first claim on smem (a global-memory buffer
   // sends every transform pass through L2); the kernel table follows and
@@ -647,7 +651,13 @@ int omp_ctas_v(const DevOp& op, int64_t batch, int64_t T) {
   if (HAD || sizeof(V) < 8 || op.n < 32 * 8 * 8) return 1;
   if (batch < 2 * (int64_t)num_sms()) return 1;
   const OmpPlan p = omp_plan<V, HAD>(op, T, 2);
-  return p.bufg || p.total > (size_t)smem_optin() - 2048 ? 1 : 2;
+  if (p.bufg) return 1;
+  // the plan must really leave two CTAs resident
+  int occ = 0;
+  auto f = p.gmode == 2 ? k_omp<V, HAD, 8, 2, false, 256, 2> : k_omp<V, HAD, 8, 0, false, 256, 2>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.total);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 256, p.total);
+  return occ >= 2 ? 2 : 1;
 }
 
 template <class V, bool HAD>
