@@ -334,7 +334,17 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
 #pragma unroll
           for (int r = RPT - 1; r >= 0; --r)
             if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
-        } else {  // (tile ownership differs from this scan's indices: no skip here)
+        } else if (ntiles) {
+          // several tiles per warp: only a thread whose own maximum reaches
+          // the band re-reads its own entries, in ascending index order
+          if (my_best >= cut)
+            for (int tile = warp; tile < ntiles && first == 0xffffffffu; tile += nw)
+#pragma unroll
+              for (int r = 0; r < RPT; ++r) {
+                const int i = tile * 32 * RPT + lane + 32 * r;
+                if (msc[i] >= cut) { first = (unsigned)i; break; }
+              }
+        } else {
           for (int k = tid; k < n; k += nth)
             if (msc[k] >= cut) { first = (unsigned)k; break; }
         }
