@@ -257,8 +257,9 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           } else {
             for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
             __syncthreads();
-            for (int j = tid; j < m; j += nth)
-              buf[padx<OLOGP>(HAD ? (int)op.omega[j] : (int)brev_n(op.omega[j], log2n))] = r[j];
+            // rows in transform-slot order (op.scat_pos ascending): the lanes'
+            // stores land on increasing slots instead of bit-reversed ones
+            for (int k = tid; k < m; k += nth) buf[padx<OLOGP>((int)op.scat_pos[k])] = r[op.scat_row[k]];
             __syncthreads();
             block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
           }
