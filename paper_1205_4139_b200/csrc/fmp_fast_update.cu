@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
           acc.load(reinterpret_cast<const T*>(src) + i0 + 4 * lane);
           fast_tile_quad<T, QR>(acc, i0, lane, gH, s_lam, reinterpret_cast<const T*>(s_xn), cn);
           if (ob) acc.store(reinterpret_cast<T*>(ob) + i0 + 4 * lane);
-          if (last) {
+          if (last && amax) {
 #pragma unroll
             for (int r = 0; r < QR; ++r)
 #pragma unroll
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
           for (int r = 0; r < RPT; ++r) {
             const int i = i0 + lane + 32 * r;
             if (ob) ob[i] = acc[r];
-            if (last) {
+            if (last && amax) {
               const double mm = mag2(acc[r]);
               msc[i] = mm;
               best = fmax(best, mm);
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
           V acc = src[i];
           fast_point<V, HAD>(acc, i, n, gF, gH, s_lam, s_xn, cn);
           if (ob) ob[i] = acc;
-          if (last) {
+          if (last && amax) {
             const double mm = mag2(acc);
             msc[i] = mm;
             best = fmax(best, mm);

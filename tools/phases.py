@@ -1,6 +1,7 @@
 """Per-phase cycle breakdown of the fused OMP solver (profiling aid).
 
-usage: python tools/phases.py [batch] [--n N --m M --k K --iters T --dtype c128|c64 --modes fast,custom:32]
+usage: python tools/phases.py [batch] [--kind fourier|hadamard --n N --m M --k K --iters T
+                                        --dtype c128|c64|f64 --modes fast,custom:32]
 (defaults: config 2, batch 1184, modes fast / conventional / custom:32)"""
 import argparse
 import os
@@ -19,17 +20,19 @@ def main():
     p.add_argument("--k", type=int, default=64)
     p.add_argument("--iters", type=int, default=0)
     p.add_argument("--dtype", default="c128")
+    p.add_argument("--kind", default="fourier")
     p.add_argument("--modes", default="fast,conventional,custom:32")
     a = p.parse_args()
     import paper_1205_4139_b200 as fmp
     n, m, k, B = a.n, a.m, a.k, a.batch
     T = a.iters or k
     rows = fmp.make_row_selection(n, m, fmp.derive_seed(2, 1 << 40))
-    Y, _, _ = fmp.make_batch("fourier", n, rows, k, B, base_seed=2)
-    Y = Y.astype(np.complex64 if a.dtype == "c64" else np.complex128)
+    Y, _, _ = fmp.make_batch(a.kind, n, rows, k, B, base_seed=2, real=a.dtype == "f64")
+    Y = Y.astype({"c64": np.complex64, "c128": np.complex128, "f64": np.float64}[a.dtype]) \
+        if a.dtype != "f64" else Y.real.copy()
     ctx = fmp.Context(0)
-    op = fmp.SensingOperator("fourier", n, rows, ctx)
-    tol = 1e-9 * np.linalg.norm(Y.astype(np.complex128), axis=1) if a.dtype == "c128" else \
+    op = fmp.SensingOperator(a.kind, n, rows, ctx)
+    tol = 1e-9 * np.linalg.norm(Y.astype(np.complex128), axis=1) if a.dtype in ("c128", "f64") else \
         1e-5 * np.linalg.norm(Y.astype(np.complex128), axis=1)
     fmp.set_phase_profiling(True)
     for md in a.modes.split(","):
