@@ -305,6 +305,9 @@ __global__ void __launch_bounds__(256, 3) k_transform_queue(DevOp op, const V* _
         const int k0 = (int)op.scat_off[lo_slot >> 8], k1 = (int)op.scat_off[(lo_slot + B) >> 8];
         __syncthreads();
         const V* rr = in + b * m;
+        // unrolled: the slot / row loads and the gathers of several rows are
+        // in flight together (L2 latency, not bandwidth, bounds this loop)
+#pragma unroll 4
         for (int k = k0 + tid; k < k1; k += nth)
           buf[padx<LOGP>((int)op.scat_pos[k] - lo_slot)] = rr[op.scat_row[k]];
       } else {
@@ -329,6 +332,9 @@ __global__ void __launch_bounds__(256, 3) k_transform_queue(DevOp op, const V* _
       }
       __syncthreads();
       const int o0 = c * (B / K);
+      // two offsets in flight per thread where the registers allow it
+      constexpr int UB = sizeof(V) * K <= 64 ? 2 : 1;
+#pragma unroll UB
       for (int o = o0 + tid; o < o0 + B / K; o += nth) {
         V v[K];
 #pragma unroll
@@ -455,7 +461,8 @@ int cluster_k(int64_t n, int dtype) {
 // for 4-byte elements (measured on config 3)
 template <class V>
 int queue_k(int64_t n, int dtype) {
-  const int64_t target = sizeof(V) <= 4 ? 32 * 1024 : 64 * 1024;
+  int64_t target = sizeof(V) <= 4 ? 32 * 1024 : 64 * 1024;
+  if (const char* e = getenv("FMP_QUEUE_KB")) target = (int64_t)atoi(e) * 1024;  // tuning
   int64_t k = 2;
   while (k <= 16 && (n / k) * (int64_t)sizeof(V) > target) k *= 2;
   if (k > 16 || n / k > transform_max_n(dtype)) return 0;
