@@ -174,8 +174,11 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
     const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
     // real Hadamard with a staged lattice: quad-lane tiles of 128 RPT/4 outputs
     constexpr bool QUAD = HAD && GSM && (sizeof(V) == 4 || sizeof(V) == 8) && RPT >= 4;
-    constexpr int QR = 8;  // 1024 outputs per warp tile, 32 per lane
+    // 8 (f64) or 16 (f32) groups of 128 outputs per warp tile: the per-atom
+    // work (atom fetch, address bases, the lq branch) spread over more MACs
+    constexpr int QR = sizeof(typename scal<V>::T) == 4 ? 16 : 8;
     const int qtiles = n / (128 * QR);
+    const bool quad = QUAD && qtiles >= nw;  // every warp owns a tile
     for (int c0 = 0; c0 < t || c0 == 0; c0 += chunk) {
       const int cn = min(chunk, t - c0);
       __syncthreads();
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(FU_THREADS) k_fast_update(
       __syncthreads();
       const bool first = c0 == 0, last = c0 + chunk >= t;
       const V* src = first ? hb : ob;  // later chunks continue from the partial h
-      if constexpr (QUAD) {
+      if (quad) {
         using T = typename scal<V>::T;
         for (int tile = warp; tile < qtiles; tile += nw) {
           const int i0 = tile * 128 * QR;
