@@ -265,6 +265,28 @@ uint64_t fmp_derive_seed(uint64_t base, uint64_t index);
 int fmp_draw_instance(uint64_t n, uint64_t m, uint64_t k, double noise_stddev, uint64_t seed,
                       double* x_out, double* noise_out);
 
+/* GPU-side generation of the same batch: fmp_make_batch's
+ * draws computed on the device of `op` (Omega = op's rows) and bit-identical
+ * to it: the mt19937_64 stream, the Fisher-Yates support, the Gaussians and
+ * y in the host's summation order.  log / cos / sin are evaluated in
+ * double-double arithmetic and rounded; values whose exact result lies
+ * within 0.025 ulp of a rounding midpoint (where glibc may round the other
+ * way, its measured error reaching 0.515 ulp) are recomputed on the host with
+ * glibc -- *fixups_out (optional) counts them.  Device buffers: y_out
+ * batch x m complex128 (interleaved), x_out batch x n complex128 or NULL,
+ * noise_norm_out batch doubles or NULL.  Synchronises `stream` (NULL = the
+ * context's) once, for the host recomputation.  Replaces, for the harness,
+ * make_instance (sensing.cpp:119-153) with Rng (random.cpp:34-67). */
+int fmp_make_batch_dev(fmp_op op, uint64_t k, double noise_stddev, int real, uint64_t base_seed,
+                       uint64_t first, uint64_t batch, double* y_out, double* x_out,
+                       double* noise_norm_out, uint64_t* fixups_out, void* stream);
+/* the device generator's double-double log (fn 0) / cos (1) / sin (2) run on
+ * the host (tests): out = the correctly rounded value, frac (optional) = the
+ * exact result's distance from it towards its neighbour, in ulps (0..0.5) */
+int fmp_dd_eval(int fn, const double* x, uint64_t count, double* out, double* frac);
+/* the same on the device (device buffers; frac required), on `stream` */
+int fmp_dd_eval_dev(int fn, const double* x, uint64_t count, double* out, double* frac, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -130,6 +130,10 @@ _sig("fmp_make_row_selection", C.c_int, _u64, _u64, _u64, _vp)
 _sig("fmp_make_batch", C.c_int, C.c_int, _u64, _vp, _u64, _u64, C.c_double, C.c_int, _u64, _u64,
      _u64, C.c_int, _vp, _vp, _vp)
 _sig("fmp_derive_seed", _u64, _u64, _u64)
+_sig("fmp_make_batch_dev", C.c_int, _vp, _u64, C.c_double, C.c_int, _u64, _u64, _u64, _vp, _vp, _vp,
+     C.POINTER(_u64), _vp)
+_sig("fmp_dd_eval", C.c_int, C.c_int, _vp, _u64, _vp, _vp)
+_sig("fmp_dd_eval_dev", C.c_int, C.c_int, _vp, _u64, _vp, _vp, _vp)
 
 
 # ---------------------------------------------------------------- errors
@@ -562,6 +566,49 @@ def make_batch(kind, n: int, rows, k: int, batch: int, base_seed: int, first: in
     return Y, X, nn
 
 
+def make_batch_dev(op: "SensingOperator", k: int, batch: int, base_seed: int, first: int = 0,
+                   noise_stddev: float = 0.0, real: bool = False, want_x: bool = False,
+                   stream=None):
+    """make_batch generated on the operator's GPU (fmp.h fmp_make_batch_dev):
+    bit-identical to make_batch for the operator's rows.
+
+    Returns (Y (batch, m) complex128, X or None, noise_norms, fixups) as torch
+    device tensors (fixups: values recomputed on the host with glibc)."""
+    import torch
+    dev = torch.device("cuda", op.ctx.device)
+    Y = torch.empty((batch, op.m), dtype=torch.complex128, device=dev)
+    X = torch.empty((batch, op.n), dtype=torch.complex128, device=dev) if want_x else None
+    nn = torch.empty(batch, dtype=torch.float64, device=dev)
+    fix = _u64(0)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    _check(_lib.fmp_make_batch_dev(op.handle, k, noise_stddev, int(real), base_seed, first, batch,
+                                   Y.data_ptr(), X.data_ptr() if want_x else None, nn.data_ptr(),
+                                   C.byref(fix), C.c_void_p(st)))
+    return Y, X, nn, int(fix.value)
+
+
+def dd_eval(fn: str, x, device: bool = False) -> tuple:
+    """The device generator's double-double log / cos / sin (fmp.h
+    fmp_dd_eval[_dev]): (correctly rounded values, ulp position), evaluated
+    on the host or, with device=True, by a kernel on cuda:0."""
+    x = np.ascontiguousarray(np.asarray(x, np.float64))
+    code = {"log": 0, "cos": 1, "sin": 2}[fn]
+    if device:
+        import torch
+        xd = torch.from_numpy(x).cuda()
+        out = torch.empty_like(xd)
+        frac = torch.empty_like(xd)
+        st = torch.cuda.current_stream().cuda_stream
+        _check(_lib.fmp_dd_eval_dev(code, xd.data_ptr(), x.size, out.data_ptr(), frac.data_ptr(),
+                                    C.c_void_p(st)))
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), frac.cpu().numpy()
+    out = np.empty_like(x)
+    frac = np.empty_like(x)
+    _check(_lib.fmp_dd_eval(code, _ptr(x), x.size, _ptr(out), _ptr(frac)))
+    return out, frac
+
+
 def least_squares(op: SensingOperator, support, y, dtype=None) -> np.ndarray:
     """least_squares (solvers.hpp:82-85), normal-equations form, on the GPU.
     Raises RankDeficientError(position) for dependent columns."""
@@ -881,7 +928,7 @@ def apply_adjoint_dev(op: SensingOperator, r, h_out=None, argmax_out=None,
 __all__ = [
     "Context", "SensingOperator", "CorrelationKernel", "compute_kernel", "fast_update",
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
-    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "gpu_crossover_for", "make_row_selection", "make_batch", "derive_seed",
+    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "gpu_crossover_for", "make_row_selection", "make_batch", "make_batch_dev", "dd_eval", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
     "least_squares", "IncrementalQR", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
     "LargeShard", "LocalExchange", "sharded_solve", "large_solve",

@@ -28,7 +28,7 @@ CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), *DEFS]
-SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_cosamp.cu", "fmp_large.cu", "fmp_fast_update.cu", "fmp_qr.cu", "fmp_transform.cu", "fmp_transform_4s.cu", "fmp_transform_fold.cu", "fmp_capi.cu", "fmp_host_gen.cpp"]
+SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_cosamp.cu", "fmp_large.cu", "fmp_fast_update.cu", "fmp_qr.cu", "fmp_transform.cu", "fmp_transform_4s.cu", "fmp_transform_fold.cu", "fmp_capi.cu", "fmp_gen.cu", "fmp_host_gen.cpp"]
 HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh"]
 
 

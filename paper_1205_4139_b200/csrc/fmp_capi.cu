@@ -1746,3 +1746,33 @@ int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* c
 }
 
 }  // extern "C"
+
+int fmp_make_batch_dev(fmp_op op, uint64_t k, double noise_stddev, int real, uint64_t base_seed,
+                       uint64_t first, uint64_t batch, double* y_out, double* x_out,
+                       double* noise_norm_out, uint64_t* fixups_out, void* stream) {
+  if (!op || !y_out) return fail(FMP_EINVAL, "null argument");
+  // make_instance's checks (sensing.cpp:121-124)
+  if (k >= (uint64_t)op->d.m) return fail(FMP_EINVAL, "sparsity k must be below the row count m");
+  if (!(noise_stddev >= 0.0)) return fail(FMP_EINVAL, "noise stddev must be non-negative");
+  if (real && op->d.kind != FMP_HADAMARD) return fail(FMP_EINVAL, "real nonzeros need a Hadamard operator");
+  if (batch == 0) return FMP_OK;
+  CU(cudaSetDevice(op->ctx->device));
+  std::lock_guard<std::mutex> lk(op->ctx->mu);
+  CU(fmp::gen_batch(op->d, (int64_t)k, noise_stddev, real, base_seed, first, (int64_t)batch, y_out,
+                    x_out, noise_norm_out, fixups_out, pick_stream(op->ctx, stream)));
+  return FMP_OK;
+}
+
+int fmp_dd_eval(int fn, const double* x, uint64_t count, double* out, double* frac) {
+  if (fn < 0 || fn > 2) return fail(FMP_EINVAL, "unknown function %d", fn);
+  if (count && (!x || !out)) return fail(FMP_EINVAL, "null argument");
+  fmp::dd_eval_host(fn, x, (int64_t)count, out, frac);
+  return FMP_OK;
+}
+
+int fmp_dd_eval_dev(int fn, const double* x, uint64_t count, double* out, double* frac, void* stream) {
+  if (fn < 0 || fn > 2) return fail(FMP_EINVAL, "unknown function %d", fn);
+  if (count && (!x || !out || !frac)) return fail(FMP_EINVAL, "null argument");
+  CU(fmp::dd_eval_dev(fn, x, (int64_t)count, out, frac, (cudaStream_t)stream));
+  return FMP_OK;
+}

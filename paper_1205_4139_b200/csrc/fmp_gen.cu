@@ -1,0 +1,604 @@
+// GPU-side instance generation: the seeded draws of
+// fmp_make_batch (fmp_host_gen.cpp) on the device, bit-identical to it.
+//
+// Reference recipe: make_instance (sensing.cpp:119-153) with Rng
+// (random.hpp:32-54, random.cpp:34-67): std::mt19937_64 seeded with
+// derive_seed(base, first + b); sample_one_based = partial Fisher-Yates over
+// 1..n then sort (random.cpp:56-67); next_complex_gaussian = sqrt(-log u1) *
+// (cos, sin)(2 pi u2) (random.cpp:46-54); noise scaled by sigma sqrt(2)
+// (sensing.cpp:143-147); y = Phi x + noise, synthesised from the K nonzeros
+// in fmp_make_batch's summation order.
+//
+// Pipeline (one stream):
+//   k_draws   one thread per signal: the engine (state in local memory), the
+//             support (Fisher-Yates through a per-signal open-addressing swap
+//             table, then an insertion sort) and the raw uniform pairs;
+//   k_trans   one thread per Gaussian (and per twiddle): log, cos, sin in
+//             double-double arithmetic, correctly rounded.  glibc's log / cos
+//             / sin are not always correctly rounded (measured max error
+//             0.515 ulp); a value whose exact result lies within kBand ulp of
+//             a rounding midpoint is listed, and the host recomputes exactly
+//             those with glibc (the only host work; typically ~5 % of the
+//             values).  Every other value equals glibc's by construction.
+//   k_compose radius, products, real / noise scaling;
+//   k_synth   one thread per measurement row: y_i = sum_j x_j u(row_i, s_j) +
+//             noise_i in the host's order (no FMA contraction: __d*_rn);
+//   k_dense   optional dense x and the per-signal noise norms.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "fmp.h"
+#include "fmp_kernels.cuh"
+
+namespace fmp {
+extern thread_local int g_launches;
+
+namespace {
+
+// ------------------------------------------------------------ double-double
+// hi + lo with |lo| <= ulp(hi) / 2.  Device: explicit _rn intrinsics so
+// nvcc never contracts; host (g++, x86-64 baseline, no FMA units targeted):
+// plain operations, std::fma for the exact product error.
+#ifdef __CUDA_ARCH__
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+#define DFMA(a, b, c) __fma_rn((a), (b), (c))
+#else
+#define DADD(a, b) ((a) + (b))
+#define DSUB(a, b) ((a) - (b))
+#define DMUL(a, b) ((a) * (b))
+#define DDIV(a, b) ((a) / (b))
+#define DFMA(a, b, c) std::fma((a), (b), (c))
+#endif
+
+struct dd {
+  double hi, lo;
+};
+
+__host__ __device__ inline dd two_sum(double a, double b) {
+  const double s = DADD(a, b), bb = DSUB(s, a);
+  return {s, DADD(DSUB(a, DSUB(s, bb)), DSUB(b, bb))};
+}
+__host__ __device__ inline dd quick_two_sum(double a, double b) {
+  const double s = DADD(a, b);
+  return {s, DSUB(b, DSUB(s, a))};
+}
+__host__ __device__ inline dd two_prod(double a, double b) {
+  const double p = DMUL(a, b);
+  return {p, DFMA(a, b, -p)};
+}
+__host__ __device__ inline dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  const dd t = two_sum(a.lo, b.lo);
+  s.lo = DADD(s.lo, t.hi);
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo = DADD(s.lo, t.lo);
+  return quick_two_sum(s.hi, s.lo);
+}
+__host__ __device__ inline dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+__host__ __device__ inline dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo = DADD(p.lo, DADD(DMUL(a.hi, b.lo), DMUL(a.lo, b.hi)));
+  return quick_two_sum(p.hi, p.lo);
+}
+__host__ __device__ inline dd dd_div(dd a, dd b) {
+  const double q1 = DDIV(a.hi, b.hi);
+  dd r = dd_add(a, dd_neg(dd_mul({q1, 0.0}, b)));
+  const double q2 = DDIV(r.hi, b.hi);
+  r = dd_add(r, dd_neg(dd_mul({q2, 0.0}, b)));
+  const double q3 = DDIV(r.hi, b.hi);
+  return dd_add(quick_two_sum(q1, q2), {q3, 0.0});
+}
+
+// constants: tools/gen_dd_consts.py
+__host__ __device__ inline dd inv_odd(int k) {  // 1 / (2k + 1), k < 24
+  constexpr double t[24][2] = {
+      {0x1.0000000000000p+0, 0x0.0p+0}, {0x1.5555555555555p-2, 0x1.5555555555555p-56},
+      {0x1.999999999999ap-3, -0x1.999999999999ap-57}, {0x1.2492492492492p-3, 0x1.2492492492492p-57},
+      {0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-58}, {0x1.745d1745d1746p-4, -0x1.745d1745d1746p-59},
+      {0x1.3b13b13b13b14p-4, -0x1.3b13b13b13b14p-58}, {0x1.1111111111111p-4, 0x1.1111111111111p-60},
+      {0x1.e1e1e1e1e1e1ep-5, 0x1.e1e1e1e1e1e1ep-61}, {0x1.af286bca1af28p-5, 0x1.af286bca1af28p-59},
+      {0x1.8618618618618p-5, 0x1.8618618618618p-59}, {0x1.642c8590b2164p-5, 0x1.642c8590b2164p-60},
+      {0x1.47ae147ae147bp-5, -0x1.eb851eb851eb8p-61}, {0x1.2f684bda12f68p-5, 0x1.2f684bda12f68p-59},
+      {0x1.1a7b9611a7b96p-5, 0x1.1a7b9611a7b96p-61}, {0x1.0842108421084p-5, 0x1.0842108421084p-60},
+      {0x1.f07c1f07c1f08p-6, -0x1.f07c1f07c1f08p-61}, {0x1.d41d41d41d41dp-6, 0x1.0750750750750p-60},
+      {0x1.bacf914c1bad0p-6, -0x1.bacf914c1bad0p-60}, {0x1.a41a41a41a41ap-6, 0x1.0690690690690p-60},
+      {0x1.8f9c18f9c18fap-6, -0x1.f3831f3831f38p-61}, {0x1.7d05f417d05f4p-6, 0x1.7d05f417d05f4p-62},
+      {0x1.6c16c16c16c17p-6, -0x1.f49f49f49f49fp-61}, {0x1.5c9882b931057p-6, 0x1.310572620ae4cp-61}};
+  return {t[k][0], t[k][1]};
+}
+__host__ __device__ inline dd inv_fact(int k) {  // 1 / k!, k < 32
+  constexpr double t[32][2] = {
+      {0x1.0000000000000p+0, 0x0.0p+0}, {0x1.0000000000000p+0, 0x0.0p+0},
+      {0x1.0000000000000p-1, 0x0.0p+0}, {0x1.5555555555555p-3, 0x1.5555555555555p-57},
+      {0x1.5555555555555p-5, 0x1.5555555555555p-59}, {0x1.1111111111111p-7, 0x1.1111111111111p-63},
+      {0x1.6c16c16c16c17p-10, -0x1.f49f49f49f49fp-65}, {0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-73},
+      {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76}, {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73},
+      {0x1.27e4fb7789f5cp-22, 0x1.cbbc05b4fa99ap-76}, {0x1.ae64567f544e4p-26, -0x1.c062e06d1f209p-80},
+      {0x1.1eed8eff8d898p-29, -0x1.2aec959e14c06p-83}, {0x1.6124613a86d09p-33, 0x1.f28e0cc748ebep-87},
+      {0x1.93974a8c07c9dp-37, 0x1.05d6f8a2efd1fp-92}, {0x1.ae7f3e733b81fp-41, 0x1.1d8656b0ee8cbp-97},
+      {0x1.ae7f3e733b81fp-45, 0x1.1d8656b0ee8cbp-101}, {0x1.952c77030ad4ap-49, 0x1.ac981465ddc6cp-103},
+      {0x1.6827863b97d97p-53, 0x1.eec01221a8b0bp-107}, {0x1.2f49b46814157p-57, 0x1.2650f61dbdcb4p-112},
+      {0x1.e542ba4020225p-62, 0x1.ea72b4afe3c2fp-120}, {0x1.71b8ef6dcf572p-66, -0x1.d043ae40c4647p-120},
+      {0x1.0ce396db7f853p-70, -0x1.aebcdbd20331cp-124}, {0x1.761b41316381ap-75, -0x1.3423c7d91404fp-130},
+      {0x1.f2cf01972f578p-80, -0x1.9ada5fcc1ab14p-135}, {0x1.3f3ccdd165fa9p-84, -0x1.58ddadf344487p-139},
+      {0x1.88e85fc6a4e5ap-89, -0x1.71c37ebd16540p-143}, {0x1.d1ab1c2dccea3p-94, 0x1.054d0c78aea14p-149},
+      {0x1.0a18a2635085dp-98, 0x1.b9e2e28e1aa54p-153}, {0x1.259f98b4358adp-103, 0x1.eaf8c39dd9bc5p-157},
+      {0x1.3932c5047d60ep-108, 0x1.832b7b530a627p-162}, {0x1.434d2e783f5bcp-113, 0x1.0b87b91be9affp-167}};
+  return {t[k][0], t[k][1]};
+}
+
+// natural log of a positive normal double to ~2^-104 relative:
+// x = 2^e m, m in [sqrt(1/2), sqrt(2)); log m = 2 atanh(s), s = (m-1)/(m+1),
+// |s| <= 0.1716, series to s^47 (the next term is below 2^-118 |s|)
+__host__ __device__ inline dd dd_log(double x) {
+  int e = 0;
+  double m = frexp(x, &e);
+  if (m < 0.70710678118654752440) {
+    m = DMUL(m, 2.0);
+    --e;
+  }
+  const dd s = dd_div({DSUB(m, 1.0), 0.0}, two_sum(m, 1.0));  // m - 1 exact (Sterbenz)
+  const dd s2 = dd_mul(s, s);
+  dd p = inv_odd(23);
+  for (int k = 22; k >= 0; --k) p = dd_add(dd_mul(p, s2), inv_odd(k));
+  dd lm = dd_mul(s, p);
+  lm = {DMUL(lm.hi, 2.0), DMUL(lm.lo, 2.0)};
+  const double ed = (double)e;
+  dd el = two_prod(ed, 0x1.62e42fefa39efp-1);
+  el = dd_add(el, {DMUL(ed, 0x1.abc9e3b39803fp-56), 0.0});
+  return dd_add(el, lm);
+}
+
+// sin and cos of a double |a| < 8 to ~2^-100 absolute (relative near zeros):
+// a = k pi/2 + r, pi/2 in three parts (~160 bits), Taylor series of sin r and
+// cos r (|r| <= pi/4 + tiny) to r^31 / 31!
+__host__ __device__ inline void dd_sincos(double a, dd* sn, dd* cs) {
+  if (a == 0.0) {  // keeps the sign of zero, as glibc does
+    *sn = {a, 0.0};
+    *cs = {1.0, 0.0};
+    return;
+  }
+  const double k = rint(DMUL(a, 0x1.45f306dc9c883p-1));
+  dd r = dd_add({a, 0.0}, dd_neg(two_prod(k, 0x1.921fb54442d18p+0)));
+  r = dd_add(r, dd_neg(two_prod(k, 0x1.1a62633145c07p-54)));
+  r = dd_add(r, dd_neg(two_prod(k, -0x1.f1976b7ed8fbcp-110)));
+  const dd r2 = dd_mul(r, r);
+  dd ps = inv_fact(31), pc = inv_fact(30);
+  for (int j = 14; j >= 0; --j) {
+    ps = dd_add(dd_neg(dd_mul(ps, r2)), inv_fact(2 * j + 1));
+    pc = dd_add(dd_neg(dd_mul(pc, r2)), inv_fact(2 * j));
+  }
+  ps = dd_mul(ps, r);
+  switch (((long long)k) & 3) {
+    case 0: *sn = ps; *cs = pc; break;
+    case 1: *sn = pc; *cs = dd_neg(ps); break;
+    case 2: *sn = dd_neg(ps); *cs = dd_neg(pc); break;
+    default: *sn = dd_neg(pc); *cs = ps; break;
+  }
+}
+
+// the correctly rounded value hi and the position of the exact value between
+// hi and its neighbour towards lo, in units of that spacing (0 .. 0.5)
+__host__ __device__ inline double round_frac(dd v) {
+  if (v.lo == 0.0 || v.hi == 0.0) return 0.0;
+  // neighbour of hi towards lo: one step of the bit pattern, up in magnitude
+  // when lo has hi's sign
+  int64_t bits;
+#ifdef __CUDA_ARCH__
+  bits = __double_as_longlong(v.hi);
+#else
+  memcpy(&bits, &v.hi, 8);
+#endif
+  bits += ((v.lo > 0.0) == (v.hi > 0.0)) ? 1 : -1;
+  double nb;
+#ifdef __CUDA_ARCH__
+  nb = __longlong_as_double(bits);
+#else
+  memcpy(&nb, &bits, 8);
+#endif
+  return fabs(v.lo) / fabs(DSUB(nb, v.hi));
+}
+
+constexpr double kBand = 0.025;  // listed when within 0.025 ulp of a midpoint
+
+// ------------------------------------------------------------- mt19937_64
+struct Mt64 {
+  static constexpr int NN = 312, MM = 156;
+  uint64_t s[NN];
+  int i;
+  __device__ void seed(uint64_t v) {
+    s[0] = v;
+    for (int j = 1; j < NN; ++j) s[j] = 6364136223846793005ULL * (s[j - 1] ^ (s[j - 1] >> 62)) + (uint64_t)j;
+    i = NN;
+  }
+  __device__ uint64_t next() {
+    if (i >= NN) {
+      for (int j = 0; j < NN; ++j) {
+        const uint64_t x = (s[j] & 0xFFFFFFFF80000000ULL) | (s[(j + 1) % NN] & 0x7FFFFFFFULL);
+        s[j] = s[(j + MM) % NN] ^ (x >> 1) ^ ((x & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+      }
+      i = 0;
+    }
+    uint64_t y = s[i++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    return y ^ (y >> 43);
+  }
+  __device__ uint64_t below(uint64_t b) {  // random.cpp:34-44
+    const uint64_t limit = (UINT64_MAX / b) * b;
+    uint64_t r;
+    do r = next(); while (r >= limit);
+    return r % b;
+  }
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+struct GenArgs {
+  int kind;
+  int64_t n, m, k, batch, G;  // G Gaussians per signal (k, plus m when noisy)
+  int noisy, real;
+  uint64_t base, first;
+  int htab;                   // swap table entries per signal (power of two)
+  const uint32_t* omega;      // 0-based rows
+  uint32_t* sup;              // batch x k, 1-based, sorted
+  uint32_t* swap_key;         // batch x htab (0xffffffff = empty)
+  uint32_t* swap_val;
+  double* u1;                 // batch x G
+  double* ang;                // batch x G
+  double* val;                // 3 batch G (log, cos, sin) then 2 n (twiddle cos, sin)
+  unsigned long long* nfix;   // listed values
+  unsigned long long* fix_idx;  // (value index << 2) | function
+  double* fix_arg;
+  unsigned long long cap;
+  double isn, sc;
+  double2* xs;                // batch x k
+  double2* noise;             // batch x m
+  double2* tw;                // n (Fourier)
+  double2* y;                 // batch x m
+  double2* x;                 // batch x n, optional
+  double* nn;                 // batch, optional
+};
+
+__device__ __forceinline__ uint32_t swap_get(const uint32_t* key, const uint32_t* val, int h, uint32_t p) {
+  for (uint32_t q = (p * 2654435761u) & (h - 1);; q = (q + 1) & (h - 1)) {
+    if (key[q] == p) return val[q];
+    if (key[q] == 0xffffffffu) return p + 1;  // untouched pool slot holds p + 1
+  }
+}
+__device__ __forceinline__ void swap_set(uint32_t* key, uint32_t* val, int h, uint32_t p, uint32_t v) {
+  for (uint32_t q = (p * 2654435761u) & (h - 1);; q = (q + 1) & (h - 1)) {
+    if (key[q] == p || key[q] == 0xffffffffu) {
+      key[q] = p;
+      val[q] = v;
+      return;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(64) k_draws(GenArgs a) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= a.batch) return;
+  Mt64 rng;
+  rng.seed(mix64(mix64(a.base) ^ mix64(a.first + (uint64_t)b)));
+  uint32_t* key = a.swap_key + b * a.htab;
+  uint32_t* val = a.swap_val + b * a.htab;
+  uint32_t* sup = a.sup + b * a.k;
+  for (int64_t i = 0; i < a.k; ++i) {  // partial Fisher-Yates (random.cpp:56-67)
+    const uint32_t j = (uint32_t)(i + (int64_t)rng.below((uint64_t)(a.n - i)));
+    const uint32_t vi = swap_get(key, val, a.htab, (uint32_t)i), vj = swap_get(key, val, a.htab, j);
+    swap_set(key, val, a.htab, (uint32_t)i, vj);
+    swap_set(key, val, a.htab, j, vi);
+    sup[i] = vj;
+  }
+  for (int64_t i = 1; i < a.k; ++i) {  // std::sort of the sample
+    const uint32_t v = sup[i];
+    int64_t j = i - 1;
+    while (j >= 0 && sup[j] > v) {
+      sup[j + 1] = sup[j];
+      --j;
+    }
+    sup[j + 1] = v;
+  }
+  double* u1 = a.u1 + b * a.G;
+  double* an = a.ang + b * a.G;
+  for (int64_t g = 0; g < a.G; ++g) {  // random.cpp:46-54
+    u1[g] = __dmul_rn(__dadd_rn((double)(rng.next() >> 11), 1.0), 0x1.0p-53);
+    const double u2 = __dmul_rn((double)(rng.next() >> 11), 0x1.0p-53);
+    an[g] = __dmul_rn(2.0 * M_PI, u2);
+  }
+}
+
+__device__ __forceinline__ void put(const GenArgs& a, int64_t vi, int fn, double arg, dd v) {
+  a.val[vi] = v.hi;
+  if (round_frac(v) > 0.5 - kBand) {
+    const unsigned long long s = atomicAdd(a.nfix, 1ULL);
+    if (s < a.cap) {
+      a.fix_idx[s] = ((unsigned long long)vi << 2) | (unsigned)fn;
+      a.fix_arg[s] = arg;
+    }
+  }
+}
+
+// fn: 0 log, 1 cos, 2 sin
+__global__ void k_trans(GenArgs a) {
+  const int64_t total = a.batch * a.G;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < total) {
+    const double u = a.u1[t], an = a.ang[t];
+    put(a, 3 * t, 0, u, dd_log(u));
+    dd s, c;
+    dd_sincos(an, &s, &c);
+    put(a, 3 * t + 1, 1, an, c);
+    if (!a.real) put(a, 3 * t + 2, 2, an, s);
+    else a.val[3 * t + 2] = s.hi;  // unused by the real variant
+  } else if (a.kind == FOURIER && t < total + a.n) {
+    const int64_t e = t - total;  // fmp_host_gen.cpp twiddles
+    const double th = __ddiv_rn(__dmul_rn(-6.283185307179586476925286766559, (double)e), (double)a.n);
+    dd s, c;
+    dd_sincos(th, &s, &c);
+    put(a, 3 * total + 2 * e, 1, th, c);
+    put(a, 3 * total + 2 * e + 1, 2, th, s);
+  }
+}
+
+__global__ void k_fixup(double* val, const unsigned long long* idx, const double* v, int64_t cnt) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < cnt) val[idx[t] >> 2] = v[t];
+}
+
+__global__ void k_compose(GenArgs a) {
+  const int64_t total = a.batch * a.G;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < total) {
+    const int64_t b = t / a.G, g = t - b * a.G;
+    const double radius = __dsqrt_rn(-a.val[3 * t]);
+    const double zr = __dmul_rn(radius, a.val[3 * t + 1]), zi = __dmul_rn(radius, a.val[3 * t + 2]);
+    if (g < a.k) {
+      a.xs[b * a.k + g] = a.real ? make_double2(__dmul_rn(1.4142135623730951, zr), 0.0)
+                                 : make_double2(zr, zi);
+    } else {
+      a.noise[b * a.m + (g - a.k)] = make_double2(__dmul_rn(zr, a.sc), __dmul_rn(zi, a.sc));
+    }
+  } else if (a.kind == FOURIER && t < total + a.n) {
+    const int64_t e = t - total;
+    a.tw[e] = make_double2(__dmul_rn(a.isn, a.val[3 * total + 2 * e]),
+                           __dmul_rn(a.isn, a.val[3 * total + 2 * e + 1]));
+  }
+}
+
+// y row i of signal b in fmp_make_batch's order: acc += x_j * u(a, c_j), then
+// + noise_i (always added, as the host adds its zero noise)
+__global__ void k_synth(GenArgs a) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.batch * a.m) return;
+  const int64_t b = t / a.m, i = t - b * a.m;
+  const uint64_t row = a.omega[i];
+  const uint32_t* sup = a.sup + b * a.k;
+  const double2* xs = a.xs + b * a.k;
+  double ar = 0.0, ai = 0.0;
+  const uint64_t msk = (uint64_t)a.n - 1;
+  for (int64_t j = 0; j < a.k; ++j) {
+    const uint64_t c = sup[j] - 1;
+    const double2 x = xs[j];
+    if (a.kind == FOURIER) {
+      const double2 w = a.tw[(row * c) & msk];
+      const double pr = __dsub_rn(__dmul_rn(x.x, w.x), __dmul_rn(x.y, w.y));
+      const double pi = __dadd_rn(__dmul_rn(x.x, w.y), __dmul_rn(x.y, w.x));
+      ar = __dadd_rn(ar, pr);
+      ai = __dadd_rn(ai, pi);
+    } else {
+      const double s = (__popcll(row & c) & 1) ? -a.isn : a.isn;
+      ar = __dadd_rn(ar, __dmul_rn(x.x, s));
+      ai = __dadd_rn(ai, __dmul_rn(x.y, s));
+    }
+  }
+  double2 nz = make_double2(0.0, 0.0);
+  if (a.noisy) nz = a.noise[b * a.m + i];
+  a.y[t] = make_double2(__dadd_rn(ar, nz.x), __dadd_rn(ai, nz.y));
+}
+
+__global__ void k_scatter_x(GenArgs a) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.batch * a.k) return;
+  const int64_t b = t / a.k;
+  a.x[b * a.n + (a.sup[t] - 1)] = a.xs[t];
+}
+
+__global__ void k_noise_norm(GenArgs a) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= a.batch) return;
+  double s = 0.0;
+  if (a.noisy) {
+    const double2* nz = a.noise + b * a.m;
+    for (int64_t i = 0; i < a.m; ++i)
+      s = __dadd_rn(s, __dadd_rn(__dmul_rn(nz[i].x, nz[i].x), __dmul_rn(nz[i].y, nz[i].y)));
+  }
+  a.nn[b] = __dsqrt_rn(s);
+}
+
+unsigned grid_of(int64_t count, int th) { return (unsigned)((count + th - 1) / th); }
+
+__global__ void k_dd_eval(int fn, const double* x, int64_t cnt, double* out, double* frac) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  dd v;
+  if (fn == 0) {
+    v = dd_log(x[i]);
+  } else {
+    dd s, c;
+    dd_sincos(x[i], &s, &c);
+    v = fn == 1 ? c : s;
+  }
+  out[i] = v.hi;
+  frac[i] = round_frac(v);
+}
+
+}  // namespace
+
+// the same evaluation on the device (tests): x, out, frac device buffers
+cudaError_t dd_eval_dev(int fn, const double* x, int64_t cnt, double* out, double* frac, cudaStream_t st) {
+  if (cnt <= 0) return cudaSuccess;
+  k_dd_eval<<<grid_of(cnt, 128), 128, 0, st>>>(fn, x, cnt, out, frac);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// Host side of the pipeline (see the file comment).  Synchronises `st` once,
+// after k_trans, to recompute the listed values with glibc.
+cudaError_t gen_batch(const DevOp& op, int64_t k, double noise_stddev, int real, uint64_t base,
+                      uint64_t first, int64_t batch, double* y_out, double* x_out, double* nn_out,
+                      uint64_t* fixups, cudaStream_t st) {
+  GenArgs a{};
+  a.kind = op.kind;
+  a.n = op.n;
+  a.m = op.m;
+  a.k = k;
+  a.batch = batch;
+  a.noisy = (!real && noise_stddev > 0.0) ? 1 : 0;
+  a.real = real;
+  a.G = k + (a.noisy ? op.m : 0);
+  a.base = base;
+  a.first = first;
+  int h = 64;
+  while (h < 4 * k) h <<= 1;
+  a.htab = h;
+  a.omega = op.omega;
+  a.isn = 1.0 / std::sqrt((double)op.n);
+  a.sc = noise_stddev * std::sqrt(2.0);
+  const int64_t total = batch * a.G, ntw = op.kind == FOURIER ? op.n : 0;
+  const int64_t nval = 3 * total + 2 * ntw;
+  a.cap = (unsigned long long)nval;
+  // one scratch allocation, carved
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_sup = carve(batch * k * 4), o_key = carve(batch * (size_t)h * 4),
+               o_val = carve(batch * (size_t)h * 4), o_u1 = carve(total * 8), o_ang = carve(total * 8),
+               o_v = carve(nval * 8), o_nf = carve(8), o_fi = carve(nval * 8), o_fa = carve(nval * 8),
+               o_xs = carve(batch * k * 16), o_nz = carve(a.noisy ? batch * op.m * 16 : 16),
+               o_tw = carve(ntw * 16 + 16);
+  char* base_p = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&base_p, off, st);
+  if (e != cudaSuccess) return e;
+  a.sup = (uint32_t*)(base_p + o_sup);
+  a.swap_key = (uint32_t*)(base_p + o_key);
+  a.swap_val = (uint32_t*)(base_p + o_val);
+  a.u1 = (double*)(base_p + o_u1);
+  a.ang = (double*)(base_p + o_ang);
+  a.val = (double*)(base_p + o_v);
+  a.nfix = (unsigned long long*)(base_p + o_nf);
+  a.fix_idx = (unsigned long long*)(base_p + o_fi);
+  a.fix_arg = (double*)(base_p + o_fa);
+  a.xs = (double2*)(base_p + o_xs);
+  a.noise = (double2*)(base_p + o_nz);
+  a.tw = (double2*)(base_p + o_tw);
+  a.y = (double2*)y_out;
+  a.x = (double2*)x_out;
+  a.nn = nn_out;
+  std::vector<unsigned long long> idx;
+  std::vector<double> arg, fixed;
+  unsigned long long cnt = 0;
+  double* fixed_d = nullptr;
+  do {
+    if ((e = cudaMemsetAsync(a.swap_key, 0xff, batch * (size_t)h * 4, st)) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(a.nfix, 0, 8, st)) != cudaSuccess) break;
+    k_draws<<<grid_of(batch, 64), 64, 0, st>>>(a);
+    ++g_launches;
+    if (total + ntw > 0) {
+      k_trans<<<grid_of(total + ntw, 128), 128, 0, st>>>(a);
+      ++g_launches;
+    }
+    if ((e = cudaMemcpyAsync(&cnt, a.nfix, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+    if (cnt > a.cap) {
+      e = cudaErrorUnknown;
+      break;
+    }
+    if (fixups) *fixups = cnt;
+    if (cnt) {
+      idx.resize(cnt);
+      arg.resize(cnt);
+      fixed.resize(cnt);
+      if ((e = cudaMemcpyAsync(idx.data(), a.fix_idx, cnt * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(arg.data(), a.fix_arg, cnt * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+      auto work = [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; ++i) {
+          const int fn = (int)(idx[i] & 3);
+          fixed[i] = fn == 0 ? std::log(arg[i]) : fn == 1 ? std::cos(arg[i]) : std::sin(arg[i]);
+        }
+      };
+      const unsigned nt = cnt > 65536 ? std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1u;
+      std::vector<std::thread> pool;
+      const size_t chunk = (cnt + nt - 1) / nt;
+      for (unsigned t = 1; t < nt; ++t)
+        pool.emplace_back(work, std::min<size_t>(cnt, t * chunk), std::min<size_t>(cnt, (t + 1) * chunk));
+      work(0, std::min<size_t>(cnt, chunk));
+      for (auto& th : pool) th.join();
+      fixed_d = a.fix_arg;  // reuse the argument list for the corrected values
+      if ((e = cudaMemcpyAsync(fixed_d, fixed.data(), cnt * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+      k_fixup<<<grid_of(cnt, 256), 256, 0, st>>>(a.val, a.fix_idx, fixed_d, (int64_t)cnt);
+      ++g_launches;
+    }
+    if (total + ntw > 0) {
+      k_compose<<<grid_of(total + ntw, 256), 256, 0, st>>>(a);
+      ++g_launches;
+    }
+    k_synth<<<grid_of(batch * op.m, 128), 128, 0, st>>>(a);
+    ++g_launches;
+    if (x_out) {
+      if ((e = cudaMemsetAsync(x_out, 0, batch * op.n * 16, st)) != cudaSuccess) break;
+      if (k > 0) {
+        k_scatter_x<<<grid_of(batch * k, 256), 256, 0, st>>>(a);
+        ++g_launches;
+      }
+    }
+    if (nn_out) {
+      k_noise_norm<<<grid_of(batch, 64), 64, 0, st>>>(a);
+      ++g_launches;
+    }
+    e = cudaGetLastError();
+    // keep the host vectors alive until the copies that read them are done
+    if (e == cudaSuccess && cnt) e = cudaStreamSynchronize(st);
+  } while (0);
+  cudaFreeAsync(base_p, st);
+  return e;
+}
+
+// host evaluation of the double-double functions (tests): out = the correctly
+// rounded value, frac = position between it and its neighbour (ulps)
+void dd_eval_host(int fn, const double* x, int64_t cnt, double* out, double* frac) {
+  for (int64_t i = 0; i < cnt; ++i) {
+    dd v;
+    if (fn == 0) {
+      v = dd_log(x[i]);
+    } else {
+      dd s, c;
+      dd_sincos(x[i], &s, &c);
+      v = fn == 1 ? c : s;
+    }
+    out[i] = v.hi;
+    if (frac) frac[i] = round_frac(v);
+  }
+}
+
+}  // namespace fmp

@@ -219,4 +219,11 @@ cudaError_t launch_qr_store(double2* qnew, const double2* v, int64_t rows, doubl
 cudaError_t launch_qr_dots(const double2* Q, int64_t rows, int t, const double2* rhs, double2* part,
                            double2* z, double2* scratch, cudaStream_t st);
 
+// seeded instance generation on the device (fmp_gen.cu)
+cudaError_t gen_batch(const DevOp& op, int64_t k, double noise_stddev, int real, uint64_t base,
+                      uint64_t first, int64_t batch, double* y_out, double* x_out, double* nn_out,
+                      uint64_t* fixups, cudaStream_t st);
+void dd_eval_host(int fn, const double* x, int64_t cnt, double* out, double* frac);
+cudaError_t dd_eval_dev(int fn, const double* x, int64_t cnt, double* out, double* frac, cudaStream_t st);
+
 }  // namespace fmp
