@@ -736,7 +736,8 @@ static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg, int dtype, ui
 // on different streams, each with its own set)
 static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
                           const fmp_omp_config* cfg, const double* dtol, fmp_omp_result* out,
-                          cudaStream_t st, int wsset = 0) {
+                          cudaStream_t st, int wsset = 0, const int* ready = nullptr,
+                          int64_t ready_chunk = 0) {
   const int wo = wsset ? S_ALT : 0;  // slot offset of the alternate set
   fmp_ctx_s* ctx = op->ctx;
   const int64_t T = (int64_t)cfg->max_iterations;
@@ -760,6 +761,8 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   a.hlen = out->history_len;
   a.hist = cfg->record_correlations ? out->history : nullptr;
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
+  a.ready = ready;
+  a.ready_chunk = ready_chunk;
   double2* w;
   ALLOC(w, wo + S_W, (size_t)a.grid * (T * (T + 1) / 2) * 16);
   a.w_ws = w;
@@ -834,6 +837,67 @@ static int pinned_reserve(fmp_ctx_s* ctx, size_t bytes) {
   cudaError_t e = cudaHostAlloc(&ctx->pinned, bytes, cudaHostAllocDefault);
   if (e != cudaSuccess) return fail(FMP_ENOMEM, "page-locked staging (%zu bytes): %s", bytes, cudaGetErrorString(e));
   ctx->pinned_bytes = bytes;
+  return FMP_OK;
+}
+
+// Host buffers, one launch: the solver starts at once and each CTA waits
+// (acquire spin) for the chunk holding its next problem; the copy stream moves
+// the measurements in chunks of one problem per CTA, each followed by a 4-byte
+// copy that raises the chunk's flag.  Results go straight into the caller's
+// page-locked buffers (stores over the host link as problems finish), so
+// nothing is exposed but the first chunk's copy and the wave tail.  Used when
+// every result buffer is page-locked (else omp_host_chunked).
+static int omp_host_streamed(fmp_op op, int dtype, const void* y, uint64_t batch,
+                             const fmp_omp_config* cfg, fmp_omp_result* out, uint64_t per) {
+  fmp_ctx_s* ctx = op->ctx;
+  cudaStream_t st = ctx->cur;
+  if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  cudaStream_t cp = ctx->copy;
+  const uint64_t m = (uint64_t)op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  const uint64_t nchunk = (batch + per - 1) / per;
+  const bool stage_in = !host_pinned(y);
+  // page-locked: the staged measurements (pageable callers), then the flag
+  // source (one int = 1)
+  const size_t in_bytes = stage_in ? ((batch * m * eb + 255) & ~size_t(255)) : 0;
+  if (int e = pinned_reserve(ctx, in_bytes + 256)) return e;
+  char* pin_in = (char*)ctx->pinned;
+  int* one = (int*)((char*)ctx->pinned + in_bytes);
+  *one = 1;
+  if (ctx->events.empty()) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  cudaEvent_t ev_ready = ctx->events[0];
+  void *dy, *dtol;
+  ALLOC(dy, S_IN, batch * m * eb);
+  ALLOC(dtol, S_TOL, batch * 8);
+  int* flags;
+  ALLOC(flags, S_SYNC, nchunk * 4);
+  std::vector<double> tv;
+  if (!cfg->tolerances) tv.assign(batch, cfg->tolerance);
+  CU(cudaMemsetAsync(flags, 0, nchunk * 4, st));
+  CU(cudaMemcpyAsync(dtol, cfg->tolerances ? cfg->tolerances : tv.data(), batch * 8,
+                     cudaMemcpyHostToDevice, st));
+  // the copy stream starts after the flags are cleared
+  CU(cudaEventRecord(ev_ready, st));
+  CU(cudaStreamWaitEvent(cp, ev_ready, 0));
+  if (int e = omp_dev_locked(op, dtype, dy, batch, cfg, (const double*)dtol, out, st, 0, flags,
+                             (int64_t)per))
+    return e;
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
+    const char* src = (const char*)y + b0 * m * eb;
+    if (stage_in) {  // overlaps the solve and the previous chunk's transfer
+      std::memcpy(pin_in + b0 * m * eb, src, nb * m * eb);
+      src = pin_in + b0 * m * eb;
+    }
+    CU(cudaMemcpyAsync((char*)dy + b0 * m * eb, src, nb * m * eb, cudaMemcpyHostToDevice, cp));
+    CU(cudaMemcpyAsync(flags + c, one, 4, cudaMemcpyHostToDevice, cp));
+  }
+  CU(cudaStreamSynchronize(st));
+  CU(cudaStreamSynchronize(cp));
   return FMP_OK;
 }
 
@@ -994,8 +1058,17 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
   // large batches: copies overlapped with the solve, chunk by chunk (each
   // chunk still fills the GPU several times over)
   const uint64_t grid = (uint64_t)fmp::omp_grid(op->d, dtype, (int64_t)batch, (int64_t)T);
-  if (!cfg->record_correlations && !g_phase_prof && batch >= 8 * grid)
+  if (!cfg->record_correlations && !g_phase_prof && batch >= 8 * grid) {
+    const char* e = getenv("FMP_HOST_PATH");  // "chunked": the multi-launch path (timing tools)
+    const bool pinned_out = host_pinned(out->support) && host_pinned(out->coeffs) &&
+                            host_pinned(out->support_size) && host_pinned(out->iterations) &&
+                            host_pinned(out->residual) && host_pinned(out->aborted) &&
+                            (!out->modes || host_pinned(out->modes)) &&
+                            (!out->history_len || host_pinned(out->history_len));
+    if (pinned_out && !(e && !strcmp(e, "chunked")))
+      return omp_host_streamed(op, dtype, y, batch, cfg, out, grid);
     return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(8, batch / (2 * grid)));
+  }
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
   std::vector<double> tv;
@@ -1379,8 +1452,8 @@ int lg_local_best(fmp_large_s* lg, double* best) {
   if (lg->fused) {
     // one shard: the band pick (solvers.cpp:90-101) with the cut taken from
     // the device best, and h0 there, in the same round trip
-    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval,
-                            lg->view == 1 ? nullptr : lg->blkmax, lg->dfirst, st));
+    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval, lg->blkmax,
+                            lg->dfirst, st));
     CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
     CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -1491,7 +1564,8 @@ int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
   A((void**)&lg->lam, (size_t)lg->T * 4);
   A((void**)&lg->part, (size_t)std::max(grid, (lg->T + 255) / 256) * 3 * 8);
   A((void**)&lg->scal, 16 * 8);
-  A((void**)&lg->blkmax, (size_t)grid * 8);
+  // per-CTA maxima, then one maximum per 128-position tile (lg_launch_first)
+  A((void**)&lg->blkmax, ((size_t)grid + (size_t)(lg->np + 127) / 128) * 8);
   A((void**)&lg->dval, 64);
   A((void**)&lg->dfirst, 64);
   A((void**)&lg->drec, 64);
@@ -1586,9 +1660,9 @@ int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0
     const void* base;
     int64_t off, stride;
     lg_view(lg, &base, &off, &stride);
-    // chunk maxima from k_lg_max (not the fast kernel's partition) let it skip chunks
-    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, nullptr,
-                            lg->view == 1 ? nullptr : lg->blkmax, lg->dfirst, st));
+    // the tile maxima of the last k_lg_max / k_lg_fast over this view
+    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, nullptr, lg->blkmax,
+                            lg->dfirst, st));
     CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
     CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

@@ -129,6 +129,10 @@ struct OmpArgs {
   int* queue;               // work counter (zeroed before launch)
   int grid;
   unsigned long long* phase_ws;  // optional per-phase cycle totals (6)
+  // streamed input (optional): problem b may be read once ready[b / ready_chunk]
+  // != 0 (set by the copy stream after the chunk's host-to-device copy)
+  const int* ready;
+  int64_t ready_chunk;
 };
 
 struct CosArgs {

@@ -67,33 +67,46 @@ __global__ void __launch_bounds__(LG_THREADS) k_lg_fast(const V* __restrict__ h0
       }
     }
     if (t0 < ntiles) {
+      double tm = 0.0;
 #pragma unroll
       for (int r = 0; r < LG_RPT; ++r) {
         const int64_t k = k0 + lane + 32 * r;
         if (k < np) {
           hs[k] = acc[r];
-          best = fmax(best, mag2(acc[r]));
+          tm = fmax(tm, mag2(acc[r]));
         }
       }
+      tm = warp_max(tm);
+      if (lane == 0) blkmax[gridDim.x + t0] = tm;  // the tile's maximum (k_lg_first)
+      best = fmax(best, tm);
     }
   }
   best = block_max(best, red);
   if (tid == 0) blkmax[blockIdx.x] = best;
 }
 
-// per-CTA max |v|^2 of a strided view v[k'] = base[off + stride k'], k' < cnt
+// max |v|^2 of a strided view v[k'] = base[off + stride k'], k' < cnt: per
+// tile of 32 LG_RPT positions into tilemax = blkmax + gridDim.x (the tiles
+// of k_lg_fast), per CTA into blkmax
 template <class V>
 __global__ void __launch_bounds__(LG_THREADS) k_lg_max(const V* __restrict__ base, int64_t off,
                                                        int64_t stride, int64_t cnt,
                                                        double* __restrict__ blkmax) {
-  // block b owns the contiguous chunk [b chunk, (b + 1) chunk): k_lg_first
-  // skips the chunks whose maximum is below the cut
   __shared__ double red[32];
-  const int64_t chunk = (cnt + gridDim.x - 1) / gridDim.x;
-  const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(cnt, k0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = LG_THREADS / 32;
+  const int64_t tile = 32 * LG_RPT, ntiles = (cnt + tile - 1) / tile;
   double best = 0.0;
-  for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-    best = fmax(best, mag2(base[off + stride * k]));
+  for (int64_t t = (int64_t)blockIdx.x * nwarps + warp; t < ntiles; t += (int64_t)gridDim.x * nwarps) {
+    double tm = 0.0;
+#pragma unroll
+    for (int r = 0; r < LG_RPT; ++r) {
+      const int64_t k = t * tile + lane + 32 * r;
+      if (k < cnt) tm = fmax(tm, mag2(base[off + stride * k]));
+    }
+    tm = warp_max(tm);
+    if (lane == 0) blkmax[gridDim.x + t] = tm;
+    best = fmax(best, tm);
+  }
   best = block_max(best, red);
   if (threadIdx.x == 0) blkmax[blockIdx.x] = best;
 }
@@ -106,35 +119,36 @@ __global__ void k_lg_reduce_max(const double* __restrict__ part, int cnt, double
   if (threadIdx.x == 0) *out = b;
 }
 
-// smallest shard position k' with |v|^2 >= cut (atomicMin over the grid);
-// with blkmax (k_lg_max's chunk maxima) only chunks reaching the cut scan
-template <class V>
-__global__ void __launch_bounds__(LG_THREADS) k_lg_first(const V* __restrict__ base, int64_t off,
-                                                         int64_t stride, int64_t cnt, double cut,
-                                                         const double* __restrict__ cut_best,
-                                                         const double* __restrict__ blkmax,
-                                                         unsigned long long* __restrict__ first) {
-  // cut_best: the best |h|^2 on the device (one shard: no host round trip);
-  // same double arithmetic as the host's best * (1 - 1e-9)
+// first index in the band: stage 1 finds the first tile whose maximum
+// reaches the cut (every tile maximum is read once, in parallel; atomicMin),
+// stage 2 the first position >= cut inside it.  A tile's maximum reaches the
+// cut iff one of its entries does (same |v|^2 arithmetic), so the result is
+// the smallest k' with |v|^2 >= cut.
+// cut_best: the best |h|^2 on the device (one shard: no host round trip);
+// same double arithmetic as the host's best * (1 - 1e-9)
+__global__ void __launch_bounds__(LG_THREADS) k_lg_first_tile(const double* __restrict__ tilemax,
+                                                              int64_t ntiles, double cut,
+                                                              const double* __restrict__ cut_best,
+                                                              unsigned long long* __restrict__ first_tile) {
   if (cut_best) cut = *cut_best * (1.0 - 1e-9);
-  if (blkmax) {
-    if (blkmax[blockIdx.x] < cut) return;
-    const int64_t chunk = (cnt + gridDim.x - 1) / gridDim.x;
-    const int64_t k0 = (int64_t)blockIdx.x * chunk, k1 = min(cnt, k0 + chunk);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-      if (mag2(base[off + stride * k]) >= cut) {
-        atomicMin(first, (unsigned long long)k);
-        break;
-      }
-    return;
-  }
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    if (mag2(base[off + stride * k]) >= cut) {
-      atomicMin(first, (unsigned long long)k);
-      break;  // later k of this thread are larger
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x)
+    if (tilemax[t] >= cut) {
+      atomicMin(first_tile, (unsigned long long)t);
+      break;  // later t of this thread are larger
     }
-  }
+}
+
+template <class V>
+__global__ void k_lg_first_elem(const V* __restrict__ base, int64_t off, int64_t stride, int64_t cnt,
+                                double cut, const double* __restrict__ cut_best,
+                                const unsigned long long* __restrict__ first_tile,
+                                unsigned long long* __restrict__ first) {
+  if (cut_best) cut = *cut_best * (1.0 - 1e-9);
+  const unsigned long long t = *first_tile;
+  if (t == ~0ull) return;
+  const int64_t k = (int64_t)t * (32 * LG_RPT) + threadIdx.x;
+  if (k < cnt && mag2(base[off + stride * k]) >= cut) atomicMin(first, (unsigned long long)k);
 }
 
 // the pick record [best, first (as a double, exact below 2^53), h0 re, h0 im]
@@ -373,15 +387,20 @@ cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st) {
 cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
                             double cut, const double* cut_best, const double* blkmax,
                             unsigned long long* first, cudaStream_t st) {
+  // blkmax: the per-CTA maxima followed by the tile maxima of the last
+  // k_lg_max / k_lg_fast over this view; first[1] is scratch for the tile
   const int grid = lg_grid();
-  cudaMemsetAsync(first, 0xff, 8, st);
+  const int64_t ntiles = (cnt + 32 * LG_RPT - 1) / (32 * LG_RPT);
+  cudaMemsetAsync(first, 0xff, 16, st);
+  k_lg_first_tile<<<(unsigned)std::min<int64_t>(grid, (ntiles + LG_THREADS - 1) / LG_THREADS), LG_THREADS, 0,
+                    st>>>(blkmax + grid, ntiles, cut, cut_best, first + 1);
   if (dtype == C128)
-    k_lg_first<double2><<<grid, LG_THREADS, 0, st>>>((const double2*)base, off, stride, cnt, cut,
-                                                     cut_best, blkmax, first);
+    k_lg_first_elem<double2><<<1, 32 * LG_RPT, 0, st>>>((const double2*)base, off, stride, cnt, cut,
+                                                       cut_best, first + 1, first);
   else
-    k_lg_first<float2><<<grid, LG_THREADS, 0, st>>>((const float2*)base, off, stride, cnt, cut,
-                                                    cut_best, blkmax, first);
-  ++g_launches;
+    k_lg_first_elem<float2><<<1, 32 * LG_RPT, 0, st>>>((const float2*)base, off, stride, cnt, cut,
+                                                      cut_best, first + 1, first);
+  g_launches += 2;
   return cudaGetLastError();
 }
 

@@ -62,6 +62,8 @@ struct OmpK {
   int tw_a;       // two-level twiddle split
   double margin;  // relative slack on the residual identity
   unsigned long long* phase_ws;  // optional: cycles per phase (conv, fast, argmax, ls, resid, other)
+  const int* ready;              // optional streamed-input flags (OmpArgs)
+  int64_t ready_chunk;
 };
 
 template <bool HAD>
@@ -74,6 +76,22 @@ __device__ __forceinline__ double2 gram(const DevOp& op, unsigned a, unsigned b)
 // column-major packed lower triangle with capacity T: W(i, j), i >= j
 __device__ __forceinline__ int wofs(int T, int i, int j) {
   return j * T - (j * (j - 1)) / 2 + (i - j);
+}
+
+// streamed input: spin (acquire) until the copy stream has flagged the
+// chunk; a flag that never arrives traps after 10 s instead of hanging
+__device__ __forceinline__ void wait_ready(const int* flag) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) return;
+    __nanosleep(500);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) __trap();
+  }
 }
 
 // GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
@@ -178,7 +196,10 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
 
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_prob = atomicAdd(a.queue, 1);
+    if (tid == 0) {
+      s_prob = atomicAdd(a.queue, 1);
+      if (a.ready && s_prob < a.batch) wait_ready(a.ready + s_prob / a.ready_chunk);
+    }
     __syncthreads();
     const int64_t prob = s_prob;
     if (prob >= a.batch) break;
@@ -637,6 +658,8 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.tw_a = p.tw_a;
   k.margin = is_double(a.dtype) ? 1e-10 : 1e-5;
   k.phase_ws = a.phase_ws;
+  k.ready = a.ready;
+  k.ready_chunk = a.ready_chunk;
   const int grid = std::max(1, a.grid);
   if constexpr (CT == 1) {
     if (p.bufg) launch_g<V, HAD, RPT, true, NT, CT>(k, p.gmode, grid, p.total, st);

@@ -428,8 +428,9 @@ def test_omp_config4_c64_support_agreement_at_scale(fmp, oracle):
 
 
 def test_omp_host_chunked_equals_device(fmp, oracle):
-    # batches >= 8 x grid take the copy/compute-overlapped host path
-    # (fmp_capi.cu omp_host_chunked): results must equal the device path bitwise
+    # batches >= 8 x grid take a copy/compute-overlapped host path (with the
+    # wrapper's page-locked results: fmp_capi.cu omp_host_streamed, one launch
+    # fed by per-chunk ready flags): results must equal the device path bitwise
     import torch
     n, m, k, B = 1024, 256, 16, 1600
     rows = fmp.make_row_selection(n, m, 31)
@@ -445,6 +446,9 @@ def test_omp_host_chunked_equals_device(fmp, oracle):
     assert np.array_equal(host.support.astype(np.int64), out["support"].cpu().numpy())
     assert np.array_equal(host.coeffs, out["coeffs"].cpu().numpy())
     assert np.array_equal(host.iterations.astype(np.int64), out["iterations"].cpu().numpy())
+    # page-locked measurements: the streamed path without its staging copy
+    pinned = fmp.omp_solve_batch(op, torch.from_numpy(Y).pin_memory().numpy(), cfg, tolerances=tol)
+    assert np.array_equal(pinned.support, host.support) and np.array_equal(pinned.coeffs, host.coeffs)
     for b in range(0, B, 397):
         r = oracle.omp_solve("fourier", n, rows, Y[b], k, tol[b], "fast")
         assert [int(v) for v in host.support[b, :int(host.support_size[b])]] == \
