@@ -39,9 +39,16 @@ __device__ __forceinline__ void pass_dif(V* buf, int logS, int log2tab, const TW
   const int S = 1 << logS;
   const int o = u & (S - 1);
   const int base = ((u >> logS) << (logS + LOGR)) + o;
+  // padx(base + j S) = padx(base) + j (S + S / 2^LOGP) when S is a multiple
+  // of the padding period, or S = 1 with base a multiple of it (R >= 2^LOGP):
+  // one pointer and a constant step instead of a shift and add per element
+  const bool lin = logS >= LOGP || (logS == 0 && LOGR >= LOGP);
+  V* const p = buf + padx<LOGP>(base);
+  const int sp = S + (S >> LOGP);
+  auto at = [&](int j) -> V& { return lin ? p[j * sp] : buf[padx<LOGP>(base + j * S)]; };
   V v[R];
 #pragma unroll
-  for (int j = 0; j < R; ++j) v[j] = buf[padx<LOGP>(base + j * S)];
+  for (int j = 0; j < R; ++j) v[j] = at(j);
   if constexpr (HAD) {
     wht_reg<R>(v);
   } else {
@@ -80,7 +87,7 @@ __device__ __forceinline__ void pass_dif(V* buf, int logS, int log2tab, const TW
     }
   }
 #pragma unroll
-  for (int j = 0; j < R; ++j) buf[padx<LOGP>(base + j * S)] = v[j];
+  for (int j = 0; j < R; ++j) at(j) = v[j];
 }
 
 // C vectors of length 2^L (stride `stride` apart, padded layout) transformed

@@ -109,7 +109,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // (position, input block) order, so every position's sum is formed in a
 // register in ascending i_hi order (deterministic) and the first register
 // pass (bits 0-4) follows without touching shared memory.
-template <class V, int LOGB, int R2, int R3, int NTH>
+template <class V, int LOGB, int R2, int R3, int NTH, int NZ>
 __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict__ tab,
                                                      const uint32_t* __restrict__ roff, int m,
                                                      int log2n, const V* __restrict__ in,
@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   constexpr int ZN = B + (B >> R1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t mbar;
-  V* z = reinterpret_cast<V*>(smem_raw);
-  V* rb = z + ZN;                                                   // m values
+  V* z = reinterpret_cast<V*>(smem_raw);                            // NZ blocks
+  V* rb = z + NZ * ZN;                                              // m values
   uint32_t* tb = reinterpret_cast<uint32_t*>(rb + ((m + 3) & ~3));  // m entries
   const int tid = threadIdx.x;
   const int S = 1 << (log2n - LOGB);
@@ -146,14 +146,18 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   for (uint32_t it = 0; b < batch; b += gridDim.x, ++it) {
     if (use_bulk) mbar_wait(&mbar, it & 1);
     V* ob = out + b * ((int64_t)S << LOGB);
-    for (int khi = 0; khi < S; ++khi) {
+    // NZ output blocks per walk of the fold table: block khi0 + q takes the
+    // sign (-1)^popc((khi0 + q) & i_hi), i.e. that of khi0 flipped by the
+    // parity of i_hi & q (khi0 is a multiple of NZ)
+    for (int khi0 = 0; khi0 < S; khi0 += NZ) {
       // entries of row tid in (position, input block) order: one running sum
-      // per position, stored when the position changes; positions without
-      // rows read as zero through `seen` (no zero fill)
-      V* row = z + tid * 33;
+      // per position and block, stored when the position changes; positions
+      // without rows read as zero through `seen` (no zero fill)
       uint32_t seen = 0, jc = 32;
-      V acc = zero;
-      const uint32_t neg_mask = (uint32_t)khi;
+      V acc[NZ];
+#pragma unroll
+      for (int q = 0; q < NZ; ++q) acc[q] = zero;
+      const uint32_t neg_mask = (uint32_t)khi0;
       for (uint32_t e = e0; e < e1; e += 4) {
         uint32_t u[4];
         V x[4];
@@ -166,23 +170,38 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
           if (u[q] == 0xffffffffu) break;
           const uint32_t j = u[q] >> 26;
           if (j != jc) {
-            if (jc < 32) row[jc] = acc;
-            acc = zero;
+            if (jc < 32) {
+#pragma unroll
+              for (int w = 0; w < NZ; ++w) z[w * ZN + tid * 33 + jc] = acc[w];
+            }
+#pragma unroll
+            for (int w = 0; w < NZ; ++w) acc[w] = zero;
             jc = j;
             seen |= 1u << j;
           }
-          acc = (__popc((u[q] >> 20) & neg_mask) & 1) ? sub(acc, x[q]) : add(acc, x[q]);
+          const uint32_t ih = (u[q] >> 20) & 63u;
+          const uint32_t par = __popc(ih & neg_mask) & 1;
+#pragma unroll
+          for (int w = 0; w < NZ; ++w)
+            acc[w] = ((par ^ (__popc(ih & (uint32_t)w) & 1)) != 0) ? sub(acc[w], x[q]) : add(acc[w], x[q]);
         }
       }
-      if (jc < 32) row[jc] = acc;
-      V v[32];
+      if (jc < 32) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = (seen >> j) & 1 ? row[j] : zero;
-      wht_regs<R1>(v);
+        for (int w = 0; w < NZ; ++w) z[w * ZN + tid * 33 + jc] = acc[w];
+      }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) row[j] = v[j];
+      for (int w = 0; w < NZ; ++w) {
+        V* row = z + w * ZN + tid * 33;
+        V v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (seen >> j) & 1 ? row[j] : zero;
+        wht_regs<R1>(v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) row[j] = v[j];
+      }
       __syncthreads();
-      if (khi == S - 1) {
+      if (khi0 + NZ >= S) {
         // every read of this vector's r is done: stage the next one
         const int64_t nb = b + gridDim.x;
         if (nb < batch) {
@@ -194,13 +213,17 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
           }
         }
       }
-      V* o = ob + ((int64_t)khi << LOGB);
-      if constexpr (R3 == 0) {
-        fold_pass<V, LOGB, R1, R1, R2, NTH, true>(z, o, sc, tid);
-      } else {
-        fold_pass<V, LOGB, R1, R1, R2, NTH, false>(z, o, sc, tid);
-        __syncthreads();
-        fold_pass<V, LOGB, R1, R1 + R2, R3, NTH, true>(z, o, sc, tid);
+#pragma unroll
+      for (int w = 0; w < NZ; ++w) {
+        V* zw = z + w * ZN;
+        V* o = ob + ((int64_t)(khi0 + w) << LOGB);
+        if constexpr (R3 == 0) {
+          fold_pass<V, LOGB, R1, R1, R2, NTH, true>(zw, o, sc, tid);
+        } else {
+          fold_pass<V, LOGB, R1, R1, R2, NTH, false>(zw, o, sc, tid);
+          __syncthreads();
+          fold_pass<V, LOGB, R1, R1 + R2, R3, NTH, true>(zw, o, sc, tid);
+        }
       }
       __syncthreads();
     }
@@ -214,7 +237,7 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   }
 }
 
-template <class V, int LOGB, int R2, int R3>
+template <class V, int LOGB, int R2, int R3, int NZ>
 cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   const DevOp& op = *a.op;
   constexpr int B = 1 << LOGB, NTH = B >> 5;
@@ -223,9 +246,10 @@ cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   // one persistent CTA per vector in flight: small batches keep the job queue
   if (a.batch < 64) return cudaErrorNotSupported;
   const int64_t m = op.m;
-  const size_t smem = (size_t)(B + (B >> 5)) * sizeof(V) + (size_t)((m + 3) & ~3) * sizeof(V) + (size_t)m * 4;
+  if ((1 << (op.log2n - LOGB)) % NZ) return cudaErrorNotSupported;
+  const size_t smem = (size_t)NZ * (B + (B >> 5)) * sizeof(V) + (size_t)((m + 3) & ~3) * sizeof(V) + (size_t)m * 4;
   if (smem + 1024 > (size_t)smem_optin()) return cudaErrorNotSupported;
-  auto kern = k_wht_fold<V, LOGB, R2, R3, NTH>;
+  auto kern = k_wht_fold<V, LOGB, R2, R3, NTH, NZ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 1;
@@ -251,7 +275,13 @@ cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t st) {
   if (op.kind != HADAMARD || !a.in_omega || a.out_omega || !a.out) return cudaErrorNotSupported;
   const char* e = getenv("FMP_FOLD");  // FMP_FOLD=-1: job queue instead (timing tools)
   if (e && atoi(e) < 0) return cudaErrorNotSupported;
-  if (a.dtype == F32) return launch_fold_k<float, 14, 5, 4>(a, st);
+  if (a.dtype == F32) {
+    if (!(e && atoi(e) == 1)) {  // FMP_FOLD=1: one block per walk (timing tools)
+      const cudaError_t r = launch_fold_k<float, 14, 5, 4, 2>(a, st);
+      if (r != cudaErrorNotSupported) return r;
+    }
+    return launch_fold_k<float, 14, 5, 4, 1>(a, st);
+  }
   return cudaErrorNotSupported;
 }
 
