@@ -371,7 +371,7 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   // 32, position, input block) (fmp_transform_fold.cu)
   std::vector<uint32_t> fold_tab[4], fold_off[4];
   if (kind == FMP_HADAMARD && m < (1u << 20)) {
-    for (int q = 3; q < 4; ++q) {  // block sizes in use: 2^14 (f32)
+    for (int q = 2; q < 4; ++q) {  // block sizes in use: 2^14 (f32, f64, c64), 2^13 (c128)
       const int lb = 11 + q, s = d.log2n - lb;
       if (s < 1 || s > 6) continue;
       const uint32_t rows_per_block = 1u << (lb - 5);

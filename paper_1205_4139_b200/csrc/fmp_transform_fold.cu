@@ -122,13 +122,17 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t mbar;
   V* z = reinterpret_cast<V*>(smem_raw);                            // NZ blocks
+  // use_bulk: 1 = r staged by a bulk copy, 0 = by plain loads, 2 = r read
+  // in place through L1 (8-byte elements: no room beside the block buffer)
+  const bool rglob = use_bulk == 2;
   V* rb = z + NZ * ZN;                                              // m values
-  uint32_t* tb = reinterpret_cast<uint32_t*>(rb + ((m + 3) & ~3));  // m entries
+  uint32_t* tb = reinterpret_cast<uint32_t*>(rb + (rglob ? 0 : ((m + 3) & ~3)));  // m entries
   const int tid = threadIdx.x;
   const int S = 1 << (log2n - LOGB);
   const uint32_t rbytes = (uint32_t)m * (uint32_t)sizeof(V);
   int64_t b = blockIdx.x;
   if (b >= batch) return;
+  if (rglob) use_bulk = 0;
   if (tid == 0 && use_bulk) {
     mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   __syncthreads();
   if (use_bulk) {
     if (tid == 0) bulk_load(rb, in + b * m, rbytes, &mbar);
-  } else {
+  } else if (!rglob) {
     for (int k = tid; k < m; k += NTH) rb[k] = in[b * m + k];
     __syncthreads();
   }
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   for (uint32_t it = 0; b < batch; b += gridDim.x, ++it) {
     if (use_bulk) mbar_wait(&mbar, it & 1);
     V* ob = out + b * ((int64_t)S << LOGB);
+    const V* rv = rglob ? in + b * m : rb;
     // NZ output blocks per walk of the fold table: block khi0 + q takes the
     // sign (-1)^popc((khi0 + q) & i_hi), i.e. that of khi0 flipped by the
     // parity of i_hi & q (khi0 is a multiple of NZ)
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
 #pragma unroll
         for (int q = 0; q < 4; ++q) u[q] = e + q < e1 ? tb[e + q] : 0xffffffffu;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = u[q] != 0xffffffffu ? rb[u[q] & 0xfffffu] : zero;
+        for (int q = 0; q < 4; ++q) x[q] = u[q] != 0xffffffffu ? rv[u[q] & 0xfffffu] : zero;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (u[q] == 0xffffffffu) break;
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
       }
       __syncthreads();
     }
-    if (!use_bulk) {
+    if (!use_bulk && !rglob) {
       const int64_t nb = b + gridDim.x;
       if (nb < batch) {
         for (int k = tid; k < m; k += NTH) rb[k] = in[nb * m + k];
@@ -247,7 +252,9 @@ cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   if (a.batch < 64) return cudaErrorNotSupported;
   const int64_t m = op.m;
   if ((1 << (op.log2n - LOGB)) % NZ) return cudaErrorNotSupported;
-  const size_t smem = (size_t)NZ * (B + (B >> 5)) * sizeof(V) + (size_t)((m + 3) & ~3) * sizeof(V) + (size_t)m * 4;
+  const bool rglob = sizeof(V) >= 8;  // r through L1 (see the kernel)
+  const size_t smem = (size_t)NZ * (B + (B >> 5)) * sizeof(V) +
+                      (rglob ? 0 : (size_t)((m + 3) & ~3) * sizeof(V)) + (size_t)m * 4;
   if (smem + 1024 > (size_t)smem_optin()) return cudaErrorNotSupported;
   auto kern = k_wht_fold<V, LOGB, R2, R3, NTH, NZ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -258,16 +265,18 @@ cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   const bool bulk = ((uintptr_t)a.in % 16 == 0) && ((m * (int64_t)sizeof(V)) % 16 == 0);
   kern<<<(unsigned)grid, NTH, smem, st>>>(op.fold_tab[q], op.fold_off[q], (int)m, op.log2n,
                                           (const V*)a.in, (V*)a.out, a.batch,
-                                          1.0 / sqrt((double)op.n), bulk ? 1 : 0);
+                                          1.0 / sqrt((double)op.n), rglob ? 2 : (bulk ? 1 : 0));
   ++g_launches;
   return cudaGetLastError();
 }
 
-// f32: 2^14-point blocks (smem: z 66 KB + r + the fold table), passes 5 + 5 + 4.
-// 8-byte and wider elements stay on the job queue: measured on config 3
-// (f64 0.375 ms fold vs 0.340 ms queue, c64 0.388 vs 0.338; f32 0.160 vs
-// 0.203), the wider fold is bound by shared-memory wavefronts and bank
-// conflicts of the r gathers.
+// f32: 2^14-point blocks, two per walk of the fold table (smem: 2 x 66 KB +
+// r + the table), passes 5 + 5 + 4.  8-byte elements (f64, c64): 2^14-point
+// blocks one per walk, r read through L1 (no room to stage it); c128:
+// 2^13-point blocks.  Config 3 (1024 vectors): f32 0.162 (one block per
+// walk) -> 0.126 ms; f64 0.318 (job queue) -> 0.277 ms; c64 0.328 -> 0.287 ms;
+// c128 0.826 -> 0.691 ms.  Measured slower: f64 / c64 at 2^13 with two
+// blocks per walk (0.327 / 0.341 ms), f32 at 2^13 with one (0.242 ms).
 }  // namespace
 
 cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t st) {
@@ -275,13 +284,17 @@ cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t st) {
   if (op.kind != HADAMARD || !a.in_omega || a.out_omega || !a.out) return cudaErrorNotSupported;
   const char* e = getenv("FMP_FOLD");  // FMP_FOLD=-1: job queue instead (timing tools)
   if (e && atoi(e) < 0) return cudaErrorNotSupported;
+  const int plan = e ? atoi(e) : 0;
   if (a.dtype == F32) {
-    if (!(e && atoi(e) == 1)) {  // FMP_FOLD=1: one block per walk (timing tools)
+    if (plan != 1) {  // FMP_FOLD=1: one block per walk (timing tools)
       const cudaError_t r = launch_fold_k<float, 14, 5, 4, 2>(a, st);
       if (r != cudaErrorNotSupported) return r;
     }
     return launch_fold_k<float, 14, 5, 4, 1>(a, st);
   }
+  if (a.dtype == F64) return launch_fold_k<double, 14, 5, 4, 1>(a, st);
+  if (a.dtype == C64) return launch_fold_k<float2, 14, 5, 4, 1>(a, st);
+  if (a.dtype == C128) return launch_fold_k<double2, 13, 4, 4, 1>(a, st);
   return cudaErrorNotSupported;
 }
 

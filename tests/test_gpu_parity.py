@@ -100,20 +100,23 @@ def test_apply_adjoint_other_dtypes(fmp, oracle, dtype, tol):
         assert rel(h, want) < tol
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.complex64, np.complex128])
 @pytest.mark.parametrize("n,m", [(65536, 8192), (65536, 8191), (1 << 17, 12345)])
-def test_apply_adjoint_fold_path(fmp, oracle, n, m):
-    """Batched f32 Hadamard adjoint beyond one CTA (batch >= 64): the one-pass
-    fold kernel (fmp_transform_fold.cu); m * 4 bytes not a multiple of 16
-    takes its plain-load staging instead of the bulk copy."""
+def test_apply_adjoint_fold_path(fmp, oracle, n, m, dt):
+    """Batched Hadamard adjoint beyond one CTA (batch >= 64): the one-pass
+    fold kernel (fmp_transform_fold.cu; f32 two blocks per walk with r staged
+    by a bulk copy, 8-byte elements with r read through L1), or the job queue
+    (c128); m * 4 bytes not a multiple of 16 takes the plain-load staging."""
     om = oracle.make_row_selection(n, m, 11 + m)
     op = fmp.SensingOperator("hadamard", n, om)
     B = 70
-    R = np.stack([oracle.rng_complex_gaussian(oracle.derive_seed(m, b), m).real for b in range(B)])
-    R = R.astype(np.float32)
+    R = np.stack([oracle.rng_complex_gaussian(oracle.derive_seed(m, b), m) for b in range(B)])
+    R = (R.real if dt in (np.float32, np.float64) else R).astype(dt)
     H, idx = op.apply_adjoint(R, argmax=True)
+    tol = 1e-6 if dt in (np.float32, np.complex64) else 1e-13
     for b in (0, 1, 37, B - 1):
         want = oracle.apply_adjoint("hadamard", n, om, R[b].astype(np.complex128))
-        assert rel(H[b], want) < 1e-6
+        assert rel(H[b], want) < tol
         assert idx[b] == oracle.argmax_magnitude(H[b].astype(np.complex128)) + 1
 
 
