@@ -15,7 +15,10 @@ def main():
     for r in rows[1:]:
         if len(r) > vi and r[mi] == "gpu__time_duration.sum":
             name = r[ki].split("(")[0][:70]
-            tot[name] += float(r[vi].replace(",", ""))
+            v = float(r[vi].replace(",", ""))
+            if v != v:  # a launch ncu could not time
+                continue
+            tot[name] += v
             cnt[name] += 1
     s = sum(tot.values())
     for name, v in sorted(tot.items(), key=lambda kv: -kv[1]):

@@ -41,9 +41,12 @@ def launches(path):
     agg = {}
     for r in rows:
         name = r[4].split("(")[0]
+        v = float(r[-1].replace(",", ""))
+        if v != v:  # a launch ncu could not time (e.g. cut off at exit)
+            continue
         agg.setdefault(name, [0, 0.0])
         agg[name][0] += 1
-        agg[name][1] += float(r[-1])
+        agg[name][1] += v
     tot = sum(v[1] for v in agg.values())
     return [{"kernel": k, "launches": v[0], "ns": v[1], "share": v[1] / tot}
             for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])]
