@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
   double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // coefficients / z
   double2* s_b = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // rhs (eliminated)
   double2* s_t = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;      // LS solution
+  double2* s_c2 = reinterpret_cast<double2*>(p); p += 16 * (size_t)C3;     // column cache (LDL^H)
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)C3 + 15) / 16) * 16;
   double* s_mg = reinterpret_cast<double*>(p); p += 8 * (size_t)C3;        // |b|^2
   unsigned* s_bits = reinterpret_cast<unsigned*>(p);                         // support bitmap
@@ -276,31 +277,54 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
         // one barrier per column.  Pivot j is g_jj - sum_k |l_jk|^2 with the
         // terms subtracted in the reference's order (solvers.cpp:148-160).
         const double diag = gram(0u, 0u).x;
-        double2* L = sm_ <= a.s_cap ? reinterpret_cast<double2*>(sm) : Lg;
         auto row = [](int i) { return (size_t)i * (i + 1) / 2; };
+        // rows [r0, sm_) of the packed triangle in the shared-memory region,
+        // rows [0, r0) in global memory: row i is rewritten at every one of
+        // its i steps, so the long bottom rows take the fast memory and the
+        // rarely touched top rows spill (r0 = 0 when the whole triangle fits)
+        int r0 = 0;
+        if (sm_ > a.s_cap) {
+          const size_t cap = (size_t)a.region / 16, tot = row(sm_);
+          while (tot - row(r0) > cap) ++r0;
+        }
+        double2* const Ls = reinterpret_cast<double2*>(sm);
+        const size_t base0 = row(r0);
+        auto Lrow = [&](int i) -> double2* { return i < r0 ? Lg + row(i) : Ls + (row(i) - base0); };
         __syncthreads();  // buf is free
+        // column j of the factor, double-buffered in smem (s_t is free until
+        // the back substitution): the update of step j reads column j from
+        // one buffer and writes column j + 1, as it finalises, into the other
+        double2* colb[2] = {s_t, s_c2};
         for (int i = warp; i < sm_; i += nw) {
           const unsigned li = s_mrg[i];
-          for (int l = lane; l <= i; l += 32) L[row(i) + l] = gram(li, s_mrg[l]);
+          double2* Li = Lrow(i);
+          for (int l = lane; l <= i; l += 32) {
+            const double2 g = gram(li, s_mrg[l]);
+            Li[l] = g;
+            if (l == 0) colb[0][i] = g;
+          }
           if (lane == 0) s_b[i] = to_c128(h0w[li]);
         }
         __syncthreads();
         bool bad = false;
         for (int j = 0; j < sm_; ++j) {
-          const double d = L[row(j) + j].x;
+          const double2* cj = colb[j & 1];
+          double2* cn = colb[(j + 1) & 1];
+          const double d = cj[j].x;
           if (!(d > 1e-12 * diag)) { bad = true; break; }
           const double inv = 1.0 / d;
           const double2 bj = s_b[j];
           for (int i = j + 1 + warp; i < sm_; i += nw) {
-            const size_t ri = row(i);
-            const double2 aij = L[ri + j];
+            double2* Li = Lrow(i);
+            const double2 aij = cj[i];
             const double2 u = make_double2(aij.x * inv, aij.y * inv);  // a_ij / d_j
             for (int l = j + 1 + lane; l <= i; l += 32) {
-              const double2 alj = L[row(l) + j];
-              double2 v = L[ri + l];
+              const double2 alj = cj[l];
+              double2 v = Li[l];
               v.x -= u.x * alj.x + u.y * alj.y;  // a_il -= a_ij conj(a_lj) / d_j
               v.y -= u.y * alj.x - u.x * alj.y;
-              L[ri + l] = v;
+              Li[l] = v;
+              if (l == j + 1) cn[i] = v;
             }
             if (lane == 0) {
               s_b[i].x -= u.x * bj.x - u.y * bj.y;
@@ -313,11 +337,11 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
         // back substitution of D L'^H x = b' (column-oriented; x into s_t):
         // x_i = (b'_i - sum_{k>i} conj(a_ki) x_k) / d_i
         for (int i = sm_ - 1; i >= 0; --i) {
-          const size_t ri = row(i);
-          const double d = L[ri + i].x;
+          const double2* Li = Lrow(i);
+          const double d = Li[i].x;
           const double2 xi = make_double2(s_b[i].x / d, s_b[i].y / d);
           for (int q = tid; q < i; q += nth) {
-            const double2 pp = L[ri + q];
+            const double2 pp = Li[q];
             s_b[q].x -= pp.x * xi.x + pp.y * xi.y;
             s_b[q].y -= pp.x * xi.y - pp.y * xi.x;
           }
@@ -389,7 +413,7 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   const DevOp& op = *c.op;
   const int64_t n = op.n;
   const int C3 = 3 * (int)c.k;
-  const size_t small = 12 * (size_t)C3 + 16 + 16 * 3 * (size_t)C3 +
+  const size_t small = 12 * (size_t)C3 + 16 + 16 * 4 * (size_t)C3 +
                        ((sizeof(V) * (size_t)C3 + 15) / 16) * 16 + 8 * (size_t)C3 +
                        4 * (size_t)((n + 31) / 32) + 64;
   const size_t bufb = ((sizeof(V) * (size_t)(n + (n >> CLOGP)) + 15) / 16) * 16;
