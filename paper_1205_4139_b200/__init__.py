@@ -475,25 +475,30 @@ def _config(cfg: SolveConfig, tolerances=None):
     return c
 
 
-_TORCH_OF = {np.dtype(np.uint64): "int64", np.dtype(np.int64): "int64", np.dtype(np.float64): "float64",
-             np.dtype(np.complex128): "complex128", np.dtype(np.complex64): "complex64",
-             np.dtype(np.float32): "float32", np.dtype(np.int32): "int32", np.dtype(np.uint8): "uint8"}
 
-
-def _host_out(shape, dtype, zero=False):
-    """Result buffers for the host-buffer entry points: page-locked (torch's
-    caching host allocator, so device->host copies run at full speed and
-    repeated calls reuse the pages) when torch and a GPU are present."""
-    dtype = np.dtype(dtype)
+def _host_outs(specs):
+    """Several result buffers carved from ONE page-locked allocation (one
+    trip through torch's host allocator per call instead of one per buffer;
+    each view keeps the block alive).  specs: (shape, dtype, zero) tuples."""
+    sizes = [int(np.prod(shape, dtype=np.int64)) * np.dtype(dt).itemsize for shape, dt, _ in specs]
+    offs, tot = [], 0
+    for b in sizes:
+        offs.append(tot)
+        tot += (b + 63) // 64 * 64
     try:
         import torch
         if torch.cuda.is_available():
-            tdt = getattr(torch, _TORCH_OF[dtype])
-            t = (torch.zeros if zero else torch.empty)(shape, dtype=tdt, pin_memory=True)
-            return t.numpy().view(dtype)
-    except (ImportError, KeyError, RuntimeError):
+            blk = torch.empty(max(tot, 64), dtype=torch.uint8, pin_memory=True).numpy()
+            out = []
+            for (shape, dt, zero), o, b in zip(specs, offs, sizes):
+                v = blk[o:o + b].view(dt).reshape(shape)
+                if zero:
+                    v.fill(0)
+                out.append(v)
+            return out
+    except (ImportError, RuntimeError):
         pass
-    return np.zeros(shape, dtype)
+    return [np.zeros(shape, dt) for shape, dt, _ in specs]
 
 
 def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
@@ -513,14 +518,11 @@ def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
     if T < 1:
         raise InvalidArgument(1, "omp_solve: max_iterations must be >= 1")
     # every entry of these is written by the solve (support / coeffs zero padded)
-    sup = _host_out((B, T), np.uint64)
-    co = _host_out((B, T), np.complex128)
-    sz = _host_out(B, np.uint64)
-    it = _host_out(B, np.uint64)
-    rn = _host_out(B, np.float64)
-    ab = _host_out(B, np.int32)
-    md = _host_out((B, T), np.uint8, zero=True)  # rows past the last iteration stay 0
-    hl = _host_out(B, np.uint64)
+    sup, co, sz, it, rn, ab, md, hl = _host_outs([
+        ((B, T), np.uint64, False), ((B, T), np.complex128, False), ((B,), np.uint64, False),
+        ((B,), np.uint64, False), ((B,), np.float64, False), ((B,), np.int32, False),
+        ((B, T), np.uint8, True),  # rows past the last iteration stay 0
+        ((B,), np.uint64, False)])
     hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
     tol = None
     if tolerances is not None:
@@ -657,13 +659,13 @@ def cosamp_solve_batch(op: SensingOperator, Y, k: int, cfg: SolveConfig, toleran
     if T < 1:
         raise InvalidArgument(1, "cosamp_solve: max_iterations must be >= 1")
     kk = max(K, 1)
-    sup = np.zeros((B, kk), np.uint64)
-    co = np.zeros((B, kk), np.complex128)
-    sz = np.zeros(B, np.uint64)
-    it = np.zeros(B, np.uint64)
-    rn = np.zeros(B)
-    ab = np.zeros(B, np.int32)
-    sh = np.zeros((B, T, kk), np.uint64) if want_history else None
+    specs = [((B, kk), np.uint64, True), ((B, kk), np.complex128, True), ((B,), np.uint64, True),
+             ((B,), np.uint64, True), ((B,), np.float64, True), ((B,), np.int32, True)]
+    if want_history:
+        specs.append(((B, T, kk), np.uint64, True))
+    outs = _host_outs(specs)  # page-locked: the device->host copies run at full speed
+    sup, co, sz, it, rn, ab = outs[:6]
+    sh = outs[6] if want_history else None
     hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
     tol = None
     if tolerances is not None:
