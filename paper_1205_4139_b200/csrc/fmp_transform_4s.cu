@@ -237,10 +237,24 @@ __global__ void __launch_bounds__(FS_THREADS, 1) k_fs_a(FsArgs a) {
           }
         }
       } else {
+        int placed = 0;
         for (int e = tid; e < a.cnt; e += nth) {
           const uint32_t pos = a.lam[e];
           const int c = (int)(pos & (N2 - 1)) - c0;
-          if (c >= 0 && c < C) buf[c * stride + slot((int)(pos >> L2))] = load_cast<V, HAD>(a.xs[e]);
+          if (c >= 0 && c < C) {
+            buf[c * stride + slot((int)(pos >> L2))] = load_cast<V, HAD>(a.xs[e]);
+            placed = 1;
+          }
+        }
+        // a sparse input (the current estimate, |support| << N2) leaves most
+        // column tiles empty: their transform is zero, so store zeros and
+        // skip the passes (the barrier of __syncthreads_or covers the fill)
+        if (!__syncthreads_or(placed)) {
+          for (int e = tid; e < N1 * C; e += nth) {
+            const int q = e / C, c = e - q * C;
+            mid[b * n + ((int64_t)q << L2) + c0 + c] = zv;
+          }
+          continue;
         }
       }
     }
