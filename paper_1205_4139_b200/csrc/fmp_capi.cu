@@ -847,58 +847,72 @@ static int pinned_reserve(fmp_ctx_s* ctx, size_t bytes) {
 // page-locked buffers (stores over the host link as problems finish), so
 // nothing is exposed but the first chunk's copy and the wave tail.  Used when
 // every result buffer is page-locked (else omp_host_chunked).
-static int omp_host_streamed(fmp_op op, int dtype, const void* y, uint64_t batch,
-                             const fmp_omp_config* cfg, fmp_omp_result* out, uint64_t per) {
-  fmp_ctx_s* ctx = op->ctx;
-  cudaStream_t st = ctx->cur;
+// stream_in_setup: device buffers for y and the tolerances, the cleared
+// flags, the tolerances copied; the copy stream ordered after the clear.
+static int stream_in_setup(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t row_bytes,
+                           const fmp_omp_config* cfg, uint64_t nchunk, void** dy, void** dtol,
+                           int** flags, cudaStream_t st) {
   if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
-  cudaStream_t cp = ctx->copy;
-  const uint64_t m = (uint64_t)op->d.m;
-  const size_t eb = fmp::elem_bytes(dtype);
-  const uint64_t nchunk = (batch + per - 1) / per;
-  const bool stage_in = !host_pinned(y);
   // page-locked: the staged measurements (pageable callers), then the flag
   // source (one int = 1)
-  const size_t in_bytes = stage_in ? ((batch * m * eb + 255) & ~size_t(255)) : 0;
-  if (int e = pinned_reserve(ctx, in_bytes + 256)) return e;
-  char* pin_in = (char*)ctx->pinned;
-  int* one = (int*)((char*)ctx->pinned + in_bytes);
-  *one = 1;
+  const size_t in_bytes = !host_pinned(y) ? ((batch * row_bytes + 255) & ~size_t(255)) : 0;
+  if (int e = pinned_reserve(ctx, in_bytes + 256 + batch * 8)) return e;
+  *(int*)((char*)ctx->pinned + in_bytes) = 1;
+  double* ptol = (double*)((char*)ctx->pinned + in_bytes + 256);  // tolerances, page-locked
   if (ctx->events.empty()) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->events.push_back(e);
   }
-  cudaEvent_t ev_ready = ctx->events[0];
-  void *dy, *dtol;
-  ALLOC(dy, S_IN, batch * m * eb);
-  ALLOC(dtol, S_TOL, batch * 8);
-  int* flags;
-  ALLOC(flags, S_SYNC, nchunk * 4);
-  std::vector<double> tv;
-  if (!cfg->tolerances) tv.assign(batch, cfg->tolerance);
-  CU(cudaMemsetAsync(flags, 0, nchunk * 4, st));
-  CU(cudaMemcpyAsync(dtol, cfg->tolerances ? cfg->tolerances : tv.data(), batch * 8,
-                     cudaMemcpyHostToDevice, st));
-  // the copy stream starts after the flags are cleared
-  CU(cudaEventRecord(ev_ready, st));
-  CU(cudaStreamWaitEvent(cp, ev_ready, 0));
-  if (int e = omp_dev_locked(op, dtype, dy, batch, cfg, (const double*)dtol, out, st, 0, flags,
-                             (int64_t)per))
-    return e;
+  ALLOC(*dy, S_IN, batch * row_bytes);
+  ALLOC(*dtol, S_TOL, batch * 8);
+  ALLOC(*flags, S_SYNC, nchunk * 4);
+  CU(cudaMemsetAsync(*flags, 0, nchunk * 4, st));
+  if (cfg->tolerances) std::memcpy(ptol, cfg->tolerances, batch * 8);
+  else std::fill(ptol, ptol + batch, cfg->tolerance);
+  CU(cudaMemcpyAsync(*dtol, ptol, batch * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaEventRecord(ctx->events[0], st));
+  CU(cudaStreamWaitEvent(ctx->copy, ctx->events[0], 0));
+  return FMP_OK;
+}
+
+// after the launch: the chunks and their flags on the copy stream, then wait
+static int stream_in_finish(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t row_bytes,
+                            uint64_t per, void* dy, int* flags, cudaStream_t st) {
+  cudaStream_t cp = ctx->copy;
+  const bool stage_in = !host_pinned(y);
+  const size_t in_bytes = stage_in ? ((batch * row_bytes + 255) & ~size_t(255)) : 0;
+  char* pin_in = (char*)ctx->pinned;
+  const int* one = (const int*)((char*)ctx->pinned + in_bytes);
+  const uint64_t nchunk = (batch + per - 1) / per;
   for (uint64_t c = 0; c < nchunk; ++c) {
     const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
-    const char* src = (const char*)y + b0 * m * eb;
+    const char* src = (const char*)y + b0 * row_bytes;
     if (stage_in) {  // overlaps the solve and the previous chunk's transfer
-      std::memcpy(pin_in + b0 * m * eb, src, nb * m * eb);
-      src = pin_in + b0 * m * eb;
+      std::memcpy(pin_in + b0 * row_bytes, src, nb * row_bytes);
+      src = pin_in + b0 * row_bytes;
     }
-    CU(cudaMemcpyAsync((char*)dy + b0 * m * eb, src, nb * m * eb, cudaMemcpyHostToDevice, cp));
+    CU(cudaMemcpyAsync((char*)dy + b0 * row_bytes, src, nb * row_bytes, cudaMemcpyHostToDevice, cp));
     CU(cudaMemcpyAsync(flags + c, one, 4, cudaMemcpyHostToDevice, cp));
   }
   CU(cudaStreamSynchronize(st));
   CU(cudaStreamSynchronize(cp));
   return FMP_OK;
+}
+
+static int omp_host_streamed(fmp_op op, int dtype, const void* y, uint64_t batch,
+                             const fmp_omp_config* cfg, fmp_omp_result* out, uint64_t per) {
+  fmp_ctx_s* ctx = op->ctx;
+  cudaStream_t st = ctx->cur;
+  const size_t row_bytes = (size_t)op->d.m * fmp::elem_bytes(dtype);
+  const uint64_t nchunk = (batch + per - 1) / per;
+  void *dy, *dtol;
+  int* flags;
+  if (int e = stream_in_setup(ctx, y, batch, row_bytes, cfg, nchunk, &dy, &dtol, &flags, st)) return e;
+  if (int e = omp_dev_locked(op, dtype, dy, batch, cfg, (const double*)dtol, out, st, 0, flags,
+                             (int64_t)per))
+    return e;
+  return stream_in_finish(ctx, y, batch, row_bytes, per, dy, flags, st);
 }
 
 // host-buffer solve in chunks: the copy stream moves chunk c + 1 in (and
@@ -1118,7 +1132,7 @@ static int cosamp_validate(fmp_op op, int dtype, uint64_t k, const fmp_omp_confi
 
 static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch, uint64_t k,
                              const fmp_omp_config* cfg, const double* dtol, fmp_cosamp_result* out,
-                             cudaStream_t st) {
+                             cudaStream_t st, const int* ready = nullptr, int64_t ready_chunk = 0) {
   fmp_ctx_s* ctx = op->ctx;
   const int64_t T = (int64_t)cfg->max_iterations, n = op->d.n, m = op->d.m;
   const size_t eb = fmp::elem_bytes(dtype);
@@ -1145,6 +1159,8 @@ static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch
   a.hist_sup = out->support_history;
   a.hist = cfg->record_correlations ? out->history : nullptr;
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
+  a.ready = ready;
+  a.ready_chunk = ready_chunk;
   const size_t c3 = 3 * (size_t)std::max<uint64_t>(k, 1);
   double2* L;
   ALLOC(L, S_W, (size_t)std::max(a.grid, 1) * c3 * (c3 + 1) / 2 * 16);
@@ -1219,6 +1235,23 @@ int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64
   const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
   const uint64_t kk = std::max<uint64_t>(k, 1);
   const size_t eb = fmp::elem_bytes(dtype);
+  // large batches with page-locked results: one launch fed by per-chunk
+  // ready flags, results stored straight into the caller's buffers (as
+  // omp_host_streamed)
+  const uint64_t grid = (uint64_t)fmp::omp_grid(op->d, dtype, (int64_t)batch, (int64_t)T);
+  if (k && !cfg->record_correlations && !g_phase_prof && batch >= 8 * grid &&
+      host_pinned(out->support) && host_pinned(out->coeffs) && host_pinned(out->support_size) &&
+      host_pinned(out->iterations) && host_pinned(out->residual) && host_pinned(out->aborted) &&
+      (!out->support_history || host_pinned(out->support_history))) {
+    void *dy, *dtol;
+    int* flags;
+    const uint64_t per = grid, nchunk = (batch + per - 1) / per;
+    if (int e = stream_in_setup(ctx, y, batch, m * eb, cfg, nchunk, &dy, &dtol, &flags, st)) return e;
+    if (int e = cosamp_dev_locked(op, dtype, dy, batch, k, cfg, (const double*)dtol, out, st, flags,
+                                  (int64_t)per))
+      return e;
+    return stream_in_finish(ctx, y, batch, m * eb, per, dy, flags, st);
+  }
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
   std::vector<double> tv;

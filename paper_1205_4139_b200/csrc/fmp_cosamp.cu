@@ -41,6 +41,8 @@ struct CosK {
   void* r_ws;               // m
   int* queue;
   unsigned long long* phase_ws;  // optional cycles per phase (conv, fast, identify, ls, resid, other)
+  const int* ready;              // optional streamed-input flags
+  int64_t ready_chunk;
 };
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
@@ -226,7 +228,10 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
 
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_prob = atomicAdd(a.queue, 1);
+    if (tid == 0) {
+      s_prob = atomicAdd(a.queue, 1);
+      if (a.ready && s_prob < a.batch) wait_ready(a.ready + s_prob / a.ready_chunk);
+    }
     __syncthreads();
     const int64_t prob = s_prob;
     if (prob >= a.batch) break;
@@ -448,6 +453,8 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   k.r_ws = c.r_ws;
   k.queue = c.queue;
   k.phase_ws = c.phase_ws;
+  k.ready = c.ready;
+  k.ready_chunk = c.ready_chunk;
   auto f = k_cosamp<V, HAD>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   f<<<std::max(1, c.grid), CS_THREADS, smem, st>>>(k);

@@ -16,6 +16,22 @@ namespace fmp {
 
 namespace {
 
+// streamed input: spin (acquire) until the copy stream has flagged the
+// chunk; a flag that never arrives traps after 10 s instead of hanging
+__device__ __forceinline__ void wait_ready(const int* flag) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) return;
+    __nanosleep(500);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) __trap();
+  }
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {

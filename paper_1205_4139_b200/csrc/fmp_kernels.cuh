@@ -157,6 +157,8 @@ struct CosArgs {
   int* queue;
   int grid;
   unsigned long long* phase_ws;
+  const int* ready;         // optional streamed-input flags (as OmpArgs)
+  int64_t ready_chunk;
 };
 
 // launchers (return cudaError_t); all async on `stream`

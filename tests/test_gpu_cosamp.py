@@ -162,3 +162,36 @@ def test_cosamp_real_and_single_precision(fmp, oracle):
                          dtype=np.complex64)
     assert g.support == [j + 1 for j in np.flatnonzero(x)]
     assert rel(g.coeffs, x[np.flatnonzero(x)]) < 1e-4
+
+
+def test_cosamp_host_streamed_equals_pageable_path(fmp, oracle):
+    # batches >= 8 x grid with page-locked results (the wrapper) take the
+    # one-launch streamed path (per-chunk ready flags, results stored into
+    # the page-locked buffers); pageable results take the plain copy path:
+    # both must agree bitwise, and with the oracle on sampled problems
+    import ctypes as C
+    n, m, k, B = 1024, 256, 16, 2400
+    om = oracle.make_row_selection(n, m, 77)
+    op = fmp.SensingOperator("fourier", n, om)
+    Y, _, _ = fmp.make_batch("fourier", n, om, k, B, base_seed=77, noise_stddev=0.01)
+    tol = np.ascontiguousarray(1e-9 * np.linalg.norm(Y, axis=1))
+    cfg = fmp.SolveConfig(10, 0.0, "fast")
+    r = fmp.cosamp_solve_batch(op, Y, k, cfg, tolerances=tol, want_history=True)
+    sup = np.zeros((B, k), np.uint64)
+    co = np.zeros((B, k), np.complex128)
+    sz, it = np.zeros(B, np.uint64), np.zeros(B, np.uint64)
+    rn, ab = np.zeros(B), np.zeros(B, np.int32)
+    sh = np.zeros((B, 10, k), np.uint64)
+    res = fmp.CosampResult(sup.ctypes.data, co.ctypes.data, sz.ctypes.data, it.ctypes.data,
+                           rn.ctypes.data, ab.ctypes.data, sh.ctypes.data, None)
+    c = fmp._config(cfg, tol.ctypes.data_as(C.POINTER(C.c_double)))
+    assert fmp._lib.fmp_cosamp_solve(op.handle, fmp.DTYPES[Y.dtype], Y.ctypes.data, B, k,
+                                     C.byref(c), C.byref(res)) == 0
+    assert np.array_equal(sup, r.support) and np.array_equal(co, r.coeffs)
+    assert np.array_equal(sz, r.support_size) and np.array_equal(it, r.iterations)
+    assert np.array_equal(rn, r.residual) and np.array_equal(ab.astype(bool), r.aborted)
+    assert np.array_equal(sh, r.support_history)
+    for b in range(0, B, 599):
+        o, _ = oracle.cosamp_solve("fourier", n, om, Y[b], k, 10, tol[b], "fast")
+        s = int(r.support_size[b])
+        assert [int(v) for v in r.support[b, :s]] == [int(v) for v in o.support]
