@@ -483,7 +483,9 @@ cudaError_t gen_batch(const DevOp& op, int64_t k, double noise_stddev, int real,
   a.sc = noise_stddev * std::sqrt(2.0);
   const int64_t total = batch * a.G, ntw = op.kind == FOURIER ? op.n : 0;
   const int64_t nval = 3 * total + 2 * ntw;
-  a.cap = (unsigned long long)nval;
+  // ~5 % of the values land in the band; the list holds 12.5 % + 4096, more
+  // than 100 standard deviations above the expected count at any size
+  a.cap = (unsigned long long)(nval / 8 + 4096);
   // one scratch allocation, carved
   size_t off = 0;
   auto carve = [&](size_t bytes) {
@@ -493,7 +495,7 @@ cudaError_t gen_batch(const DevOp& op, int64_t k, double noise_stddev, int real,
   };
   const size_t o_sup = carve(batch * k * 4), o_key = carve(batch * (size_t)h * 4),
                o_val = carve(batch * (size_t)h * 4), o_u1 = carve(total * 8), o_ang = carve(total * 8),
-               o_v = carve(nval * 8), o_nf = carve(8), o_fi = carve(nval * 8), o_fa = carve(nval * 8),
+               o_v = carve(nval * 8), o_nf = carve(8), o_fi = carve(a.cap * 8), o_fa = carve(a.cap * 8),
                o_xs = carve(batch * k * 16), o_nz = carve(a.noisy ? batch * op.m * 16 : 16),
                o_tw = carve(ntw * 16 + 16);
   char* base_p = nullptr;
