@@ -125,8 +125,12 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   // use_bulk: 1 = r staged by a bulk copy, 0 = by plain loads, 2 = r read
   // in place through L1 (8-byte elements: no room beside the block buffer)
   const bool rglob = use_bulk == 2;
+  // use_bulk >= 4: as use_bulk - 4, with the fold table read in place
+  // (through L1) instead of staged, which leaves room to stage r
+  const bool tglob = use_bulk >= 4;
+  if (tglob) use_bulk -= 4;
   V* rb = z + NZ * ZN;                                              // m values
-  uint32_t* tb = reinterpret_cast<uint32_t*>(rb + (rglob ? 0 : ((m + 3) & ~3)));  // m entries
+  const uint32_t* tb = tglob ? tab : reinterpret_cast<uint32_t*>(rb + (rglob ? 0 : ((m + 3) & ~3)));
   const int tid = threadIdx.x;
   const int S = 1 << (log2n - LOGB);
   const uint32_t rbytes = (uint32_t)m * (uint32_t)sizeof(V);
@@ -137,7 +141,10 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
     mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int k = tid; k < m; k += NTH) tb[k] = tab[k];
+  if (!tglob) {
+    uint32_t* ts = reinterpret_cast<uint32_t*>(rb + (rglob ? 0 : ((m + 3) & ~3)));  // m entries
+    for (int k = tid; k < m; k += NTH) ts[k] = tab[k];
+  }
   const uint32_t e0 = roff[tid], e1 = roff[tid + 1];
   __syncthreads();
   if (use_bulk) {
@@ -252,9 +259,14 @@ cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   if (a.batch < 64) return cudaErrorNotSupported;
   const int64_t m = op.m;
   if ((1 << (op.log2n - LOGB)) % NZ) return cudaErrorNotSupported;
-  const bool rglob = sizeof(V) >= 8;  // r through L1 (see the kernel)
+  const char* fe = getenv("FMP_FOLD");
+  // 8-byte elements: r staged with the table read in place through L1
+  // (f64 0.279 -> 0.264 ms, c64 0.289 -> 0.279 ms at config 3), or with
+  // FMP_FOLD=2 r read in place and the table staged; c128: r in place
+  const bool tglob = sizeof(V) == 8 && !(fe && atoi(fe) == 2);
+  const bool rglob = sizeof(V) >= 8 && !tglob;  // r through L1 (see the kernel)
   const size_t smem = (size_t)NZ * (B + (B >> 5)) * sizeof(V) +
-                      (rglob ? 0 : (size_t)((m + 3) & ~3) * sizeof(V)) + (size_t)m * 4;
+                      (rglob ? 0 : (size_t)((m + 3) & ~3) * sizeof(V)) + (tglob ? 0 : (size_t)m * 4);
   if (smem + 1024 > (size_t)smem_optin()) return cudaErrorNotSupported;
   auto kern = k_wht_fold<V, LOGB, R2, R3, NTH, NZ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -265,15 +277,17 @@ cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   const bool bulk = ((uintptr_t)a.in % 16 == 0) && ((m * (int64_t)sizeof(V)) % 16 == 0);
   kern<<<(unsigned)grid, NTH, smem, st>>>(op.fold_tab[q], op.fold_off[q], (int)m, op.log2n,
                                           (const V*)a.in, (V*)a.out, a.batch,
-                                          1.0 / sqrt((double)op.n), rglob ? 2 : (bulk ? 1 : 0));
+                                          1.0 / sqrt((double)op.n),
+                                          (rglob ? 2 : (bulk ? 1 : 0)) + (tglob ? 4 : 0));
   ++g_launches;
   return cudaGetLastError();
 }
 
 // f32: 2^14-point blocks, two per walk of the fold table (smem: 2 x 66 KB +
 // r + the table), passes 5 + 5 + 4.  8-byte elements (f64, c64): 2^14-point
-// blocks one per walk, r read through L1 (no room to stage it); c128:
-// 2^13-point blocks.  Config 3 (1024 vectors): f32 0.162 (one block per
+// blocks one per walk, r staged and the table read through L1 (no room for
+// both; r read through L1 instead measured slower); c128: 2^13-point blocks,
+// r through L1.  Config 3 (1024 vectors): f32 0.162 (one block per
 // walk) -> 0.126 ms; f64 0.318 (job queue) -> 0.277 ms; c64 0.328 -> 0.287 ms;
 // c128 0.826 -> 0.691 ms.  Measured slower: f64 / c64 at 2^13 with two
 // blocks per walk (0.327 / 0.341 ms), f32 at 2^13 with one (0.242 ms).
