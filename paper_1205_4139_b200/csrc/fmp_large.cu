@@ -96,16 +96,31 @@ __global__ void __launch_bounds__(LG_THREADS) k_lg_max(const V* __restrict__ bas
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = LG_THREADS / 32;
   const int64_t tile = 32 * LG_RPT, ntiles = (cnt + tile - 1) / tile;
   double best = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * nwarps + warp; t < ntiles; t += (int64_t)gridDim.x * nwarps) {
-    double tm = 0.0;
+  // TU tiles per warp per round, all loads issued before the reductions
+  // (one tile at a time leaves each warp waiting on HBM latency per tile)
+  constexpr int TU = 4;
+  const int64_t step = (int64_t)gridDim.x * nwarps;
+  for (int64_t t0 = (int64_t)blockIdx.x * nwarps + warp; t0 < ntiles; t0 += TU * step) {
+    V v[TU][LG_RPT];
 #pragma unroll
-    for (int r = 0; r < LG_RPT; ++r) {
-      const int64_t k = t * tile + lane + 32 * r;
-      if (k < cnt) tm = fmax(tm, mag2(base[off + stride * k]));
+    for (int u = 0; u < TU; ++u)
+#pragma unroll
+      for (int r = 0; r < LG_RPT; ++r) {
+        const int64_t k = (t0 + u * step) * tile + lane + 32 * r;
+        v[u][r] = k < cnt ? base[off + stride * k] : zero_of(V{});
+      }
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      const int64_t t = t0 + u * step;
+      double tm = 0.0;
+#pragma unroll
+      for (int r = 0; r < LG_RPT; ++r) tm = fmax(tm, mag2(v[u][r]));
+      tm = warp_max(tm);
+      if (t < ntiles) {
+        if (lane == 0) blkmax[gridDim.x + t] = tm;
+        best = fmax(best, tm);
+      }
     }
-    tm = warp_max(tm);
-    if (lane == 0) blkmax[gridDim.x + t] = tm;
-    best = fmax(best, tm);
   }
   best = block_max(best, red);
   if (threadIdx.x == 0) blkmax[blockIdx.x] = best;
