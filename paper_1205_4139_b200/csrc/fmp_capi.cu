@@ -1726,6 +1726,96 @@ int fmp_large_stop(fmp_large lg) {
   return FMP_OK;
 }
 
+// One shard (fmp_large_solve): one host round trip per iteration.  LS, the
+// explicit residual a conventional next row needs, the next correlation,
+// its band pick and every scalar the host decides on are enqueued together;
+// the correlation is speculative (wasted on the last iteration, an abort or
+// a halt), which the single synchronisation pays for many times over.  Same
+// kernels in the same order as fmp_large_advance + lg_local_best, so the
+// results are bitwise those of the two-round-trip protocol.
+static int lg_advance_fused(fmp_large_s* lg, uint64_t pick, const double* h0_at, int* done,
+                            double* local_best) {
+  cudaStream_t st = lg_stream(lg);
+  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
+                       lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
+  const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
+  if (next_conv)
+    if (int e = lg_residual_launch(lg, lg->s + 1)) return e;
+  double sc[3] = {0, 0, 0};
+  CU(cudaMemcpyAsync(sc, lg->scal + 2, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(sc + 1, lg->scal + 6, 8, cudaMemcpyDeviceToHost, st));
+  if (next_conv) CU(cudaMemcpyAsync(sc + 2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
+  const bool spec = lg->t < lg->T;
+  int spec_view = lg->view;
+  if (spec) {
+    if ((int64_t)(lg->t + 1) <= lg->fast_until) {
+      CU(fmp::lg_launch_fast(lg->dtype, lg->h0s, lg->hs, lg->gcm, lg->np, lg->P, lg->p, lg->n,
+                             lg->lam, lg->xn, lg->s + 1, lg->blkmax, st));
+      spec_view = 1;
+    } else {
+      if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->r, lg->hfull, 1, nullptr, st)) return e;
+      spec_view = 2;
+    }
+    const int keep = lg->view;
+    lg->view = spec_view;
+    const void* base;
+    int64_t off, stride;
+    lg_view(lg, &base, &off, &stride);
+    lg->view = keep;
+    if (spec_view == 1) CU(fmp::lg_launch_reduce_max(lg->blkmax, lg->dval, st));
+    else CU(fmp::lg_launch_max(lg->dtype, base, off, stride, lg->np, lg->blkmax, lg->dval, st));
+    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval, lg->blkmax,
+                            lg->dfirst, st));
+    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
+    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaStreamSynchronize(st));
+  if (sc[1] != 0.0) {  // rank deficient: keep the previous state (solvers.cpp:380-385)
+    lg->aborted = 1;
+    lg->done = true;
+    *done = 1;
+    if (next_conv || !lg->rn_explicit) {
+      if (int e = lg_residual(lg, &lg->rn)) return e;
+      lg->rn_explicit = true;
+    }
+    return FMP_OK;
+  }
+  lg->s += 1;
+  lg->support.push_back(pick);
+  lg->sel[pick] = 1;
+  lg->iters = lg->t;
+  const double zz = sc[0];
+  const double r2id = lg->yy - zz;  // residual and halting (solvers.cpp:388-402)
+  const double margin = lg->dtype == FMP_C128 ? 1e-10 : 1e-5;
+  const bool near = !(r2id > lg->tol * lg->tol + margin * lg->yy);
+  if (next_conv) {
+    lg->rn = std::sqrt(sc[2]);
+    lg->rn_explicit = true;
+  } else if (near) {
+    if (int e = lg_residual(lg, &lg->rn)) return e;
+    lg->rn_explicit = true;
+  } else {
+    lg->rn = std::sqrt(std::max(r2id, 0.0));
+    lg->rn_explicit = false;
+  }
+  if ((lg->rn_explicit && lg->rn <= lg->tol) || lg->t >= lg->T) {
+    lg->done = true;
+    *done = 1;
+    if (!lg->rn_explicit) {
+      if (int e = lg_residual(lg, &lg->rn)) return e;
+      lg->rn_explicit = true;
+    }
+    return FMP_OK;
+  }
+  lg->t += 1;
+  lg->view = spec_view;
+  lg->first_ready = true;
+  *local_best = lg->first_rec[0];
+  *done = 0;
+  return FMP_OK;
+}
+
 int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* done,
                       double* local_best) {
   if (!lg || !h0_at || !done || !local_best) return fail(FMP_EINVAL, "null argument");
@@ -1740,6 +1830,7 @@ int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* don
     return fmp_large_stop(lg);
   }
   CU(cudaSetDevice(lg->op->ctx->device));
+  if (lg->fused && !getenv("FMP_LARGE_TWO_TRIPS")) return lg_advance_fused(lg, pick, h0_at, done, local_best);
   cudaStream_t st = lg_stream(lg);
   {
     std::lock_guard<std::mutex> lk(lg->op->ctx->mu);

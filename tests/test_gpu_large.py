@@ -62,3 +62,28 @@ def test_config5_prefix(fmp, oracle):
     r = oracle.omp_solve("fourier", n, rows, y.astype(np.complex128), T, 0.0, "fast")
     assert list(sup) == list(r.support)
     assert rel(co, r.coeffs) < 1e-4
+
+
+@pytest.mark.parametrize("mode,noise", [("gpu", 0.0), ("conventional", 0.02), ("fast", 0.02)])
+def test_single_round_trip_equals_two_round_trips(fmp, mode, noise):
+    # fmp_large_solve's one-synchronisation iteration (speculative next
+    # correlation, fmp_capi.cu lg_advance_fused) against the two-round-trip
+    # protocol: bitwise the same supports, coefficients, counters, residual
+    # (noisy signals halt on the tolerance, exercising the discarded
+    # speculation and the explicit-residual branches)
+    import os
+    n, m, k = 4096, 1024, 40
+    rows = fmp.make_row_selection(n, m, fmp.derive_seed(8, 1 << 40))
+    op = fmp.SensingOperator("fourier", n, rows)
+    Y, _, nn = fmp.make_batch("fourier", n, rows, k, 1, base_seed=8, noise_stddev=noise)
+    y = Y[0]
+    t = float(nn[0]) if noise else 1e-9 * np.linalg.norm(y)
+    cfg = fmp.SolveConfig(2 * k, t, mode)
+    one = fmp.large_solve(op, y, cfg, dtype=np.complex128)
+    os.environ["FMP_LARGE_TWO_TRIPS"] = "1"
+    try:
+        two = fmp.large_solve(op, y, cfg, dtype=np.complex128)
+    finally:
+        del os.environ["FMP_LARGE_TWO_TRIPS"]
+    assert np.array_equal(one[0], two[0]) and np.array_equal(one[1], two[1])
+    assert one[2:] == two[2:]
