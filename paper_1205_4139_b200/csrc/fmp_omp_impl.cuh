@@ -683,6 +683,13 @@ cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
   if constexpr (!HAD && sizeof(V) >= 8) {
     if (omp_ctas_v<V, HAD>(*a.op, a.batch, a.max_iter) == 2) return launch_omp_t<V, HAD, 8, 256, 2>(a, st);
   }
+  // latency regime (no more problems than SMs) at n = 1024: one 4-warp CTA
+  // per problem, whose block-wide barriers and reductions are cheaper than
+  // those of 16 warps (config 1: 75.8 -> 65.9 us per recovery)
+  if (a.op->n == 32 * 8 * 4 && a.batch <= num_sms()) {
+    const char* e = getenv("FMP_OMP_NT");  // FMP_OMP_NT=512: the 16-warp CTA (timing tools)
+    if (!(e && atoi(e) == 512)) return launch_omp_t<V, HAD, 8, 128, 1>(a, st);
+  }
   // lanes own RPT outputs; pick RPT so that one tile per warp covers n
   constexpr int NW = OMP_THREADS / 32;
   if (a.op->n >= 32 * 8 * NW && OMP_THREADS <= 512) return launch_omp_t<V, HAD, 8, OMP_THREADS, 1>(a, st);
