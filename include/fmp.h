@@ -214,6 +214,10 @@ uint64_t fmp_qr_cols(fmp_qr qr);
  * squares, residual, other), summed over CTAs, readable afterwards */
 int fmp_set_phase_profiling(int enabled);
 int fmp_phase_cycles(fmp_ctx ctx, double* out6);
+/* with phase profiling on, the fp32 solves (c64 / f32) also count, over the
+ * last solve: identifications, fp64-re-evaluated candidates, and
+ * identifications whose candidates overflowed the per-CTA list */
+int fmp_refine_stats(fmp_ctx ctx, double* out3);
 
 /* ------------------------------------------- sharded single-signal solver */
 /* omp_solve for ONE large signal spread over `nshards` GPUs (config 5).

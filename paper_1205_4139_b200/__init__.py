@@ -83,6 +83,7 @@ _sig("fmp_fma_peak", C.c_int, _vp, C.c_int, C.POINTER(C.c_double))
 _sig("fmp_last_error", C.c_char_p)
 _sig("fmp_set_phase_profiling", C.c_int, C.c_int)
 _sig("fmp_phase_cycles", C.c_int, _vp, _vp)
+_sig("fmp_refine_stats", C.c_int, _vp, _vp)
 _sig("fmp_last_launch_count", C.c_int)
 _sig("fmp_ctx_create", C.c_int, C.c_int, C.POINTER(_vp))
 _sig("fmp_ctx_destroy", C.c_int, _vp)
@@ -219,6 +220,14 @@ class Context:
         v = np.zeros(6)
         _check(_lib.fmp_phase_cycles(self.handle, _ptr(v)))
         return dict(zip(["conventional", "fast", "identify", "least_squares", "residual", "other"], v))
+
+    def refine_stats(self) -> dict:
+        """fp32 solves, last solve with phase profiling on: identifications,
+        candidates re-evaluated in fp64, identifications that overflowed the
+        per-CTA candidate list."""
+        v = np.zeros(3)
+        _check(_lib.fmp_refine_stats(self.handle, _ptr(v)))
+        return dict(zip(["identifications", "candidates", "overflows"], v))
 
     def close(self) -> None:
         if getattr(self, "handle", None):

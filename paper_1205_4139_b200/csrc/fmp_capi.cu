@@ -76,7 +76,7 @@ struct Workspace {
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
             S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
-            S_OHSUP,
+            S_OHSUP, S_Y64, S_H0X, S_GOFF, S_RST,
             S_ALT = 64 };  // S_ALT + slot: the alternate per-CTA workspace set
 
 }  // namespace
@@ -90,6 +90,16 @@ struct fmp_ctx_s {
   void* pinned = nullptr;             // page-locked staging for pageable host buffers (lazy)
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;    // chunk hand-offs between the two streams (lazy)
+  // abort word of the streamed-input paths: page-locked, mapped into the
+  // device address space; the host raises it on an error path so a kernel
+  // spinning on ready flags returns without any further CUDA call (lazy)
+  int* abort_host = nullptr;
+  const volatile int* abort_dev = nullptr;
+  // the workspaces are one set per context: a call on another stream waits
+  // for the last call that used them (ws_done, recorded on ws_stream)
+  cudaEvent_t ws_done = nullptr;
+  cudaStream_t ws_stream = nullptr;
+  bool ws_pending = false;
   Workspace ws;
   std::mutex mu;
 };
@@ -123,7 +133,8 @@ cudaStream_t pick_stream(fmp_ctx_s* ctx, void* s) {
 
 // batched transform on device pointers
 int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_omega,
-                  const void* in, void* out, uint64_t batch, uint64_t* amax, cudaStream_t st) {
+                  const void* in, void* out, uint64_t batch, uint64_t* amax, cudaStream_t st,
+                  int slot_off = 0) {
   fmp_ctx_s* ctx = op->ctx;
   fmp::TransformArgs a{};
   a.op = &op->d;
@@ -137,14 +148,30 @@ int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_om
   a.argmax_out = amax;
   if (op->d.n > fmp::transform_max_n(dtype)) {
     void* w;
-    ALLOC(w, S_WORK, (size_t)batch * op->d.n * fmp::elem_bytes(dtype));
+    ALLOC(w, slot_off + S_WORK, (size_t)batch * op->d.n * fmp::elem_bytes(dtype));
     a.work = w;
     int* sy;
-    ALLOC(sy, S_SYNC, (32 + batch) * sizeof(int));
+    ALLOC(sy, slot_off + S_SYNC, (32 + batch) * sizeof(int));
     a.sync = sy;
   }
   CU(fmp::launch_transform(a, st));
   g_launch_count = fmp::last_launch_count();
+  return FMP_OK;
+}
+
+// Serialise workspace users across streams: a call enqueued on stream st
+// first waits for the previous call's work if that went to another stream
+// (ws_enter), and marks its own end (ws_leave).  Calls on one stream are
+// already ordered.  Held under ctx->mu.
+int ws_enter(fmp_ctx_s* ctx, cudaStream_t st) {
+  if (ctx->ws_pending && ctx->ws_stream != st) CU(cudaStreamWaitEvent(st, ctx->ws_done, 0));
+  return FMP_OK;
+}
+int ws_leave(fmp_ctx_s* ctx, cudaStream_t st) {
+  if (!ctx->ws_done) CU(cudaEventCreateWithFlags(&ctx->ws_done, cudaEventDisableTiming));
+  CU(cudaEventRecord(ctx->ws_done, st));
+  ctx->ws_stream = st;
+  ctx->ws_pending = true;
   return FMP_OK;
 }
 
@@ -175,6 +202,19 @@ int fmp_phase_cycles(fmp_ctx ctx, double* out6) {
   CU(cudaStreamSynchronize(ctx->cur));
   CU(cudaMemcpy(v, ph, sizeof(v), cudaMemcpyDeviceToHost));
   for (int i = 0; i < 6; ++i) out6[i] = (double)v[i];
+  return FMP_OK;
+}
+
+int fmp_refine_stats(fmp_ctx ctx, double* out3) {
+  if (!ctx || !out3) return fail(FMP_EINVAL, "null argument");
+  CU(cudaSetDevice(ctx->device));
+  cudaError_t e = cudaSuccess;
+  void* rs = ctx->ws.get(S_RST, 64, &e);
+  if (!rs) return fail(FMP_ENOMEM, "refine statistics buffer");
+  unsigned long long v[3];
+  CU(cudaStreamSynchronize(ctx->cur));
+  CU(cudaMemcpy(v, rs, sizeof(v), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 3; ++i) out3[i] = (double)v[i];
   return FMP_OK;
 }
 
@@ -433,8 +473,21 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   if ((e = fmp::launch_kernel_finish(d, st)) != cudaSuccess)
     return cleanup(fail(FMP_ECUDA, "kernel finish: %s", cudaGetErrorString(e)));
   launches += 2;
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess)
+  // max_{k != 0} |c_k| for the fp32 paths' rounding bounds
+  unsigned long long* goff = nullptr;
+  {
+    cudaError_t ea = cudaSuccess;
+    goff = (unsigned long long*)ctx->ws.get(S_GOFF, 8, &ea);
+    if (!goff) return cleanup(fail(FMP_ENOMEM, "operator build scratch: %s", cudaGetErrorString(ea)));
+  }
+  if ((e = fmp::launch_gmax_off(d, goff, st)) != cudaSuccess)
+    return cleanup(fail(FMP_ECUDA, "kernel bound: %s", cudaGetErrorString(e)));
+  ++launches;
+  unsigned long long gbits = 0;
+  if ((e = cudaMemcpyAsync(&gbits, goff, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
     return cleanup(fail(FMP_ECUDA, "operator build: %s", cudaGetErrorString(e)));
+  std::memcpy(&d.goff, &gbits, 8);
   g_launch_count = launches;
   *out = op;
   return FMP_OK;
@@ -763,6 +816,29 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
   a.ready = ready;
   a.ready_chunk = ready_chunk;
+  a.abort_word = ctx->abort_dev;
+  if (!fmp::is_double(dtype)) {
+    // fp32 data: the fp64 h0 = Phi^H y of every problem (the widened fp32
+    // measurements through the fp64 transform), from which the solver
+    // re-evaluates its identification candidates and takes the least-squares
+    // right-hand side.  Needs the whole input: not on the streamed path.
+    if (ready) return fail(FMP_EINVAL, "internal: streamed input with fp32 data");
+    const int wdt = fmp::is_complex(dtype) ? FMP_C128 : FMP_F64;
+    const size_t web = (size_t)fmp::elem_bytes(wdt);
+    double* y64;
+    ALLOC(y64, wo + S_Y64, batch * m * web);
+    CU(fmp::launch_widen((const float*)y, y64, (int64_t)(batch * m * (web / 8)), st));
+    void* h0x;
+    ALLOC(h0x, wo + S_H0X, batch * n * web);
+    if (int s = run_transform(op, wdt, 1, 1, 0, y64, h0x, batch, nullptr, st, wo)) return s;
+    a.h0x = h0x;
+    if (g_phase_prof) {
+      unsigned long long* rs;
+      ALLOC(rs, S_RST, 64);
+      CU(cudaMemsetAsync(rs, 0, 64, st));
+      a.rstats = rs;
+    }
+  }
   double2* w;
   ALLOC(w, wo + S_W, (size_t)a.grid * (T * (T + 1) / 2) * 16);
   a.w_ws = w;
@@ -853,6 +929,19 @@ static int stream_in_setup(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t
                            const fmp_omp_config* cfg, uint64_t nchunk, void** dy, void** dtol,
                            int** flags, cudaStream_t st) {
   if (!ctx->copy) CU(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  if (!ctx->abort_host) {
+    int* h = nullptr;
+    CU(cudaHostAlloc((void**)&h, 64, cudaHostAllocMapped));
+    void* dv = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dv, h, 0);
+    if (e != cudaSuccess) {
+      cudaFreeHost(h);
+      return fail(FMP_ECUDA, "abort word: %s", cudaGetErrorString(e));
+    }
+    ctx->abort_host = h;
+    ctx->abort_dev = (const volatile int*)dv;
+  }
+  *(volatile int*)ctx->abort_host = 0;
   // page-locked: the staged measurements (pageable callers), then the flag
   // source (one int = 1)
   const size_t in_bytes = !host_pinned(y) ? ((batch * row_bytes + 255) & ~size_t(255)) : 0;
@@ -876,8 +965,29 @@ static int stream_in_setup(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t
   return FMP_OK;
 }
 
-// after the launch: the chunks and their flags on the copy stream, then wait
+// after the launch: the chunks and their flags on the copy stream, then wait.
+// Any failure raises the abort word first, so the kernel spinning on the
+// remaining flags returns (its problems marked kInputLost) instead of hanging
+static int stream_in_chunks(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t row_bytes,
+                            uint64_t per, void* dy, int* flags, cudaStream_t st);
 static int stream_in_finish(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t row_bytes,
+                            uint64_t per, void* dy, int* flags, cudaStream_t st,
+                            const int32_t* aborted_host = nullptr) {
+  const int rc = stream_in_chunks(ctx, y, batch, row_bytes, per, dy, flags, st);
+  if (rc != FMP_OK) {
+    *(volatile int*)ctx->abort_host = 1;
+    cudaStreamSynchronize(st);
+    cudaStreamSynchronize(ctx->copy);
+    return rc;
+  }
+  if (aborted_host)
+    for (uint64_t b = 0; b < batch; ++b)
+      if (aborted_host[b] == 2)
+        return fail(FMP_ECUDA, "streamed input: problem %llu never arrived (copy stream stalled)",
+                    (unsigned long long)b);
+  return FMP_OK;
+}
+static int stream_in_chunks(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_t row_bytes,
                             uint64_t per, void* dy, int* flags, cudaStream_t st) {
   cudaStream_t cp = ctx->copy;
   const bool stage_in = !host_pinned(y);
@@ -910,9 +1020,12 @@ static int omp_host_streamed(fmp_op op, int dtype, const void* y, uint64_t batch
   int* flags;
   if (int e = stream_in_setup(ctx, y, batch, row_bytes, cfg, nchunk, &dy, &dtol, &flags, st)) return e;
   if (int e = omp_dev_locked(op, dtype, dy, batch, cfg, (const double*)dtol, out, st, 0, flags,
-                             (int64_t)per))
+                             (int64_t)per)) {
+    *(volatile int*)ctx->abort_host = 1;  // nothing was launched, or it must not wait
+    cudaStreamSynchronize(st);
     return e;
-  return stream_in_finish(ctx, y, batch, row_bytes, per, dy, flags, st);
+  }
+  return stream_in_finish(ctx, y, batch, row_bytes, per, dy, flags, st, out->aborted);
 }
 
 // host-buffer solve in chunks: the copy stream moves chunk c + 1 in (and
@@ -1079,7 +1192,8 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
                             host_pinned(out->residual) && host_pinned(out->aborted) &&
                             (!out->modes || host_pinned(out->modes)) &&
                             (!out->history_len || host_pinned(out->history_len));
-    if (pinned_out && !(e && !strcmp(e, "chunked")))
+    // (fp32 data needs the whole batch for its fp64 h0 before the solve)
+    if (pinned_out && !(e && !strcmp(e, "chunked")) && fmp::is_double(dtype))
       return omp_host_streamed(op, dtype, y, batch, cfg, out, grid);
     return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(8, batch / (2 * grid)));
   }
@@ -1161,6 +1275,7 @@ static int cosamp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch
   a.grid = fmp::omp_grid(op->d, dtype, (int64_t)batch, T);
   a.ready = ready;
   a.ready_chunk = ready_chunk;
+  a.abort_word = ctx->abort_dev;
   const size_t c3 = 3 * (size_t)std::max<uint64_t>(k, 1);
   double2* L;
   ALLOC(L, S_W, (size_t)std::max(a.grid, 1) * c3 * (c3 + 1) / 2 * 16);
@@ -1248,9 +1363,12 @@ int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64
     const uint64_t per = grid, nchunk = (batch + per - 1) / per;
     if (int e = stream_in_setup(ctx, y, batch, m * eb, cfg, nchunk, &dy, &dtol, &flags, st)) return e;
     if (int e = cosamp_dev_locked(op, dtype, dy, batch, k, cfg, (const double*)dtol, out, st, flags,
-                                  (int64_t)per))
+                                  (int64_t)per)) {
+      *(volatile int*)ctx->abort_host = 1;
+      cudaStreamSynchronize(st);
       return e;
-    return stream_in_finish(ctx, y, batch, m * eb, per, dy, flags, st);
+    }
+    return stream_in_finish(ctx, y, batch, m * eb, per, dy, flags, st, out->aborted);
   }
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;

@@ -43,6 +43,7 @@ struct CosK {
   unsigned long long* phase_ws;  // optional cycles per phase (conv, fast, identify, ls, resid, other)
   const int* ready;              // optional streamed-input flags
   int64_t ready_chunk;
+  const volatile int* abort_word;
 };
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
   __shared__ double red[32];
   __shared__ int s_hist[256];
   __shared__ unsigned long long s_ctl[4];
-  __shared__ int s_prob;
+  __shared__ int s_prob, s_lost;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T, K = a.K;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
@@ -226,15 +227,29 @@ __global__ void __launch_bounds__(CS_THREADS, 1) k_cosamp(CosK a) {
     }
   };
 
+  // s_lost: streamed input abandoned (host abort or timeout), sticky: the
+  // CTA fails every later problem without waiting again
+  if (tid == 0) s_lost = 0;
   for (;;) {
     __syncthreads();
     if (tid == 0) {
       s_prob = atomicAdd(a.queue, 1);
-      if (a.ready && s_prob < a.batch) wait_ready(a.ready + s_prob / a.ready_chunk);
+      if (!s_lost && a.ready && s_prob < a.batch &&
+          !wait_ready(a.ready + s_prob / a.ready_chunk, a.abort_word))
+        s_lost = 1;
     }
     __syncthreads();
     const int64_t prob = s_prob;
     if (prob >= a.batch) break;
+    if (s_lost) {
+      if (tid == 0) {
+        a.size[prob] = 0;
+        a.iters[prob] = 0;
+        a.resid[prob] = 0.0;
+        a.aborted[prob] = kInputLost;
+      }
+      continue;
+    }
     const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
     const double tol = a.tol[prob];
     double yy = 0.0;
@@ -455,6 +470,7 @@ cudaError_t launch_cos(const CosArgs& c, cudaStream_t st) {
   k.phase_ws = c.phase_ws;
   k.ready = c.ready;
   k.ready_chunk = c.ready_chunk;
+  k.abort_word = c.abort_word;
   auto f = k_cosamp<V, HAD>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   f<<<std::max(1, c.grid), CS_THREADS, smem, st>>>(k);

@@ -17,20 +17,29 @@ namespace fmp {
 namespace {
 
 // streamed input: spin (acquire) until the copy stream has flagged the
-// chunk; a flag that never arrives traps after 10 s instead of hanging
-__device__ __forceinline__ void wait_ready(const int* flag) {
+// chunk.  Returns false instead when the host raised the abort word (a
+// page-locked, device-mapped int the host sets on an error path, so no CUDA
+// call is needed to release the kernel) or after 60 s without the flag; the
+// caller then marks its problems failed and the host reports FMP_ECUDA.  No
+// trap: the context survives.
+__device__ __forceinline__ bool wait_ready(const int* flag, const volatile int* abort_word) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
+  for (unsigned spin = 0;; ++spin) {
     int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if (v) return;
+    if (v) return true;
     __nanosleep(500);
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 10000000000ull) __trap();
+    if ((spin & 63) == 63) {  // the abort word lives in host memory: poll it sparingly
+      if (abort_word && *abort_word) return false;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60000000000ull) return false;
+    }
   }
 }
+// aborted[] value of a problem whose streamed input never arrived
+constexpr int kInputLost = 2;
 
 int num_sms() {
   static int sms = 0;

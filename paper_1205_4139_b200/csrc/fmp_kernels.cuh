@@ -28,6 +28,7 @@ struct DevOp {
   float2* g32 = nullptr;      // c rounded to c64 (Fourier)
   double* gr64 = nullptr;     // c real part (Hadamard), exact k/N
   uint16_t* glat = nullptr;   // Hadamard lattice N*c + 32768 (|N c| <= M); null if M > 32767
+  double goff = 0.0;          // max over k != 0 of |c_k| (fp32 rounding bounds)
   // Omega scatter sorted by transform slot (slot = brev(row) Fourier, row
   // Hadamard): the large-n transform's blocks find their rows by bisection
   uint32_t* scat_pos = nullptr;  // m, ascending slots
@@ -133,6 +134,11 @@ struct OmpArgs {
   // != 0 (set by the copy stream after the chunk's host-to-device copy)
   const int* ready;
   int64_t ready_chunk;
+  const volatile int* abort_word;  // device view of the host's abort word (streamed input)
+  // fp32 data: fp64 h0 = Phi^H y per problem (batch x n, c128 / f64; the
+  // identification and the least-squares right-hand side are decided in fp64)
+  const void* h0x;
+  unsigned long long* rstats;  // optional: identifications, candidates, overflows
 };
 
 struct CosArgs {
@@ -159,6 +165,7 @@ struct CosArgs {
   unsigned long long* phase_ws;
   const int* ready;         // optional streamed-input flags (as OmpArgs)
   int64_t ready_chunk;
+  const volatile int* abort_word;
 };
 
 // launchers (return cudaError_t); all async on `stream`
@@ -171,6 +178,10 @@ int fs_split(int log2n);  // N1 = 2^fs_split rows of the two-pass transform, 0: 
 cudaError_t launch_fast_update(const FastUpdateArgs& a, cudaStream_t stream);
 cudaError_t launch_argmax(const ArgmaxArgs& a, cudaStream_t stream);
 cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t stream);
+// max over k != 0 of |c_k| into *out (zeroed by the launcher)
+cudaError_t launch_gmax_off(const DevOp& op, unsigned long long* out, cudaStream_t stream);
+// widen fp32 values to fp64 (count scalars)
+cudaError_t launch_widen(const float* in, double* out, int64_t count, cudaStream_t stream);
 cudaError_t launch_twiddles(const DevOp& op, cudaStream_t stream);
 cudaError_t launch_omp(const OmpArgs& a, cudaStream_t stream);
 cudaError_t launch_cosamp(const CosArgs& a, cudaStream_t stream);

@@ -64,7 +64,22 @@ struct OmpK {
   unsigned long long* phase_ws;  // optional: cycles per phase (conv, fast, argmax, ls, resid, other)
   const int* ready;              // optional streamed-input flags (OmpArgs)
   int64_t ready_chunk;
+  const volatile int* abort_word;  // host-raised abort of the streamed input (OmpArgs)
+  // fp32 data (REFINE): fp64 h0 = Phi^H y per problem (batch x n, c128 / f64),
+  // the error-bound coefficient and max_{k != 0} |c_k| (DevOp::goff)
+  const void* h0x;
+  double ecoef;
+  double goff;
+  unsigned long long* rstats;  // optional: identifications, candidates, overflows
 };
+
+// candidates re-evaluated in fp64 per identification (fp32 data) before the
+// block falls back to evaluating every qualifying element thread-serially
+constexpr int RCAP = 64;
+
+template <class V> struct wide_t { using T = double2; };
+template <> struct wide_t<double> { using T = double; };
+template <> struct wide_t<float> { using T = double; };
 
 template <bool HAD>
 __device__ __forceinline__ double2 gram(const DevOp& op, unsigned a, unsigned b) {
@@ -86,7 +101,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[96];
   __shared__ unsigned redu[32];
-  __shared__ int s_prob;
+  __shared__ int s_prob, s_lost;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
@@ -134,6 +149,14 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   V* s_xn = reinterpret_cast<V*>(p); p += ((sizeof(V) * (size_t)T + 15) / 16) * 16;
   unsigned* s_lam = reinterpret_cast<unsigned*>(p); p += ((4 * (size_t)T + 15) / 16) * 16;
   unsigned* s_sel = reinterpret_cast<unsigned*>(p);  // n bits: atoms selected so far
+  p += ((4 * (size_t)((n + 31) / 32) + 15) / 16) * 16;
+  // REFINE: identification candidates (index, fp64 |h|^2) and their count
+  double* s_cval = reinterpret_cast<double*>(p); p += 8 * RCAP;
+  unsigned* s_cand = reinterpret_cast<unsigned*>(p); p += 4 * RCAP;
+  int* s_ncand = reinterpret_cast<int*>(p);
+  constexpr bool REFINE = sizeof(typename scal<V>::T) == 4;
+  using X = typename wide_t<V>::T;
+  const X* h0x_all = reinterpret_cast<const X*>(a.h0x);
 
   // slot -> row map of the Omega scatter (-1: zero slot), so the adjoint's
   // first pass reads r directly
@@ -178,17 +201,33 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     }
   };
 
+  // s_lost: streamed input abandoned (host abort or timeout), sticky: the
+  // CTA fails every later problem without waiting again
+  if (tid == 0) s_lost = 0;
   for (;;) {
     __syncthreads();
     if (tid == 0) {
       s_prob = atomicAdd(a.queue, 1);
-      if (a.ready && s_prob < a.batch) wait_ready(a.ready + s_prob / a.ready_chunk);
+      if (!s_lost && a.ready && s_prob < a.batch &&
+          !wait_ready(a.ready + s_prob / a.ready_chunk, a.abort_word))
+        s_lost = 1;
     }
     __syncthreads();
     const int64_t prob = s_prob;
     if (prob >= a.batch) break;
+    if (s_lost) {
+      if (tid == 0) {
+        a.size[prob] = 0;
+        a.iters[prob] = 0;
+        a.resid[prob] = 0.0;
+        a.aborted[prob] = kInputLost;
+        if (a.hlen) a.hlen[prob] = 0;
+      }
+      continue;
+    }
     const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
     const double tol = a.tol[prob];
+    const X* h0x = REFINE ? h0x_all + prob * n : nullptr;
 
     for (int i = tid; i < (n + 31) / 32; i += nth) s_sel[i] = 0u;
     if (s_xmap)
@@ -238,6 +277,50 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
       return sqrt(block_sum(r2, red));
     };
 
+    // REFINE: the fp64 residual norm ||y - Phi_Lambda x|| (solvers.cpp:388-389)
+    // summed directly over the cnt atoms, O(M t), with fp64 entries of Phi
+    // (entry(), transform.cpp:154-163): halting decisions near the tolerance
+    // and the reported residual_norm do not depend on fp32 rounding
+    auto residual64 = [&](int cnt) -> double {
+      double r2 = 0.0;
+      for (int j = tid; j < m; j += nth) {
+        const unsigned w = op.omega[j];
+        double ar = 0.0, ai = 0.0;
+        for (int q = 0; q < cnt; ++q) {
+          const double2 xv = s_x[q];
+          const unsigned l = s_lam[q];
+          if constexpr (HAD) {
+            const double sg = (__popc(w & l) & 1) ? -1.0 : 1.0;
+            ar = fma(sg, xv.x, ar);
+            ai = fma(sg, xv.y, ai);
+          } else {
+            const double2 e = op.tw64[(w * l) & (unsigned)(n - 1)];
+            ar = fma(xv.x, e.x, fma(-xv.y, e.y, ar));
+            ai = fma(xv.x, e.y, fma(xv.y, e.x, ai));
+          }
+        }
+        const double2 yv = to_c128(y[j]);
+        const double rr = yv.x - ar * sc, ri = yv.y - ai * sc;
+        r2 += rr * rr + ri * ri;
+      }
+      return sqrt(block_sum(r2, red));
+    };
+    // REFINE: fp64 correlation h_j = h0_j - sum_tau x_tau c[(j - lambda_tau)
+    // mod N] (or c[j ^ lambda_tau]), the reference's fast_update value
+    // (kernel.cpp:227-261) from the fp64 h0 and kernel, one thread
+    auto h64_serial = [&](unsigned j) -> double {
+      double2 acc = to_c128(h0x[j]);
+      for (int q = 0; q < s; ++q) {
+        const double2 xv = s_x[q];
+        const double2 g = gram<HAD>(op, j, s_lam[q]);
+        acc.x -= xv.x * g.x - xv.y * g.y;
+        acc.y -= xv.x * g.y + xv.y * g.x;
+      }
+      return acc.x * acc.x + acc.y * acc.y;
+    };
+    // |h0_j| <= ||phi_j|| ||y|| = sqrt(M/N) ||y|| bounds every correlation
+    const double hy = sqrt((double)m / (double)n * yy);
+
     if (!(rn <= tol)) {
       for (int t = 1; t <= T; ++t) {
         const bool fast_row = t >= 2 && (int64_t)t <= a.fast_until;
@@ -249,6 +332,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
                          : nullptr;
         double best = 0.0;
         double m2[RPT];
+        if (REFINE && tid == 0) *s_ncand = 0;  // read after the barriers below
         mark(5);
         if (!fast_row) {
           // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
@@ -326,40 +410,154 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         const double my_best = best;  // this thread's own maximum
         best = block_max<false>(best, red);
         mark(fast_row ? 1 : 0);
-        if (best == 0.0) break;
-        const double cut = best * (1.0 - kTieBandRel);
-        unsigned first = 0xffffffffu;
-        if (!fast_row) {
-          // only a thread whose own maximum (over these same indices k) reaches
-          // the band can hold the pick
-          const double scv = t == 1 ? 1.0 : sc;
-          if (my_best >= cut)
-            for (int k = tid; k < n; k += nth)
-              if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
-        } else if (regs_only) {
-#pragma unroll
-          for (int r = RPT - 1; r >= 0; --r)
-            if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
-        } else if (ntiles) {
-          // several tiles per warp: only a thread whose own maximum reaches
-          // the band re-reads its own entries, in ascending index order
-          if (my_best >= cut)
-            for (int tile = warp; tile < ntiles && first == 0xffffffffu; tile += nw)
-#pragma unroll
-              for (int r = 0; r < RPT; ++r) {
-                const int i = tile * 32 * RPT + lane + 32 * r;
-                if (msc[i] >= cut) { first = (unsigned)i; break; }
-              }
-        } else {
-          for (int k = tid; k < n; k += nth)
-            if (msc[k] >= cut) { first = (unsigned)k; break; }
+        if (!REFINE && best == 0.0) break;
+        double cut = best * (1.0 - kTieBandRel);
+        if constexpr (REFINE) {
+          // fp32 correlations decide nothing by themselves: every index whose
+          // fp32 |h| is within twice the rounding bound E of the fp32 maximum
+          // is a candidate, re-evaluated below in fp64.  E bounds |h32 - h64|
+          // by ecoef (a multiple of 2^-24 (log2 N + 2)) times the largest
+          // magnitude any term of the accumulation can reach: |h0_j| <= hy,
+          // the off-diagonal kernel terms goff * sum|x|, the diagonal one
+          // gamma * max|x| (identical in every warp: same shuffle tree)
+          double xs1 = 0.0, xmx = 0.0;
+          for (int q = lane; q < s; q += 32) {
+            const double2 xv = s_x[q];
+            const double ax = sqrt(xv.x * xv.x + xv.y * xv.y);
+            xs1 += ax;
+            xmx = fmax(xmx, ax);
+          }
+          xs1 = warp_sum(xs1);
+          xmx = warp_max(xmx);
+          const double e = a.ecoef * (hy + a.goff * xs1 + gamma * xmx);
+          const double lo = sqrt(best) * (1.0 - kTieBandRel) - 2.0 * e;
+          cut = lo > 0.0 ? lo * lo : -1.0;  // -1: every element qualifies
         }
-        const unsigned pick = block_min_u<false>(first, redu);  // redu: only used here
+        // own elements with |h|^2 >= cut, ascending index; f(k) returns true to stop
+        auto scan = [&](auto&& f) {
+          if (!fast_row) {
+            // only a thread whose own maximum (over these same indices k) reaches
+            // the band can hold the pick
+            const double scv = t == 1 ? 1.0 : sc;
+            if (my_best >= cut)
+              for (int k = tid; k < n; k += nth)
+                if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut && f((unsigned)k)) return;
+          } else if (regs_only) {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+              if (warp < ntiles && m2[r] >= cut && f((unsigned)(warp * 32 * RPT + lane + 32 * r)))
+                return;
+          } else if (ntiles) {
+            // several tiles per warp: only a thread whose own maximum reaches
+            // the band re-reads its own entries, in ascending index order
+            if (my_best >= cut)
+              for (int tile = warp; tile < ntiles; tile += nw)
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                  const int i = tile * 32 * RPT + lane + 32 * r;
+                  if (msc[i] >= cut && f((unsigned)i)) return;
+                }
+          } else {
+            for (int k = tid; k < n; k += nth)
+              if (msc[k] >= cut && f((unsigned)k)) return;
+          }
+        };
+        unsigned pick;
+        if constexpr (!REFINE) {
+          unsigned first = 0xffffffffu;
+          if (!fast_row) {
+            // only a thread whose own maximum (over these same indices k) reaches
+            // the band can hold the pick
+            const double scv = t == 1 ? 1.0 : sc;
+            if (my_best >= cut)
+              for (int k = tid; k < n; k += nth)
+                if (mag2(scale(buf[padx<OLOGP>(k)], scv)) >= cut) { first = (unsigned)k; break; }
+          } else if (regs_only) {
+#pragma unroll
+            for (int r = RPT - 1; r >= 0; --r)
+              if (m2[r] >= cut) first = (unsigned)(warp * 32 * RPT + lane + 32 * r);
+          } else if (ntiles) {
+            // several tiles per warp: only a thread whose own maximum reaches
+            // the band re-reads its own entries, in ascending index order
+            if (my_best >= cut)
+              for (int tile = warp; tile < ntiles && first == 0xffffffffu; tile += nw)
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                  const int i = tile * 32 * RPT + lane + 32 * r;
+                  if (msc[i] >= cut) { first = (unsigned)i; break; }
+                }
+          } else {
+            for (int k = tid; k < n; k += nth)
+              if (msc[k] >= cut) { first = (unsigned)k; break; }
+          }
+          pick = block_min_u<false>(first, redu);  // redu: only used here
+        } else {
+          scan([&](unsigned k) {
+            const int c = atomicAdd(s_ncand, 1);
+            if (c < RCAP) s_cand[c] = k;
+            return false;
+          });
+          __syncthreads();
+          const int nc = *s_ncand;
+          double best64;
+          if (nc <= RCAP) {
+            // one warp per candidate, lanes over the atoms (fixed shuffle tree)
+            for (int c = warp; c < nc; c += nw) {
+              const unsigned j = s_cand[c];
+              double ar = 0.0, ai = 0.0;
+              for (int q = lane; q < s; q += 32) {
+                const double2 xv = s_x[q];
+                const double2 g = gram<HAD>(op, j, s_lam[q]);
+                ar = fma(xv.x, g.x, fma(-xv.y, g.y, ar));
+                ai = fma(xv.x, g.y, fma(xv.y, g.x, ai));
+              }
+              ar = warp_sum(ar);
+              ai = warp_sum(ai);
+              if (lane == 0) {
+                const double2 h0j = to_c128(h0x[j]);
+                const double hr = h0j.x - ar, hi = h0j.y - ai;
+                s_cval[c] = hr * hr + hi * hi;
+              }
+            }
+            __syncthreads();
+            // the reference's rule on the fp64 values (solvers.cpp:90-101):
+            // every warp reduces the same list
+            double b = 0.0;
+            for (int c = lane; c < nc; c += 32) b = fmax(b, s_cval[c]);
+            best64 = warp_max(b);
+            const double cut64 = best64 * (1.0 - kTieBandRel);
+            unsigned f = 0xffffffffu;
+            for (int c = lane; c < nc; c += 32)
+              if (s_cval[c] >= cut64) f = min(f, s_cand[c]);
+            pick = warp_min_u(f);
+          } else {
+            // more candidates than the list holds: every thread evaluates its
+            // own qualifying elements serially (max, then first in band)
+            double b = 0.0;
+            scan([&](unsigned k) { b = fmax(b, h64_serial(k)); return false; });
+            best64 = block_max(b, red);
+            const double cut64 = best64 * (1.0 - kTieBandRel);
+            unsigned f = 0xffffffffu;
+            scan([&](unsigned k) {
+              if (h64_serial(k) >= cut64) { f = k; return true; }
+              return false;
+            });
+            pick = block_min_u(f, redu);
+          }
+          if (a.rstats && tid == 0) {
+            atomicAdd(a.rstats, 1ull);
+            atomicAdd(a.rstats + 1, (unsigned long long)nc);
+            if (nc > RCAP) atomicAdd(a.rstats + 2, 1ull);
+          }
+          if (best64 == 0.0) break;
+        }
         if (pick >= (unsigned)n) break;  // no candidate (cannot happen: the maximum is in band)
         // stagnation guard (solvers.cpp:365-367): selected-atom bitmap, no barrier
         if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
         // b_s = h0[pick], read early so its latency hides behind the row pass
-        const V bpre = buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick];
+        // (REFINE: the fp64 h0)
+        const V bpre = REFINE ? zv : (buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
+        const double2 bpre64 = REFINE ? to_c128(h0x[pick]) : make_double2(0.0, 0.0);
         mark(2);
 
         // ---- least squares: append one Gram row to W = L^{-1} (G = L L^H).
@@ -429,7 +627,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         // one reciprocal square root instead of a sqrt and per-element
         // divisions (fp64 division / sqrt are long software sequences)
         const double invd = rsqrt(d2);
-        const double2 bnew = to_c128(bpre);
+        const double2 bnew = REFINE ? bpre64 : to_c128(bpre);
         const double2 znew = make_double2((bnew.x - lzr) * invd, (bnew.y - lzi) * invd);
         // new row of W, one pass per column j < s (eight threads each; column
         // j of the packed W is contiguous): W_sj = -(1/d) sum_{i=j}^{s-1}
@@ -494,18 +692,36 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         // ---- residual and halting (solvers.cpp:388-402)
         const bool next_conv = t < T && !((int64_t)(t + 1) <= a.fast_until);
         const double r2id = yy - zz;  // ||y||^2 - ||P y||^2
-        const bool near = !(r2id > tol * tol + a.margin * yy);
-        if (next_conv || near) {
-          rn = residual_explicit(s);
-          rn_explicit = true;
-        } else {
-          rn = sqrt(fmax(r2id, 0.0));
+        if constexpr (REFINE) {
+          // halting on fp64 values: the identity (b = fp64 h0, LS in fp64)
+          // unless it is within 1e-10 ||y||^2 of tol^2, then the direct fp64
+          // residual; an fp32 r is formed only to feed a conventional row
+          if (next_conv) residual_explicit(s);
+          bool halt;
+          if (fabs(r2id - tol * tol) <= 1e-10 * yy) {
+            rn = residual64(s);
+            halt = rn <= tol;
+          } else {
+            halt = r2id <= tol * tol;
+          }
           rn_explicit = false;
+          mark(4);
+          if (halt) break;
+        } else {
+          const bool near = !(r2id > tol * tol + a.margin * yy);
+          if (next_conv || near) {
+            rn = residual_explicit(s);
+            rn_explicit = true;
+          } else {
+            rn = sqrt(fmax(r2id, 0.0));
+            rn_explicit = false;
+          }
+          mark(4);
+          if (rn_explicit && rn <= tol) break;
         }
-        mark(4);
-        if (rn_explicit && rn <= tol) break;
       }
-      if (!rn_explicit) rn = residual_explicit(s);
+      if (REFINE) rn = residual64(s);
+      else if (!rn_explicit) rn = residual_explicit(s);
       mark(4);
     }
     // ---- results (RecoveryResult, solvers.hpp:53-64)
@@ -514,6 +730,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     for (int j = tid; j < T; j += nth) {
       sup[j] = j < s ? (uint64_t)s_lam[j] + 1 : 0;
       co[j] = j < s ? s_x[j] : make_double2(0.0, 0.0);
+      if (a.modes && j >= tlast) a.modes[prob * T + j] = 0;  // rows never run
     }
     if (tid == 0) {
       a.size[prob] = (uint64_t)s;
@@ -550,7 +767,8 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
   const size_t hi_n = ((size_t)n >> p.tw_a) + ((size_t)n >> p.tw_a) / 8 + 1;
   const size_t tw = HAD ? 0 : al((lo_n + hi_n) * sizeof(V));
   const size_t small = al(3 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
-                       al(4 * (size_t)((n + 31) / 32));
+                       al(4 * (size_t)((n + 31) / 32)) +
+                       (sizeof(typename scal<V>::T) == 4 ? (size_t)12 * RCAP + 16 : 0);
   // ctas > 1: the SM's shared memory (optin + 1 KB) split between the CTAs,
   // less each CTA's 1 KB reservation and the kernel's static shared memory
   // (1936 bytes; omp_ctas_v confirms the residency with the occupancy API)
@@ -644,6 +862,15 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.phase_ws = a.phase_ws;
   k.ready = a.ready;
   k.ready_chunk = a.ready_chunk;
+  k.abort_word = a.abort_word;
+  k.h0x = a.h0x;
+  k.goff = op.goff;
+  k.rstats = a.rstats;
+  if (sizeof(typename scal<V>::T) == 4) {
+    if (!a.h0x) return cudaErrorInvalidValue;
+    // fp32 rounding bound coefficient: 8 x 2^-24 per transform level (+2)
+    k.ecoef = 8.0 * 0x1p-24 * (double)(op.log2n + 2);
+  }
   const int grid = std::max(1, a.grid);
   if constexpr (CT == 1) {
     if (p.bufg) launch_g<V, HAD, RPT, true, NT, CT>(k, p.gmode, grid, p.total, st);

@@ -629,6 +629,40 @@ cudaError_t launch_kernel_finish(const DevOp& op, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// max_{k != 0} |c_k|: non-negative doubles order like their bit patterns
+__global__ void k_gmax_off(DevOp op, unsigned long long* out) {
+  double v = 0.0;
+  for (int64_t k = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < op.n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double2 g = op.g64[k];
+    v = fmax(v, sqrt(g.x * g.x + g.y * g.y));
+  }
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
+cudaError_t launch_gmax_off(const DevOp& op, unsigned long long* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, 8, st);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = std::min<int64_t>((op.n + 255) / 256, 8 * num_sms());
+  k_gmax_off<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, st>>>(op, out);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_widen(const float* in, double* out, int64_t count, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 16 * num_sms());
+  k_widen<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, st>>>(in, out, count);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_twiddles(const DevOp& op, cudaStream_t st) {
   const int64_t blocks = (op.n + 255) / 256;
   k_twiddles<<<(unsigned)blocks, 256, 0, st>>>(op);
