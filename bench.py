@@ -80,6 +80,12 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=0)
     p.add_argument("--solver", default="omp", choices=["omp", "cosamp"],
                    help="cosamp: CoSaMP with sparsity K on the same workload (SURVEY §8 f1)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every GPU solves the config's batch; strong: the config's batch "
+                        "is split across the GPUs")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launch / sharding / timing / reporting only, no GPU work (CPU, gloo): "
+                        "exercises the multi-rank path where no GPU is present")
     a = p.parse_args()
     CFG.update(CONFIGS[a.config])
     if a.dtype:
@@ -143,18 +149,59 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
-def dist_setup():
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N ranks of this script
+    (one per GPU, RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* as torchrun sets
+    them) and wait; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rc = 0
+    for pr in procs:
+        rc = max(rc, pr.wait())
+    sys.exit(rc)
+
+
+def dist_setup(args):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+        sys.exit(2)
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if args.dry_run or not torch.cuda.is_available():
+            dist.init_process_group("gloo")
+        else:
+            # NCCL's init log names the communicator size (comm ... nRanks N)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available() and not args.dry_run:
         torch.cuda.set_device(local)
     return ws, rank, local
+
+
+def shard_of(B_total, ws, rank, scaling):
+    """(signals on this rank, first global signal index, signals over all
+    ranks): weak scaling gives every rank the config's batch (signals
+    rank * B ...), strong scaling splits the config's batch."""
+    if scaling == "weak":
+        return B_total, rank * B_total, B_total * ws
+    base, extra = divmod(B_total, ws)
+    cnt = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    return cnt, first, B_total
 
 
 def allreduce_max(x: float, ws: int) -> float:
@@ -162,7 +209,8 @@ def allreduce_max(x: float, ws: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -186,6 +234,31 @@ def problem(batch, first, threads=0):
     # the oracle and the GPU see the same (possibly fp32-rounded) measurements
     yw = Y.astype(np.complex128)
     tol = nn.copy() if CFG["noise"] > 0 else 1e-9 * np.linalg.norm(yw, axis=1)
+    return rows, Y, tol
+
+
+def problem_oracle(orc, batch, first):
+    """problem() generated by the reference's own generators through the
+    oracle library (make_row_selection / make_instance, sensing.cpp:119-153;
+    the harness's real N(0,1) instances), so the reference arm never loads
+    this package: the same bytes problem() produces (host generator pinned
+    to the reference's draws, tests/test_abi.py)."""
+    n, m, k, s = CFG["n"], CFG["m"], CFG["k"], CFG["seed"]
+    rows = orc.make_row_selection(n, m, orc.derive_seed(s, 1 << 40))
+    Y = np.zeros((batch, m), np.complex128)
+    nn = np.zeros(batch)
+    for b in range(batch):
+        seed = orc.derive_seed(s, first + b)
+        if CFG["real"]:
+            _, y = orc.make_real_instance(CFG["kind"], n, rows, k, seed)
+        else:
+            _, y, e = orc.make_instance(CFG["kind"], n, rows, k, CFG["noise"], seed)
+            nn[b] = np.linalg.norm(e)
+        Y[b] = y
+    dt = NP_DT[CFG["dtype"]]
+    Y = np.ascontiguousarray((Y.real if CFG["real"] else Y).astype(dt))
+    yw = Y.astype(np.complex128)
+    tol = nn if CFG["noise"] > 0 else 1e-9 * np.linalg.norm(yw, axis=1)
     return rows, Y, tol
 
 
@@ -244,29 +317,45 @@ def run_cpu(Y, tol, rows, sample, mode, threads):
     return len(Yw) / dt, dt, kind, res
 
 
+def workload_config(args, ws):
+    """The `config` object of BOTH arms' lines (identical, so the driver can
+    pair them): the BASELINE workload and its batch; solver choices
+    (correlation mode, switch point) are reported beside it."""
+    B, _, tot = shard_of(CFG["batch"], ws, 0, args.scaling)
+    return {"workload": CFG["name"], "batch": CFG["batch"], "signals_per_step": tot,
+            "scaling": args.scaling, "parallelism": f"batch-sharded x{ws}"}
+
+
 def reference_arm(args, ws, rank):
+    """The reference's own CPU omp_solve (oracle/_ref: its sources compiled by
+    oracle/Makefile; the C restatement if that is absent) on this host's
+    cores, on the same workload; each step is a bounded sample of the batch
+    (the first `sample` signals).  Inputs come from the reference's own
+    generators: this process never loads the CUDA package."""
     if rank != 0:
         return
     threads = cpu_threads()
     sample = args.cpu_sample or 4 * threads
-    rows, Y, tol = problem(sample, 0)
+    orc, kind = reference_oracle()
+    rows, Y, tol = problem_oracle(orc, sample, 0)
     mode = "fast"
     for _ in range(max(1, args.warmup)):
         run_cpu(Y, tol, rows, min(sample, threads), mode, threads)
-    times, kind = [], "reference"
+    times = []
     for _ in range(args.steps):
         _, dt, kind, _ = run_cpu(Y, tol, rows, sample, mode, threads)
         times.append(dt)
     value = sample * args.steps / sum(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": CFG["dtype"],
-        "data": "synthetic (seeded, SURVEY §8d)",
-        "config": {"workload": CFG["name"], "batch_per_step": sample, "mode": mode},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": CFG["dtype"],
+        "data": "synthetic (seeded, SURVEY §8d; the reference's own generators)",
+        "config": workload_config(args, ws), "mode": mode,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{sample} signals per step, Fast mode (the reference's "
-                                   f"fastest mode at this shape), one solve per host thread"},
+                         "sample": f"{sample} of the workload's signals per step (signals 0..{sample - 1}), "
+                                   f"omp_solve in Fast mode (the reference's fastest mode at this shape; "
+                                   f"supports are mode-independent), one solve per host thread"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -439,14 +528,14 @@ def our_arm(args, ws, rank, local):
     import paper_1205_4139_b200 as fmp
 
     n, m, k, T = CFG["n"], CFG["m"], CFG["k"], CFG["iters"]
-    B = CFG["batch"]
+    B, first, B_all = shard_of(CFG["batch"], ws, rank, args.scaling)
     ctx = fmp.Context(local)
     # a real (non-default) stream: handle 0 would mean "the context's own stream"
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     t0 = time.perf_counter()
-    rows, Y, tol_h = problem(B, rank * B)
+    rows, Y, tol_h = problem(B, first)
     log(f"[rank {rank}] generated {B} signals in {time.perf_counter() - t0:.1f}s")
     op = fmp.SensingOperator(CFG["kind"], n, rows, ctx)
     y_dev = torch.from_numpy(Y).to("cuda")
@@ -498,12 +587,12 @@ def our_arm(args, ws, rank, local):
         tot_ms, launches = timed(mname, fu, args.steps, args.warmup)
     tot_ms = allreduce_max(tot_ms, ws)
     ms_step = tot_ms / args.steps
-    value = B * ws / (ms_step * 1e-3)
+    value = B_all / (ms_step * 1e-3)
 
     sup = out["support"].cpu().numpy()
     iters = out["iterations"].cpu().numpy()
     ncheck = min(B, 256)
-    truth = true_supports(rank * B, ncheck)
+    truth = true_supports(first, ncheck)
     found = float(np.mean([set(truth[b]) <= set(sup[b][sup[b] > 0].tolist())
                            for b in range(ncheck)]))
 
@@ -546,9 +635,10 @@ def our_arm(args, ws, rank, local):
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = allreduce_max(float(np.median(e2e_t)), ws)
     eb = Y.dtype.itemsize
-    e2e = {"value": B * ws / e2e_s, "unit": UNIT,
+    e2e = {"value": B_all / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(B * m * eb + B * 8),
            "d2h_bytes_per_step": int(B * T * 8 + B * T * 16 + B * 8 * 3 + B * 4),
+           "per": "rank (bytes per step on each GPU)",
            "api": "fmp_omp_solve (host buffers, pinned y)",
            "timing": f"median of {E2E_STEPS} calls, wall clock around each blocking call"}
 
@@ -574,12 +664,11 @@ def our_arm(args, ws, rank, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": CFG["dtype"],
+            "scaling": args.scaling, "vs_baseline": None, "dtype": CFG["dtype"],
             "data": "synthetic (seeded, SURVEY §8d; host-generated, resident in HBM)",
-            "config": {"workload": CFG["name"], "batch_per_gpu": B, "mode": best,
-                       "fast_until": fu if fu < (1 << 40) else "inf", "mode_step_ms": per,
-                       "l2": "flushed (512 MB write) between timed steps",
-                       "parallelism": f"batch-sharded x{ws}"},
+            "config": workload_config(args, ws),
+            "mode": best, "fast_until": fu if fu < (1 << 40) else "inf", "mode_step_ms": per,
+            "batch_per_gpu": B, "l2": "flushed (512 MB write) between timed steps",
             "gpu_launches": launches, "true_support_recovered": found,
             "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
             "cpu_baseline": cpu, "c3": c3,
@@ -618,7 +707,8 @@ def cosamp_reference_arm(args, ws, rank):
         return
     threads = cpu_threads()
     sample = args.cpu_sample or max(4, min(CFG["batch"], 4 * threads))
-    rows, Y, tol = problem(sample, 0)
+    orc, _ = reference_oracle()
+    rows, Y, tol = problem_oracle(orc, sample, 0)
     mode = "fast" if args.mode in ("auto", "gpu") else args.mode
     for _ in range(max(1, args.warmup)):
         run_cpu_cosamp(Y, tol, rows, min(sample, threads), mode, threads)
@@ -629,7 +719,7 @@ def cosamp_reference_arm(args, ws, rank):
     value = sample * args.steps / sum(times)
     print(json.dumps({
         "impl": "reference", "metric": "cosamp_recoveries_per_sec", "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": CFG["dtype"], "data": "synthetic (seeded, SURVEY §8d)",
         "config": {"workload": "cosamp " + CFG["name"], "batch_per_step": sample, "mode": mode},
@@ -646,12 +736,12 @@ def cosamp_arm(args, ws, rank, local):
     import paper_1205_4139_b200 as fmp
 
     n, m, k, T = CFG["n"], CFG["m"], CFG["k"], CFG["iters"]
-    B = args.batch or CFG["batch"]
+    B, first, B_all = shard_of(CFG["batch"], ws, rank, args.scaling)
     ctx = fmp.Context(local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    rows, Y, tol_h = problem(B, rank * B)
+    rows, Y, tol_h = problem(B, first)
     op = fmp.SensingOperator(CFG["kind"], n, rows, ctx)
     y_dev = torch.from_numpy(Y).to("cuda")
     tol_dev = torch.from_numpy(tol_h).to("cuda")
@@ -684,11 +774,11 @@ def cosamp_arm(args, ws, rank, local):
     with Clocks(local) as clk:
         tot_ms, launches = timed(best, args.steps, args.warmup)
     ms_step = allreduce_max(tot_ms, ws) / args.steps
-    value = B * ws / (ms_step * 1e-3)
+    value = B_all / (ms_step * 1e-3)
     sup = out["support"].cpu().numpy()
     iters = out["iterations"].cpu().numpy()
     ncheck = min(B, 256)
-    truth = true_supports(rank * B, ncheck)
+    truth = true_supports(first, ncheck)
     found = float(np.mean([sorted(truth[b]) == sup[b][sup[b] > 0].tolist() for b in range(ncheck)]))
     fpk = ctx.fma_peak(CFG["dtype"] in ("c128", "f64"))
     achieved = cosamp_flops(iters, best == "fast", n, k) / (ms_step * 1e-3)
@@ -710,7 +800,7 @@ def cosamp_arm(args, ws, rank, local):
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = allreduce_max(float(np.median(e2e_t)), ws)
     eb = Y.dtype.itemsize
-    e2e = {"value": B * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * m * eb + B * 8),
+    e2e = {"value": B_all / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(B * m * eb + B * 8),
            "d2h_bytes_per_step": int(B * k * 24 + B * 8 * 3 + B * 4),
            "api": "fmp_cosamp_solve (host buffers, pinned y)",
            "timing": f"median of {E2E_STEPS} calls, wall clock around each blocking call"}
@@ -729,7 +819,7 @@ def cosamp_arm(args, ws, rank, local):
         print(json.dumps({
             "metric": "cosamp_recoveries_per_sec", "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": CFG["dtype"],
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": CFG["dtype"],
             "data": "synthetic (seeded, SURVEY §8d; resident in HBM)",
             "config": {"workload": "cosamp " + CFG["name"], "batch_per_gpu": B, "mode": best,
                        "mode_step_ms": per, "max_iterations": T,
@@ -741,14 +831,54 @@ def cosamp_arm(args, ws, rank, local):
         }), flush=True)
 
 
+def dry_arm(args, ws, rank):
+    """--dry-run: the multi-rank plumbing without a GPU — shard by global
+    signal index, generate this rank's signals, barrier-bracketed steps timed
+    on the host clock, max over ranks, rank 0 prints the line."""
+    B, first, B_all = shard_of(CFG["batch"], ws, rank, args.scaling)
+    _, Y, _ = problem(min(B, 8), first)  # (a small slice: plumbing only)
+    times = []
+    for _ in range(args.warmup + args.steps):
+        barrier(ws)
+        t0 = time.perf_counter()
+        float(np.abs(Y).sum())
+        barrier(ws)
+        times.append(time.perf_counter() - t0)
+    ms = allreduce_max(1e3 * float(np.mean(times[args.warmup:])), ws)
+    firsts = [first]
+    if ws > 1:
+        import torch.distributed as dist
+        firsts = [None] * ws
+        dist.all_gather_object(firsts, first)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": B_all / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": CFG["dtype"], "data": "dry run (no GPU work)", "dry_run": True,
+            "config": workload_config(args, ws), "batch_per_gpu": B, "rank_first_signal": firsts,
+        }), flush=True)
+
+
 def main():
     args = parse()
-    ws, rank, local = dist_setup()
-    if args.solver == "cosamp":
-        (cosamp_reference_arm(args, ws, rank) if args.impl == "reference"
-         else cosamp_arm(args, ws, rank, local))
-    elif args.impl == "reference":
-        reference_arm(args, ws, rank)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        spawn_ranks(args.gpus)
+    if args.impl == "reference":
+        # the reference arm is CPU only: rank 0 runs it, the others exit
+        # without work (no process group, no GPU)
+        rank = int(os.environ.get("RANK", "0"))
+        ws = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        if args.solver == "cosamp":
+            cosamp_reference_arm(args, ws, rank)
+        else:
+            reference_arm(args, ws, rank)
+        return
+    ws, rank, local = dist_setup(args)
+    if args.dry_run:
+        dry_arm(args, ws, rank)
+    elif args.solver == "cosamp":
+        cosamp_arm(args, ws, rank, local)
     elif args.config == 5:
         large_arm(args, ws, rank, local)
     else:

@@ -25,7 +25,16 @@
  *     (kernel.cpp:213-222, sensing.cpp:94,104, transform.cpp:121,138),
  *     FMP_ERANK = RankDeficientError (solvers.hpp:42-51)
  *   - handles are re-entrant per handle; use one context per host thread
- *     for concurrent work
+ *     for concurrent work.  A context's device workspaces are shared by its
+ *     calls, so calls on one context are ordered on the device: a `_dev`
+ *     call enqueued on another stream than the previous call first waits
+ *     (cudaStreamWaitEvent) for that call's work.  Independent solves that
+ *     should overlap on the device need separate contexts.
+ *   - results of the fused solvers are deterministic for a given launch
+ *     configuration but not bitwise batch-invariant: the solver's CTA shape
+ *     depends on the batch (fmp_omp_plan_info), and block reductions over a
+ *     different number of warps round differently (supports are unaffected
+ *     beyond the reference's own 1e-9 tie band)
  */
 #ifndef FMP_H
 #define FMP_H
@@ -102,6 +111,10 @@ uint64_t fmp_gpu_crossover(int kind, uint64_t n);
  * of `dtype` with max_iterations T on op (the solver's configuration depends
  * on the batch: two CTAs per SM when both fit) */
 uint64_t fmp_gpu_crossover_for(fmp_op op, int dtype, uint64_t batch, uint64_t max_iterations);
+/* the fused solver's configuration for such a solve (tests / tools):
+ * out4 = {CTAs per SM, threads per CTA, kernel table (0 global memory,
+ * 1 shared full, 2 shared conjugate half), transform buffer in global memory} */
+int fmp_omp_plan_info(fmp_op op, int dtype, uint64_t batch, uint64_t max_iterations, int* out4);
 
 /* ------------------------------------------------------ transforms (batched) */
 /* SensingOperator::apply, Phi x (sensing.cpp:93-100): x batch x n -> y batch x m */

@@ -97,6 +97,7 @@ _sig("fmp_operator_kernel", C.c_int, _vp, _vp, _vp, _vp, C.POINTER(_u64))
 _sig("fmp_crossover_iteration", _u64, C.c_int, _u64)
 _sig("fmp_gpu_crossover", _u64, C.c_int, _u64)
 _sig("fmp_gpu_crossover_for", _u64, _vp, C.c_int, _u64, _u64)
+_sig("fmp_omp_plan_info", C.c_int, _vp, C.c_int, _u64, _u64, _vp)
 _sig("fmp_apply", C.c_int, _vp, C.c_int, _vp, _u64, _vp)
 _sig("fmp_apply_dev", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
 _sig("fmp_apply_adjoint", C.c_int, _vp, C.c_int, _vp, _u64, _vp, _vp)
@@ -267,6 +268,15 @@ def gpu_crossover_for(op: "SensingOperator", dtype, batch: int, max_iterations: 
     """Switch point mode "gpu" uses for this batched solve (the solver runs two
     CTAs per SM when the batch and shared memory allow, which moves it)."""
     return int(_lib.fmp_gpu_crossover_for(op.handle, DTYPES[np.dtype(dtype)], batch, max_iterations))
+
+
+def omp_plan_info(op: "SensingOperator", dtype, batch: int, max_iterations: int) -> dict:
+    """The fused solver's configuration for a batched solve (tests / tools)."""
+    v = np.zeros(4, np.int32)
+    _check(_lib.fmp_omp_plan_info(op.handle, DTYPES[np.dtype(dtype)], batch, max_iterations, _ptr(v)))
+    return {"ctas_per_sm": int(v[0]), "threads": int(v[1]),
+            "kernel_table": ("global", "smem_full", "smem_conj_half")[int(v[2])],
+            "buffer_in_global": bool(v[3])}
 
 
 def make_row_selection(n: int, m: int, seed: int) -> np.ndarray:

@@ -104,6 +104,32 @@ struct fmp_ctx_s {
   std::mutex mu;
 };
 
+// The context mutex plus workspace ordering: the grow-only workspaces are
+// one set per context, so a call that enqueues work on stream st first waits
+// for the previous call's work if that went to another stream (use), and
+// marks the end of its own on destruction.  Calls on one stream are ordered
+// by the stream itself.
+struct CtxLock {
+  fmp_ctx_s* c;
+  std::lock_guard<std::mutex> lk;
+  cudaStream_t st = nullptr;
+  bool used = false;
+  explicit CtxLock(fmp_ctx_s* ctx) : c(ctx), lk(ctx->mu) {}
+  void use(cudaStream_t s) {
+    if (c->ws_pending && c->ws_stream != s) cudaStreamWaitEvent(s, c->ws_done, 0);
+    st = s;
+    used = true;
+  }
+  ~CtxLock() {
+    if (!used) return;
+    if (!c->ws_done && cudaEventCreateWithFlags(&c->ws_done, cudaEventDisableTiming) != cudaSuccess) return;
+    if (cudaEventRecord(c->ws_done, st) == cudaSuccess) {
+      c->ws_stream = st;
+      c->ws_pending = true;
+    }
+  }
+};
+
 struct fmp_op_s {
   fmp_ctx_s* ctx = nullptr;
   DevOp d;
@@ -156,22 +182,6 @@ int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_om
   }
   CU(fmp::launch_transform(a, st));
   g_launch_count = fmp::last_launch_count();
-  return FMP_OK;
-}
-
-// Serialise workspace users across streams: a call enqueued on stream st
-// first waits for the previous call's work if that went to another stream
-// (ws_enter), and marks its own end (ws_leave).  Calls on one stream are
-// already ordered.  Held under ctx->mu.
-int ws_enter(fmp_ctx_s* ctx, cudaStream_t st) {
-  if (ctx->ws_pending && ctx->ws_stream != st) CU(cudaStreamWaitEvent(st, ctx->ws_done, 0));
-  return FMP_OK;
-}
-int ws_leave(fmp_ctx_s* ctx, cudaStream_t st) {
-  if (!ctx->ws_done) CU(cudaEventCreateWithFlags(&ctx->ws_done, cudaEventDisableTiming));
-  CU(cudaEventRecord(ctx->ws_done, st));
-  ctx->ws_stream = st;
-  ctx->ws_pending = true;
   return FMP_OK;
 }
 
@@ -250,6 +260,14 @@ uint64_t fmp_gpu_crossover_for(fmp_op op, int dtype, uint64_t batch, uint64_t ma
   return (uint64_t)fmp::omp_gpu_fast_until(op->d, dtype, (int64_t)batch, (int64_t)max_iterations);
 }
 
+int fmp_omp_plan_info(fmp_op op, int dtype, uint64_t batch, uint64_t max_iterations, int* out4) {
+  if (!op || !out4) return fail(FMP_EINVAL, "null argument");
+  if (int s = check_dtype(op->d, dtype)) return s;
+  CU(cudaSetDevice(op->ctx->device));
+  fmp::omp_info(op->d, dtype, (int64_t)batch, (int64_t)max_iterations, out4);
+  return FMP_OK;
+}
+
 int fmp_ctx_create(int device, fmp_ctx* out) {
   if (!out) return fail(FMP_EINVAL, "null output handle");
   int count = 0;
@@ -319,7 +337,8 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
     if (i && r[i] == r[i - 1]) return fail(FMP_EINVAL, "row indices must be distinct");
   }
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
+  lk.use(ctx->cur);
   fmp_op_s* op = new fmp_op_s;
   op->ctx = ctx;
   op->rows = r;
@@ -553,11 +572,12 @@ static int transform_host(fmp_op op, int dtype, int inverse, int in_omega, int o
   if (!in || (!out && !amax)) return fail(FMP_EINVAL, "null buffer");
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   const size_t eb = fmp::elem_bytes(dtype);
   const size_t inb = batch * (in_omega ? op->d.m : op->d.n) * eb;
   const size_t outb = batch * (out_omega ? op->d.m : op->d.n) * eb;
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   void *din = nullptr, *dout = nullptr;
   uint64_t* damax = nullptr;
   if (int s = copy_in(ctx, S_IN, in, inb, &din, st)) return s;
@@ -595,8 +615,10 @@ int fmp_apply_dev(fmp_op op, int dtype, const void* x, uint64_t batch, void* y_o
   if (!op || !x || !y_out) return fail(FMP_EINVAL, "null argument");
   if (int s = check_dtype(op->d, dtype)) return s;
   CU(cudaSetDevice(op->ctx->device));
-  std::lock_guard<std::mutex> lk(op->ctx->mu);
-  return run_transform(op, dtype, 0, 0, 1, x, y_out, batch, nullptr, pick_stream(op->ctx, stream));
+  CtxLock lk(op->ctx);
+  cudaStream_t st = pick_stream(op->ctx, stream);
+  lk.use(st);
+  return run_transform(op, dtype, 0, 0, 1, x, y_out, batch, nullptr, st);
 }
 
 int fmp_apply_adjoint_dev(fmp_op op, int dtype, const void* r, uint64_t batch, void* h_out,
@@ -604,9 +626,10 @@ int fmp_apply_adjoint_dev(fmp_op op, int dtype, const void* r, uint64_t batch, v
   if (!op || !r || (!h_out && !argmax_out)) return fail(FMP_EINVAL, "null argument");
   if (int s = check_dtype(op->d, dtype)) return s;
   CU(cudaSetDevice(op->ctx->device));
-  std::lock_guard<std::mutex> lk(op->ctx->mu);
-  return run_transform(op, dtype, 1, 1, 0, r, h_out, batch, argmax_out,
-                       pick_stream(op->ctx, stream));
+  CtxLock lk(op->ctx);
+  cudaStream_t st = pick_stream(op->ctx, stream);
+  lk.use(st);
+  return run_transform(op, dtype, 1, 1, 0, r, h_out, batch, argmax_out, st);
 }
 
 // ------------------------------------------------------------ fast update
@@ -664,8 +687,9 @@ int fmp_fast_update(fmp_op op, int dtype, const void* h0, const uint64_t* suppor
   }
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   const size_t eb = fmp::elem_bytes(dtype);
   void *dh0, *dsup = nullptr, *dco = nullptr, *dout = nullptr;
   uint64_t* damax = nullptr;
@@ -693,9 +717,10 @@ int fmp_fast_update_dev(fmp_op op, int dtype, const void* h0, const uint32_t* su
   if (!h0 || (t && (!support0 || !coeffs)) || (!h_out && !argmax_out))
     return fail(FMP_EINVAL, "null buffer");
   CU(cudaSetDevice(op->ctx->device));
-  std::lock_guard<std::mutex> lk(op->ctx->mu);
-  return fast_update_dev_locked(op, dtype, h0, support0, coeffs, t, batch, h_out, argmax_out,
-                                pick_stream(op->ctx, stream));
+  CtxLock lk(op->ctx);
+  cudaStream_t st = pick_stream(op->ctx, stream);
+  lk.use(st);
+  return fast_update_dev_locked(op, dtype, h0, support0, coeffs, t, batch, h_out, argmax_out, st);
 }
 
 int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t batch,
@@ -704,8 +729,9 @@ int fmp_argmax_band(fmp_ctx ctx, int dtype, const void* h, uint64_t n, uint64_t 
   if (dtype < 0 || dtype > 3) return fail(FMP_EINVAL, "unknown dtype");
   if (n == 0) return fail(FMP_EINVAL, "empty vector");
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   void* dh;
   uint64_t* di;
   if (int s = copy_in(ctx, S_IN, h, batch * n * fmp::elem_bytes(dtype), &dh, st)) return s;
@@ -733,8 +759,9 @@ int fmp_least_squares(fmp_op op, int dtype, const void* y, const uint64_t* suppo
   if (s == 0) return FMP_OK;
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   void *dy, *dsup;
   if (int e = copy_in(ctx, S_IN, y, batch * m * fmp::elem_bytes(dtype), &dy, st)) return e;
   if (int e = copy_in(ctx, S_SUP, s0.data(), s0.size() * 4, &dsup, st)) return e;
@@ -883,8 +910,9 @@ int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
     return fail(FMP_EINVAL, "null buffer");
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = pick_stream(ctx, stream);
+  lk.use(st);
   const double* dtol = cfg->tolerances;
   if (!dtol) {
     std::vector<double> tv(batch, cfg->tolerance);
@@ -1178,8 +1206,9 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
       if (!(cfg->tolerances[b] >= 0.0)) return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
   const size_t eb = fmp::elem_bytes(dtype);
   // large batches: copies overlapped with the solve, chunk by chunk (each
@@ -1319,8 +1348,9 @@ int fmp_cosamp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch, ui
     return fail(FMP_EINVAL, "null buffer");
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = pick_stream(ctx, stream);
+  lk.use(st);
   const double* dtol = cfg->tolerances;
   if (!dtol) {
     std::vector<double> tv(batch, cfg->tolerance);
@@ -1345,8 +1375,9 @@ int fmp_cosamp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, uint64
       if (!(cfg->tolerances[b] >= 0.0)) return fail(FMP_EINVAL, "cosamp_solve: tolerance must be >= 0");
   fmp_ctx_s* ctx = op->ctx;
   CU(cudaSetDevice(ctx->device));
-  std::lock_guard<std::mutex> lk(ctx->mu);
+  CtxLock lk(ctx);
   cudaStream_t st = ctx->cur;
+  lk.use(st);
   const uint64_t T = cfg->max_iterations, n = (uint64_t)op->d.n, m = (uint64_t)op->d.m;
   const uint64_t kk = std::max<uint64_t>(k, 1);
   const size_t eb = fmp::elem_bytes(dtype);
@@ -1489,8 +1520,9 @@ uint64_t fmp_qr_cols(fmp_qr q) { return q ? (uint64_t)q->t : 0; }
 int fmp_qr_push_column(fmp_qr q, const double* col, int* accepted) {
   if (!q || !col || !accepted) return fail(FMP_EINVAL, "null argument");
   CU(cudaSetDevice(q->ctx->device));
-  std::lock_guard<std::mutex> lk(q->ctx->mu);
+  CtxLock lk(q->ctx);
   cudaStream_t st = q->ctx->cur;
+  lk.use(st);
   double o2 = 0.0;  // l2_norm(col) in the reference's order (types.cpp:32-36)
   for (int64_t i = 0; i < 2 * q->rows; ++i) o2 += col[i] * col[i];
   const double orig = std::sqrt(o2);
@@ -1522,8 +1554,9 @@ int fmp_qr_push_column(fmp_qr q, const double* col, int* accepted) {
 int fmp_qr_solve(fmp_qr q, const double* rhs, double* x_out) {
   if (!q || !rhs || (!x_out && q->t)) return fail(FMP_EINVAL, "null argument");
   CU(cudaSetDevice(q->ctx->device));
-  std::lock_guard<std::mutex> lk(q->ctx->mu);
+  CtxLock lk(q->ctx);
   cudaStream_t st = q->ctx->cur;
+  lk.use(st);
   const int t = q->t;
   if (t == 0) return FMP_OK;
   CU(cudaMemcpyAsync(q->v, rhs, (size_t)q->rows * 16, cudaMemcpyHostToDevice, st));
@@ -1755,7 +1788,8 @@ int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best)
   if (!lg || !y || !local_best) return fail(FMP_EINVAL, "null argument");
   if (!(tol >= 0.0)) return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
   CU(cudaSetDevice(lg->op->ctx->device));
-  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CtxLock lk(lg->op->ctx);
+  lk.use(lg->op->ctx->cur);
   cudaStream_t st = lg_stream(lg);
   CU(cudaMemcpyAsync(lg->y, y, lg->m * lg->eb, cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(lg->scal, 0, 16 * 8, st));
@@ -1804,7 +1838,8 @@ int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best)
 int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0_at) {
   if (!lg || !atom || !h0_at) return fail(FMP_EINVAL, "null argument");
   CU(cudaSetDevice(lg->op->ctx->device));
-  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CtxLock lk(lg->op->ctx);
+  lk.use(lg->op->ctx->cur);
   cudaStream_t st = lg_stream(lg);
   if (!(lg->first_ready && global_best == lg->first_rec[0])) {
     const double cut = global_best * (1.0 - 1e-9);  // kTieBandRel, solvers.cpp:40
@@ -1836,7 +1871,8 @@ int fmp_large_stop(fmp_large lg) {
   if (lg->done) return FMP_OK;
   lg->done = true;
   CU(cudaSetDevice(lg->op->ctx->device));
-  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CtxLock lk(lg->op->ctx);
+  lk.use(lg->op->ctx->cur);
   if (!lg->rn_explicit) {
     if (int e = lg_residual(lg, &lg->rn)) return e;
     lg->rn_explicit = true;
@@ -1854,7 +1890,8 @@ int fmp_large_stop(fmp_large lg) {
 static int lg_advance_fused(fmp_large_s* lg, uint64_t pick, const double* h0_at, int* done,
                             double* local_best) {
   cudaStream_t st = lg_stream(lg);
-  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CtxLock lk(lg->op->ctx);
+  lk.use(lg->op->ctx->cur);
   CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
                        lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
   const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
@@ -1951,7 +1988,8 @@ int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* don
   if (lg->fused && !getenv("FMP_LARGE_TWO_TRIPS")) return lg_advance_fused(lg, pick, h0_at, done, local_best);
   cudaStream_t st = lg_stream(lg);
   {
-    std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+    CtxLock lk(lg->op->ctx);
+    lk.use(lg->op->ctx->cur);
     // least squares (replicated)
     CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
                          lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
@@ -2017,7 +2055,8 @@ int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* don
     }
   }
   *done = 0;
-  std::lock_guard<std::mutex> lk(lg->op->ctx->mu);
+  CtxLock lk(lg->op->ctx);
+  lk.use(lg->op->ctx->cur);
   return lg_local_best(lg, local_best);
 }
 

@@ -191,6 +191,8 @@ int omp_grid(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 // point of FMP_MODE_GPU for it
 int omp_ctas(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
 int omp_gpu_fast_until(const DevOp& op, int dtype, int64_t batch, int64_t max_iter);
+// {CTAs per SM, threads per CTA, kernel-table mode, buffer in global memory}
+void omp_info(const DevOp& op, int dtype, int64_t batch, int64_t max_iter, int* out4);
 int fast_update_grid(const DevOp& op, int dtype, int64_t batch);
 // largest n the smem-resident transform handles for this element size
 int64_t transform_max_n(int dtype);

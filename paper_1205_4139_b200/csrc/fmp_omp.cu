@@ -10,6 +10,20 @@ cudaError_t launch_omp_f32(const OmpArgs& a, cudaStream_t st);
 int omp_ctas_c128(const DevOp& op, int64_t batch, int64_t T);
 int omp_ctas_c64(const DevOp& op, int64_t batch, int64_t T);
 
+void omp_info_c128(const DevOp& op, int64_t batch, int64_t T, int* out4);
+void omp_info_c64(const DevOp& op, int64_t batch, int64_t T, int* out4);
+void omp_info_f64(const DevOp& op, int64_t batch, int64_t T, int* out4);
+void omp_info_f32(const DevOp& op, int64_t batch, int64_t T, int* out4);
+
+void omp_info(const DevOp& op, int dtype, int64_t batch, int64_t T, int* out4) {
+  switch (dtype) {
+    case C128: omp_info_c128(op, batch, T, out4); break;
+    case C64: omp_info_c64(op, batch, T, out4); break;
+    case F64: omp_info_f64(op, batch, T, out4); break;
+    default: omp_info_f32(op, batch, T, out4); break;
+  }
+}
+
 int omp_ctas(const DevOp& op, int dtype, int64_t batch, int64_t T) {
   switch (dtype) {
     case C128: return omp_ctas_c128(op, batch, T);

@@ -8,4 +8,8 @@ cudaError_t launch_omp_c64(const OmpArgs& a, cudaStream_t st) {
 int omp_ctas_c64(const DevOp& op, int64_t batch, int64_t T) {
   return op.kind == HADAMARD ? 1 : omp_ctas_v<float2, false>(op, batch, T);
 }
+void omp_info_c64(const DevOp& op, int64_t batch, int64_t T, int* out4) {
+  if (op.kind == HADAMARD) omp_info_v<float2, true>(op, batch, T, out4);
+  else omp_info_v<float2, false>(op, batch, T, out4);
+}
 }  // namespace fmp

@@ -5,4 +5,7 @@ namespace fmp {
 cudaError_t launch_omp_f32(const OmpArgs& a, cudaStream_t st) {
   return launch_omp_v<float, true>(a, st);
 }
+void omp_info_f32(const DevOp& op, int64_t batch, int64_t T, int* out4) {
+  omp_info_v<float, true>(op, batch, T, out4);
+}
 }  // namespace fmp

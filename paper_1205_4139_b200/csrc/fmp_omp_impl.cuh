@@ -905,6 +905,22 @@ int omp_ctas_v(const DevOp& op, int64_t batch, int64_t T) {
   return occ >= 2 ? 2 : 1;
 }
 
+// the configuration launch_omp_v picks: CTAs per SM, threads per CTA, kernel
+// table mode (0 global, 1 smem full, 2 smem conjugate half), buffer in global
+template <class V, bool HAD>
+void omp_info_v(const DevOp& op, int64_t batch, int64_t T, int* out4) {
+  int ctas = 1;
+  if constexpr (!HAD && sizeof(V) >= 8) ctas = omp_ctas_v<V, HAD>(op, batch, T);
+  int nt = ctas == 2 ? 256 : OMP_THREADS;
+  const char* e = getenv("FMP_OMP_NT");
+  if (ctas == 1 && op.n == 32 * 8 * 4 && batch <= num_sms() && !(e && atoi(e) == 512)) nt = 128;
+  const OmpPlan p = omp_plan<V, HAD>(op, T, ctas);
+  out4[0] = ctas;
+  out4[1] = nt;
+  out4[2] = p.gmode;
+  out4[3] = p.bufg ? 1 : 0;
+}
+
 template <class V, bool HAD>
 cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
   if constexpr (!HAD && sizeof(V) >= 8) {

@@ -420,16 +420,6 @@ def test_omp_config4_shape(fmp, oracle, dtype, tol):
     assert agree == B
 
 
-@pytest.mark.slow
-def test_omp_config4_c64_support_agreement_at_scale(fmp, oracle):
-    # fp32 rounding vs the fp64 oracle's 1e-9 tie band: measured agreement
-    import subprocess, sys, os
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, os.path.join(root, "tools", "fp32_agreement.py"), "16"],
-                         capture_output=True, text=True, timeout=900).stdout
-    assert "c64 support agreement 16 / 16" in out, out
-
-
 def test_omp_host_chunked_equals_device(fmp, oracle):
     # batches >= 8 x grid take a copy/compute-overlapped host path (with the
     # wrapper's page-locked results: fmp_capi.cu omp_host_streamed, one launch
