@@ -1023,7 +1023,10 @@ static int stream_in_chunks(fmp_ctx_s* ctx, const void* y, uint64_t batch, size_
   char* pin_in = (char*)ctx->pinned;
   const int* one = (const int*)((char*)ctx->pinned + in_bytes);
   const uint64_t nchunk = (batch + per - 1) / per;
+  // test hook: the host side fails after the first chunk (error-path test)
+  const char* stall = getenv("FMP_TEST_STALL_INPUT");
   for (uint64_t c = 0; c < nchunk; ++c) {
+    if (c == 1 && stall && *stall == '1') return fail(FMP_ECUDA, "input stream failed (test hook)");
     const uint64_t b0 = c * per, nb = std::min(per, batch - b0);
     const char* src = (const char*)y + b0 * row_bytes;
     if (stage_in) {  // overlaps the solve and the previous chunk's transfer

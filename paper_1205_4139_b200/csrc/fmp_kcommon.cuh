@@ -25,16 +25,20 @@ namespace {
 __device__ __forceinline__ bool wait_ready(const int* flag, const volatile int* abort_word) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (unsigned spin = 0;; ++spin) {
+  // the abort word lives in host memory: a read crosses PCIe and competes
+  // with the input copies, so it is polled once per millisecond of waiting
+  unsigned long long next_poll = t0 + 1000000ull;
+  for (;;) {
     int v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     if (v) return true;
     __nanosleep(500);
-    if ((spin & 63) == 63) {  // the abort word lives in host memory: poll it sparingly
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t >= next_poll) {
       if (abort_word && *abort_word) return false;
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 60000000000ull) return false;
+      next_poll = t + 1000000ull;
     }
   }
 }

@@ -492,3 +492,37 @@ def test_omp_host_chunked_pageable_buffers(fmp):
     assert np.array_equal(sup, ref.support) and np.array_equal(co, ref.coeffs)
     assert np.array_equal(sz, ref.support_size) and np.array_equal(it, ref.iterations)
     assert np.array_equal(rn, ref.residual) and np.array_equal(ab.astype(bool), ref.aborted)
+
+
+@pytest.mark.parametrize("solver", ["omp", "cosamp"])
+def test_streamed_input_failure_leaves_context_usable(fmp, oracle, solver):
+    """The host-buffer solve that streams its input into a running kernel:
+    when the host side fails mid-stream (test hook), the abort word releases
+    the kernel (no trap, no hang), the call reports the error, and the same
+    context solves correctly afterwards."""
+    n, m, k, B = 1024, 256, 12, 1600  # >= 8 x grid: the streamed path
+    rows = fmp.make_row_selection(n, m, 41)
+    op = fmp.SensingOperator("fourier", n, rows)
+    Y, _, _ = fmp.make_batch("fourier", n, rows, k, B, base_seed=41)
+    tol = 1e-9 * np.linalg.norm(Y, axis=1)
+    cfg = fmp.SolveConfig(k, 0.0, "fast")
+
+    def solve():
+        if solver == "omp":
+            return fmp.omp_solve_batch(op, Y, cfg, tolerances=tol)
+        return fmp.cosamp_solve_batch(op, Y, k, cfg, tolerances=tol, want_history=False)
+    os.environ["FMP_TEST_STALL_INPUT"] = "1"
+    try:
+        with pytest.raises(Exception):
+            solve()
+    finally:
+        del os.environ["FMP_TEST_STALL_INPUT"]
+    res = solve()
+    for b in (0, B // 2, B - 1):
+        s = int(res.support_size[b])
+        if solver == "omp":
+            r = oracle.omp_solve("fourier", n, rows, Y[b], k, tol[b], "fast")
+            assert [int(v) for v in res.support[b, :s]] == [int(v) for v in r.support]
+        else:
+            r, _ = oracle.cosamp_solve("fourier", n, rows, Y[b], k, k, tol[b], "fast")
+            assert [int(v) for v in res.support[b, :s]] == [int(v) for v in r.support]
