@@ -446,21 +446,19 @@ def large_arm(args, ws, rank, local):
     log(f"[rank {rank}] generated the signal in {time.perf_counter() - t0:.1f}s")
     op = fmp.SensingOperator(CFG["kind"], n, rows, ctx)
     y = Y[0]
-    exchange = None
-    if ws > 1:
-        from paper_1205_4139_b200.dist import TorchExchange
-        exchange = TorchExchange()
     mode = "adaptive" if args.mode == "auto" else args.mode
     mname, fu = parse_mode(mode, n, CFG["kind"])
     cfg = fmp.SolveConfig(T, float(tol_h[0]), mname, fast_until=fu)
+    # one shard per GPU; NCCL between the ranks (the unique id travels over
+    # torch.distributed), the exchanges inside fmp_large_group_solve
+    comm = None
+    if ws > 1:
+        from paper_1205_4139_b200.dist import nccl_comm
+        comm = nccl_comm(local)
+    shard = fmp.LargeShard(op, cfg, rank, ws, dtype=NP_DT[CFG["dtype"]], comm=comm)
 
     def solve():
-        if ws == 1:  # one shard: the whole loop in C (fmp_large_solve)
-            return fmp.large_solve(op, y, cfg, dtype=NP_DT[CFG["dtype"]])
-        shard = fmp.LargeShard(op, cfg, rank, ws, dtype=NP_DT[CFG["dtype"]])
-        res = fmp.sharded_solve([shard], y, float(tol_h[0]), exchange)
-        shard.close()
-        return res
+        return fmp.sharded_solve([shard], y, float(tol_h[0]))
 
     for _ in range(max(1, args.warmup)):
         res = solve()

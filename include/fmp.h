@@ -233,37 +233,56 @@ int fmp_phase_cycles(fmp_ctx ctx, double* out6);
 int fmp_refine_stats(fmp_ctx ctx, double* out3);
 
 /* ------------------------------------------- sharded single-signal solver */
-/* omp_solve for ONE large signal spread over `nshards` GPUs (config 5).
- * Shard p owns the correlation entries k = p + nshards * k' (1-based atom
- * k + 1).  Each iteration the caller exchanges two things between shards:
- *   1. best = max over shards of fmp_large's local best |h|^2
- *   2. pick = min over shards of fmp_large_first(best) (0 = none on that
- *      shard), together with h0 at pick from the owning shard
- * then calls fmp_large_advance(pick, h0) on every shard.  Least squares is
- * replicated (bit-identical on every shard).  The identification rule is the
- * reference's band argmax (solvers.cpp:90-101) evaluated globally.
- * fmp_large_solve runs the whole loop for nshards = 1.  Fourier only. */
+/* omp_solve (solvers.cpp:296-411) for ONE large signal spread over `nshards`
+ * shards, one per GPU (config 5).  Shard p owns the correlation entries
+ * k = p + nshards * k' (1-based atom k + 1): its fast rows read its class of
+ * the kernel, its conventional rows are (N / nshards)-point transforms of the
+ * residual folded into its class, and the residual is the sum over shards of
+ * their atoms' forward transforms.  Per iteration the shards exchange one
+ * identification record (all-gather of at most 64 candidates re-evaluated in
+ * fp64; fmp_large_merge_records is the rule) and, before a conventional row,
+ * one M-vector (all-reduce sum); least squares is replicated bit-identically.
+ * Picks and coefficients do not depend on nshards.  Fourier only.
+ *
+ * Exchanges run on the device: through NCCL when every shard of the group
+ * has a communicator (one rank per shard: fmp_comm_init_rank across
+ * processes, fmp_comm_init_all for several GPUs in one process), else
+ * between shards of one process on one GPU (emulation: all nshards shards
+ * passed to one fmp_large_group_solve call).  The host synchronises once per
+ * iteration on the previous iteration's decisions (halting, rank deficiency)
+ * while the device already computes the next correlation. */
+typedef struct fmp_comm_s* fmp_comm;
+/* NCCL (libnccl.so.2, loaded at first use): a 128-byte unique id made on one
+ * rank and shared with the others (any transport), then one communicator
+ * per rank on `device` */
+int fmp_comm_unique_id(void* id128);
+int fmp_comm_init_rank(int device, int nranks, int rank, const void* id128, fmp_comm* out);
+/* n communicators of one process, rank i on devices[i] */
+int fmp_comm_init_all(const int* devices, int n, fmp_comm* out);
+int fmp_comm_destroy(fmp_comm comm);
+
 typedef struct fmp_large_s* fmp_large;
+/* comm: this shard's communicator, or NULL (nshards == 1, or emulation) */
 int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
-                     const fmp_omp_config* cfg, fmp_large* out);
+                     const fmp_omp_config* cfg, fmp_comm comm, fmp_large* out);
 int fmp_large_destroy(fmp_large lg);
-/* y: m values (host); *local_best: max |h_1|^2 of this shard (t = 1), or -1
- * when ||y|| <= tol (no iterations) */
-int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best);
-/* first 1-based atom of this shard with |h|^2 >= global_best (1 - 1e-9), or 0;
- * h0_at (2 doubles) receives h0 there */
-int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0_at);
-/* append `atom` (1-based; h0_at its h0), least squares, residual, halting and
- * the next correlation; *done = 1 when the solve has ended; *local_best as in
- * fmp_large_begin for the next iteration */
-int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* done,
-                      double* local_best);
-/* end the solve without appending (zero correlation or a repeated atom) */
-int fmp_large_stop(fmp_large lg);
+/* solve with the `count` shards of this process (all nshards for emulation or
+ * one process over several GPUs, one per process with NCCL across
+ * processes); y: m values (host), tol: absolute residual tolerance */
+int fmp_large_group_solve(fmp_large* shards, int count, const void* y, double tol);
 int fmp_large_result(fmp_large lg, uint64_t* support, double* coeffs, uint64_t* support_size,
                      uint64_t* iterations, double* residual, int32_t* aborted);
+/* the whole solve on one GPU (nshards = 1) */
 int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* cfg,
                     fmp_omp_result* out);
+/* the record merge every shard runs after the all-gather (host twin of the
+ * device kernel, for tests): `recs` = nshards records of
+ * fmp_large_record_size() bytes, `selbits` the selected-atom bitmap (or
+ * NULL); out4 = {atom (0-based, as double), best |h|^2, flags, 0} with flags
+ * 1 zero correlation, 2 stagnation, 4 a record overflowed (exact fallback),
+ * 8 more candidates than a shard evaluates */
+int fmp_large_record_size(void);
+int fmp_large_merge_records(const void* recs, int nshards, const uint32_t* selbits, double* out4);
 
 /* ------------------------------------------------------ instance generation */
 /* seeded synthetic problems for the bench / parity harness, following the

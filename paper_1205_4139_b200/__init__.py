@@ -119,13 +119,16 @@ _sig("fmp_qr_destroy", C.c_int, _vp)
 _sig("fmp_qr_push_column", C.c_int, _vp, _vp, C.POINTER(C.c_int))
 _sig("fmp_qr_solve", C.c_int, _vp, _vp, _vp)
 _sig("fmp_qr_cols", _u64, _vp)
-_sig("fmp_large_create", C.c_int, _vp, C.c_int, _u64, _u64, C.POINTER(OmpConfig), C.POINTER(_vp))
+_sig("fmp_comm_unique_id", C.c_int, _vp)
+_sig("fmp_comm_init_rank", C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.POINTER(_vp))
+_sig("fmp_comm_init_all", C.c_int, _vp, C.c_int, _vp)
+_sig("fmp_comm_destroy", C.c_int, _vp)
+_sig("fmp_large_create", C.c_int, _vp, C.c_int, _u64, _u64, C.POINTER(OmpConfig), _vp, C.POINTER(_vp))
 _sig("fmp_large_destroy", C.c_int, _vp)
-_sig("fmp_large_begin", C.c_int, _vp, _vp, C.c_double, C.POINTER(C.c_double))
-_sig("fmp_large_first", C.c_int, _vp, C.c_double, C.POINTER(_u64), _vp)
-_sig("fmp_large_advance", C.c_int, _vp, _u64, _vp, C.POINTER(C.c_int), C.POINTER(C.c_double))
-_sig("fmp_large_stop", C.c_int, _vp)
+_sig("fmp_large_group_solve", C.c_int, _vp, C.c_int, _vp, C.c_double)
 _sig("fmp_large_result", C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp)
+_sig("fmp_large_record_size", C.c_int)
+_sig("fmp_large_merge_records", C.c_int, _vp, C.c_int, _vp, _vp)
 _sig("fmp_large_solve", C.c_int, _vp, C.c_int, _vp, C.POINTER(OmpConfig), C.POINTER(OmpResult))
 _sig("fmp_least_squares", C.c_int, _vp, C.c_int, _vp, _vp, _u64, _u64, _vp, C.POINTER(C.c_int64))
 _sig("fmp_make_row_selection", C.c_int, _u64, _u64, _u64, _vp)
@@ -768,18 +771,53 @@ class IncrementalQR:
 
 
 # ------------------------------------------- sharded single-signal solver
+class Comm:
+    """An NCCL communicator for one shard (fmp_comm_*)."""
+
+    def __init__(self, handle, nranks: int, rank: int):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _check(_lib.fmp_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def init_rank(cls, device: int, nranks: int, rank: int, uid: bytes) -> "Comm":
+        h = _vp()
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        _check(_lib.fmp_comm_init_rank(int(device), int(nranks), int(rank), buf, C.byref(h)))
+        return cls(h, nranks, rank)
+
+    @classmethod
+    def init_all(cls, devices) -> list:
+        devs = (C.c_int * len(devices))(*devices)
+        hs = (_vp * len(devices))()
+        _check(_lib.fmp_comm_init_all(devs, len(devices), hs))
+        return [cls(hs[i], len(devices), i) for i in range(len(devices))]
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.fmp_comm_destroy(self.handle)
+            self.handle = None
+
+
 class LargeShard:
     """Shard p of P of the config-5 solver (fmp_large_*): correlation entries
-    k = p + P k' live here; least squares is replicated."""
+    k = p + P k' live here; least squares is replicated.  `comm`: this shard's
+    NCCL communicator (one rank per GPU), or None for P = 1 and for shards
+    emulated on one GPU (all P passed to one sharded_solve call)."""
 
     def __init__(self, op: SensingOperator, cfg: SolveConfig, shard: int = 0, nshards: int = 1,
-                 dtype=np.complex64):
+                 dtype=np.complex64, comm: Optional[Comm] = None):
         self.op = op
         self.dtype = np.dtype(dtype)
+        self.comm = comm
         c = _config(cfg)
         h = _vp()
         _check(_lib.fmp_large_create(op.handle, DTYPES[self.dtype], shard, nshards, C.byref(c),
-                                     C.byref(h)))
+                                     comm.handle if comm is not None else None, C.byref(h)))
         self.handle = h
         self.T = int(cfg.max_iterations)
 
@@ -794,29 +832,6 @@ class LargeShard:
         except Exception:
             pass
 
-    def begin(self, y, tol: float) -> float:
-        y = np.ascontiguousarray(np.asarray(y, self.dtype))
-        self._y = y
-        b = C.c_double(0)
-        _check(_lib.fmp_large_begin(self.handle, _ptr(y), float(tol), C.byref(b)))
-        return b.value
-
-    def first(self, best: float):
-        a = _u64(0)
-        h = np.zeros(2)
-        _check(_lib.fmp_large_first(self.handle, float(best), C.byref(a), _ptr(h)))
-        return int(a.value), complex(h[0], h[1])
-
-    def advance(self, atom: int, h0: complex):
-        h = np.array([h0.real, h0.imag])
-        d = C.c_int(0)
-        b = C.c_double(0)
-        _check(_lib.fmp_large_advance(self.handle, int(atom), _ptr(h), C.byref(d), C.byref(b)))
-        return bool(d.value), b.value
-
-    def stop(self):
-        _check(_lib.fmp_large_stop(self.handle))
-
     def result(self):
         sup = np.zeros(self.T, np.uint64)
         co = np.zeros(self.T, np.complex128)
@@ -829,38 +844,48 @@ class LargeShard:
         return sup[:s].copy(), co[:s].copy(), int(it.value), rn.value, bool(ab.value)
 
 
-class LocalExchange:
-    """In-process exchange for shards emulated on one device (tests)."""
-
-    def max(self, values):
-        return max(values)
-
-    def first(self, atoms):
-        cands = [(a, h) for a, h in atoms if a > 0]
-        return min(cands, key=lambda ah: ah[0]) if cands else (0, 0j)
-
-
-def sharded_solve(shards, y, tol: float, exchange=None):
-    """Drive shards through one solve (identification = the reference's band
-    argmax over the union of the shards, solvers.cpp:90-101).  `shards` holds
-    the local shard objects (all P of them when emulating on one device, one
-    per process otherwise with a distributed `exchange`)."""
-    ex = exchange or LocalExchange()
-    bests = [sh.begin(y, tol) for sh in shards]
-    best = ex.max(bests)
-    if best < 0:  # ||y|| <= tol: no iterations
-        return shards[0].result()
-    while True:
-        if best == 0.0:
-            for sh in shards:
-                sh.stop()
-            break
-        atom, h0 = ex.first([sh.first(best) for sh in shards])
-        outs = [sh.advance(atom, h0) for sh in shards]
-        if any(d for d, _ in outs):
-            break
-        best = ex.max([b for _, b in outs])
+def sharded_solve(shards, y, tol: float):
+    """One solve over the local shards (fmp_large_group_solve): all P of them
+    when emulating on one GPU, this process's shard(s) with NCCL otherwise.
+    Returns (support, coeffs, iterations, residual_norm, aborted)."""
+    y = np.ascontiguousarray(np.asarray(y, shards[0].dtype))
+    hs = (_vp * len(shards))(*[sh.handle for sh in shards])
+    _check(_lib.fmp_large_group_solve(hs, len(shards), _ptr(y), float(tol)))
     return shards[0].result()
+
+
+RECORD_BYTES = int(_lib.fmp_large_record_size())
+RECORD_CANDIDATES = (RECORD_BYTES - 16) // 16
+
+
+def make_record(best32: float, cands) -> bytes:
+    """One shard's identification record (fmp_kernels.cuh LgRec): its best
+    working-precision |h|^2 and its (global atom 0-based, fp64 |h|^2)
+    candidates; more than RECORD_CANDIDATES sets the overflow count."""
+    buf = np.zeros(RECORD_BYTES, np.uint8)
+    buf[:8] = np.frombuffer(np.float64(best32).tobytes(), np.uint8)
+    buf[8:12] = np.frombuffer(np.uint32(len(cands)).tobytes(), np.uint8)
+    for i, (j, m64) in enumerate(cands[:RECORD_CANDIDATES]):
+        o = 16 + 16 * i
+        buf[o:o + 8] = np.frombuffer(np.uint64(j).tobytes(), np.uint8)
+        buf[o + 8:o + 16] = np.frombuffer(np.float64(m64).tobytes(), np.uint8)
+    return buf.tobytes()
+
+
+def merge_records(records, selected=None, n: int = 0) -> dict:
+    """The merge every shard runs after the all-gather of records
+    (fmp_large_merge_records; the device kernel's host twin)."""
+    blob = np.frombuffer(b"".join(records), np.uint8).copy()
+    sel = None
+    if selected is not None:
+        bits = np.zeros((n + 31) // 32, np.uint32)
+        for a in selected:
+            bits[a >> 5] |= np.uint32(1 << (a & 31))
+        sel = bits
+    out = np.zeros(4)
+    _check(_lib.fmp_large_merge_records(_ptr(blob), len(records), _ptr(sel) if sel is not None else None,
+                                        _ptr(out)))
+    return {"atom": int(out[0]) if out[0] >= 0 else None, "best64": float(out[1]), "flags": int(out[2])}
 
 
 def large_solve(op: SensingOperator, y, cfg: SolveConfig, dtype=np.complex64):

@@ -28,8 +28,8 @@ CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"), *DEFS]
-SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_cosamp.cu", "fmp_large.cu", "fmp_fast_update.cu", "fmp_qr.cu", "fmp_transform.cu", "fmp_transform_4s.cu", "fmp_transform_fold.cu", "fmp_capi.cu", "fmp_gen.cu", "fmp_host_gen.cpp"]
-HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh"]
+SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.cu", "fmp_omp.cu", "fmp_cosamp.cu", "fmp_large.cu", "fmp_large_host.cu", "fmp_fast_update.cu", "fmp_qr.cu", "fmp_transform.cu", "fmp_transform_4s.cu", "fmp_transform_fold.cu", "fmp_capi.cu", "fmp_gen.cu", "fmp_host_gen.cpp"]
+HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh", "fmp_capi_internal.cuh"]
 
 
 def _newest_dep() -> float:
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -17,181 +17,18 @@
 #include <vector>
 
 #include "fmp.h"
+#include "fmp_capi_internal.cuh"
 #include "fmp_kernels.cuh"
 
 using fmp::DevOp;
+using namespace fmpi;
 
-namespace {
-
+namespace fmpi {
 thread_local std::string g_err;
 int g_phase_prof = 0;
 thread_local int g_launch_count = 0;
+}  // namespace fmpi
 
-int fail(int code, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
-  g_err = buf;
-  return code;
-}
-
-#define CU(expr)                                                                   \
-  do {                                                                             \
-    cudaError_t e_ = (expr);                                                       \
-    if (e_ != cudaSuccess)                                                         \
-      return fail(e_ == cudaErrorMemoryAllocation ? FMP_ENOMEM : FMP_ECUDA,        \
-                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-
-bool pow2(uint64_t n) { return n && !(n & (n - 1)); }
-int ilog2(uint64_t n) {
-  int p = 0;
-  while (n >>= 1) ++p;
-  return p;
-}
-
-// grow-only device scratch, one buffer per slot
-struct Workspace {
-  std::vector<std::pair<void*, size_t>> slot;
-  void* get(int i, size_t bytes, cudaError_t* err) {
-    if ((int)slot.size() <= i) slot.resize(i + 1, {nullptr, 0});
-    bytes = std::max<size_t>(bytes, 256);
-    if (slot[i].second < bytes) {
-      if (slot[i].first) cudaFree(slot[i].first);
-      slot[i] = {nullptr, 0};
-      void* p = nullptr;
-      *err = cudaMalloc(&p, bytes);
-      if (*err != cudaSuccess) return nullptr;
-      slot[i] = {p, bytes};
-    }
-    return slot[i].first;
-  }
-  ~Workspace() {
-    for (auto& s : slot)
-      if (s.first) cudaFree(s.first);
-  }
-};
-
-enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
-            S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
-            S_OHSUP, S_Y64, S_H0X, S_GOFF, S_RST,
-            S_ALT = 64 };  // S_ALT + slot: the alternate per-CTA workspace set
-
-}  // namespace
-
-struct fmp_ctx_s {
-  int device = 0;
-  cudaStream_t own = nullptr;
-  cudaStream_t cur = nullptr;
-  cudaStream_t copy = nullptr;        // host<->device copies overlapped with solves (lazy)
-  cudaStream_t alt = nullptr;         // second compute stream (lazy)
-  void* pinned = nullptr;             // page-locked staging for pageable host buffers (lazy)
-  size_t pinned_bytes = 0;
-  std::vector<cudaEvent_t> events;    // chunk hand-offs between the two streams (lazy)
-  // abort word of the streamed-input paths: page-locked, mapped into the
-  // device address space; the host raises it on an error path so a kernel
-  // spinning on ready flags returns without any further CUDA call (lazy)
-  int* abort_host = nullptr;
-  const volatile int* abort_dev = nullptr;
-  // the workspaces are one set per context: a call on another stream waits
-  // for the last call that used them (ws_done, recorded on ws_stream)
-  cudaEvent_t ws_done = nullptr;
-  cudaStream_t ws_stream = nullptr;
-  bool ws_pending = false;
-  Workspace ws;
-  std::mutex mu;
-};
-
-// The context mutex plus workspace ordering: the grow-only workspaces are
-// one set per context, so a call that enqueues work on stream st first waits
-// for the previous call's work if that went to another stream (use), and
-// marks the end of its own on destruction.  Calls on one stream are ordered
-// by the stream itself.
-struct CtxLock {
-  fmp_ctx_s* c;
-  std::lock_guard<std::mutex> lk;
-  cudaStream_t st = nullptr;
-  bool used = false;
-  explicit CtxLock(fmp_ctx_s* ctx) : c(ctx), lk(ctx->mu) {}
-  void use(cudaStream_t s) {
-    if (c->ws_pending && c->ws_stream != s) cudaStreamWaitEvent(s, c->ws_done, 0);
-    st = s;
-    used = true;
-  }
-  ~CtxLock() {
-    if (!used) return;
-    if (!c->ws_done && cudaEventCreateWithFlags(&c->ws_done, cudaEventDisableTiming) != cudaSuccess) return;
-    if (cudaEventRecord(c->ws_done, st) == cudaSuccess) {
-      c->ws_stream = st;
-      c->ws_pending = true;
-    }
-  }
-};
-
-struct fmp_op_s {
-  fmp_ctx_s* ctx = nullptr;
-  DevOp d;
-  std::vector<uint64_t> rows;  // sorted, 1-based
-};
-
-namespace {
-
-#define ALLOC(var, slot, bytes)                                       \
-  do {                                                                \
-    cudaError_t e_ = cudaSuccess;                                     \
-    var = (std::remove_reference_t<decltype(var)>)ctx->ws.get(slot, (bytes), &e_);             \
-    if (!var) return fail(FMP_ENOMEM, "device workspace (%zu bytes): %s", \
-                          (size_t)(bytes), cudaGetErrorString(e_));   \
-  } while (0)
-
-int check_dtype(const DevOp& d, int dtype) {
-  if (dtype < 0 || dtype > 3) return fail(FMP_EINVAL, "unknown dtype %d", dtype);
-  if (d.kind == fmp::FOURIER && !fmp::is_complex(dtype))
-    return fail(FMP_EINVAL, "real dtypes need a Hadamard operator");
-  return FMP_OK;
-}
-
-cudaStream_t pick_stream(fmp_ctx_s* ctx, void* s) {
-  return s ? (cudaStream_t)s : ctx->cur;
-}
-
-// batched transform on device pointers
-int run_transform(fmp_op_s* op, int dtype, int inverse, int in_omega, int out_omega,
-                  const void* in, void* out, uint64_t batch, uint64_t* amax, cudaStream_t st,
-                  int slot_off = 0) {
-  fmp_ctx_s* ctx = op->ctx;
-  fmp::TransformArgs a{};
-  a.op = &op->d;
-  a.dtype = dtype;
-  a.inverse = inverse;
-  a.in_omega = in_omega;
-  a.out_omega = out_omega;
-  a.in = in;
-  a.out = out;
-  a.batch = (int64_t)batch;
-  a.argmax_out = amax;
-  if (op->d.n > fmp::transform_max_n(dtype)) {
-    void* w;
-    ALLOC(w, slot_off + S_WORK, (size_t)batch * op->d.n * fmp::elem_bytes(dtype));
-    a.work = w;
-    int* sy;
-    ALLOC(sy, slot_off + S_SYNC, (32 + batch) * sizeof(int));
-    a.sync = sy;
-  }
-  CU(fmp::launch_transform(a, st));
-  g_launch_count = fmp::last_launch_count();
-  return FMP_OK;
-}
-
-int copy_in(fmp_ctx_s* ctx, int slot, const void* host, size_t bytes, void** dev, cudaStream_t st) {
-  ALLOC(*dev, slot, bytes);
-  CU(cudaMemcpyAsync(*dev, host, bytes, cudaMemcpyHostToDevice, st));
-  return FMP_OK;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -1574,533 +1411,6 @@ int fmp_qr_solve(fmp_qr q, const double* rhs, double* x_out) {
   }
   std::memcpy(x_out, x.data(), (size_t)t * 16);
   return FMP_OK;
-}
-
-}  // extern "C"
-
-// ===================================================== sharded single signal
-struct fmp_large_s {
-  fmp_op_s* op = nullptr;
-  int dtype = FMP_C64;
-  int P = 1, p = 0;
-  int64_t n = 0, m = 0, np = 0;
-  int T = 1;
-  int64_t fast_until = 0;
-  size_t eb = 8;
-  // device
-  void *h0s = nullptr, *hs = nullptr, *gcm = nullptr, *hfull = nullptr, *xdense = nullptr;
-  void *ax = nullptr, *r = nullptr, *y = nullptr, *xn = nullptr;
-  double2 *W = nullptr, *x = nullptr, *z = nullptr, *l = nullptr;
-  uint32_t* lam = nullptr;
-  double *part = nullptr, *scal = nullptr, *blkmax = nullptr, *dval = nullptr;
-  unsigned long long* dfirst = nullptr;
-  double* drec = nullptr;  // pick record (k_lg_pick)
-  bool own_gcm = false;
-  // one shard (fmp_large_solve): the first-in-band pick rides along with the
-  // local best, cut on the device (fewer host round trips per iteration)
-  bool fused = false, first_ready = false;
-  double first_rec[4] = {0, 0, 0, 0};
-  // host state (mirrors omp_solve's loop variables, solvers.cpp:306-403)
-  int t = 0, s = 0, iters = 0, aborted = 0;
-  double yy = 0, tol = 0, rn = 0;
-  bool rn_explicit = true, done = true;
-  int view = 0;  // 0: h0s (t = 1), 1: hs (fast row), 2: hfull strided (conventional row)
-  std::vector<uint64_t> support;  // 0-based atoms in selection order
-  std::vector<uint8_t> sel;
-  std::vector<void*> allocs;
-};
-
-namespace {
-
-int lg_alloc(fmp_large_s* lg, void** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 256));
-  if (e != cudaSuccess) return fail(FMP_ENOMEM, "large solver alloc (%zu bytes): %s", bytes,
-                                    cudaGetErrorString(e));
-  lg->allocs.push_back(*p);
-  return FMP_OK;
-}
-
-cudaStream_t lg_stream(fmp_large_s* lg) { return lg->op->ctx->cur; }
-
-// current correlation view of this shard
-void lg_view(fmp_large_s* lg, const void** base, int64_t* off, int64_t* stride) {
-  if (lg->view == 0) { *base = lg->h0s; *off = 0; *stride = 1; }
-  else if (lg->view == 1) { *base = lg->hs; *off = 0; *stride = 1; }
-  else { *base = lg->hfull; *off = lg->p; *stride = lg->P; }
-}
-
-int lg_local_best(fmp_large_s* lg, double* best) {
-  cudaStream_t st = lg_stream(lg);
-  const void* base;
-  int64_t off, stride;
-  lg_view(lg, &base, &off, &stride);
-  if (lg->view == 1) CU(fmp::lg_launch_reduce_max(lg->blkmax, lg->dval, st));
-  else CU(fmp::lg_launch_max(lg->dtype, base, off, stride, lg->np, lg->blkmax, lg->dval, st));
-  if (lg->fused) {
-    // one shard: the band pick (solvers.cpp:90-101) with the cut taken from
-    // the device best, and h0 there, in the same round trip
-    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval, lg->blkmax,
-                            lg->dfirst, st));
-    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
-    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    lg->first_ready = true;
-    *best = lg->first_rec[0];
-    return FMP_OK;
-  }
-  CU(cudaMemcpyAsync(best, lg->dval, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  return FMP_OK;
-}
-
-// explicit residual r = y - Phi_Lambda x (replicated on every shard);
-// enqueued only, ||r||^2 left in dval
-// cnt: atoms in the estimate (lg->s, or lg->s + 1 right after LS appended one)
-int lg_residual_launch(fmp_large_s* lg, int cnt);
-
-int lg_residual(fmp_large_s* lg, double* rn) {
-  if (int e = lg_residual_launch(lg, lg->s)) return e;
-  cudaStream_t st = lg_stream(lg);
-  double r2 = 0;
-  CU(cudaMemcpyAsync(&r2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  *rn = std::sqrt(r2);
-  return FMP_OK;
-}
-
-int lg_residual_launch(fmp_large_s* lg, int cnt) {
-  cudaStream_t st = lg_stream(lg);
-  if (lg->op->d.fs_l1) {
-    // two-pass forward transform straight from the sparse estimate, gathered
-    // at Omega (no dense scatter, fmp_transform_4s.cu)
-    fmp_ctx_s* ctx = lg->op->ctx;
-    void* w;
-    ALLOC(w, S_WORK, (size_t)lg->n * lg->eb);
-    fmp::FsTransform t{};
-    t.op = &lg->op->d;
-    t.dtype = lg->dtype;
-    t.inverse = 0;
-    t.in_mode = 2;
-    t.lam = lg->lam;
-    t.xs = lg->x;
-    t.cnt = cnt;
-    t.mid = w;
-    t.out_mode = 1;
-    t.out = lg->ax;
-    t.batch = 1;
-    CU(fmp::launch_transform_fs(t, st));
-  } else {
-    CU(cudaMemsetAsync(lg->xdense, 0, (size_t)lg->n * lg->eb, st));
-    CU(fmp::lg_launch_scatter_x(lg->dtype, lg->xdense, lg->lam, lg->x, cnt, st));
-    if (int e = run_transform(lg->op, lg->dtype, 0, 0, 1, lg->xdense, lg->ax, 1, nullptr, st)) return e;
-  }
-  CU(fmp::lg_launch_resid(lg->dtype, lg->y, lg->ax, lg->r, lg->m, lg->part, lg->dval, st));
-  return FMP_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int fmp_large_create(fmp_op op, int dtype, uint64_t shard, uint64_t nshards,
-                     const fmp_omp_config* cfg, fmp_large* out) {
-  if (!op || !cfg || !out) return fail(FMP_EINVAL, "null argument");
-  if (op->d.kind != fmp::FOURIER)
-    return fail(FMP_EUNSUPPORTED, "the sharded solver is implemented for Fourier operators");
-  if (dtype != FMP_C64 && dtype != FMP_C128) return fail(FMP_EINVAL, "complex dtypes only");
-  if (nshards < 1 || shard >= nshards || (uint64_t)op->d.n % nshards)
-    return fail(FMP_EINVAL, "bad shard %llu of %llu", (unsigned long long)shard,
-                (unsigned long long)nshards);
-  if (cfg->max_iterations < 1) return fail(FMP_EINVAL, "omp_solve: max_iterations must be >= 1");
-  fmp_ctx_s* ctx = op->ctx;
-  CU(cudaSetDevice(ctx->device));
-  fmp_large_s* lg = new fmp_large_s;
-  lg->op = op;
-  lg->dtype = dtype;
-  lg->P = (int)nshards;
-  lg->p = (int)shard;
-  lg->n = op->d.n;
-  lg->m = op->d.m;
-  lg->np = lg->n / lg->P;
-  lg->T = (int)cfg->max_iterations;
-  lg->eb = fmp::elem_bytes(dtype);
-  {
-    fmp_omp_config c = *cfg;
-    lg->fast_until = c.mode == FMP_MODE_CONVENTIONAL ? 0
-                     : c.mode == FMP_MODE_FAST       ? std::numeric_limits<int64_t>::max()
-                     : c.mode == FMP_MODE_ADAPTIVE   ? (int64_t)fmp_crossover_iteration(FMP_FOURIER, (uint64_t)lg->n)
-                     : c.mode == FMP_MODE_GPU        ? (int64_t)fmp_gpu_crossover(FMP_FOURIER, (uint64_t)lg->n)
-                                                     : (int64_t)std::min<uint64_t>(c.fast_until, INT64_MAX);
-  }
-  const size_t eb = lg->eb;
-  const int grid = fmp::lg_grid();
-  int st = FMP_OK;
-  auto A = [&](void** p, size_t b) { if (!st) st = lg_alloc(lg, p, b); };
-  A(&lg->h0s, lg->np * eb);
-  A(&lg->hs, lg->np * eb);
-  A(&lg->hfull, lg->n * eb);
-  if (!op->d.fs_l1) A(&lg->xdense, lg->n * eb);  // (the two-pass transform reads the sparse estimate)
-  A(&lg->ax, lg->m * eb);
-  A(&lg->r, lg->m * eb);
-  A(&lg->y, lg->m * eb);
-  A(&lg->xn, (size_t)lg->T * eb);
-  A((void**)&lg->W, (size_t)lg->T * (lg->T + 1) / 2 * 16);
-  A((void**)&lg->x, (size_t)lg->T * 16);
-  A((void**)&lg->z, (size_t)lg->T * 16);
-  A((void**)&lg->l, (size_t)lg->T * 16);
-  A((void**)&lg->lam, (size_t)lg->T * 4);
-  A((void**)&lg->part, (size_t)std::max(grid, (lg->T + 255) / 256) * 3 * 8);
-  A((void**)&lg->scal, 16 * 8);
-  // per-CTA maxima, then one maximum per 128-position tile (lg_launch_first)
-  A((void**)&lg->blkmax, ((size_t)grid + (size_t)(lg->np + 127) / 128) * 8);
-  A((void**)&lg->dval, 64);
-  A((void**)&lg->dfirst, 64);
-  A((void**)&lg->drec, 64);
-  if (!st && lg->P > 1) {
-    A(&lg->gcm, lg->n * eb);
-    lg->own_gcm = true;
-  }
-  if (st) {
-    fmp_large_destroy(lg);
-    return st;
-  }
-  const void* g = dtype == FMP_C128 ? (const void*)op->d.g64 : (const void*)op->d.g32;
-  if (lg->P > 1) {
-    cudaError_t e = fmp::lg_launch_classmajor(dtype, g, lg->gcm, lg->n, lg->P, ctx->cur);
-    if (e != cudaSuccess) {
-      fmp_large_destroy(lg);
-      return fail(FMP_ECUDA, "class-major kernel: %s", cudaGetErrorString(e));
-    }
-  } else {
-    lg->gcm = const_cast<void*>(g);
-  }
-  *out = lg;
-  return FMP_OK;
-}
-
-int fmp_large_destroy(fmp_large lg) {
-  if (!lg) return FMP_OK;
-  cudaSetDevice(lg->op->ctx->device);
-  cudaStreamSynchronize(lg->op->ctx->cur);
-  for (void* p : lg->allocs) cudaFree(p);
-  delete lg;
-  return FMP_OK;
-}
-
-int fmp_large_begin(fmp_large lg, const void* y, double tol, double* local_best) {
-  if (!lg || !y || !local_best) return fail(FMP_EINVAL, "null argument");
-  if (!(tol >= 0.0)) return fail(FMP_EINVAL, "omp_solve: tolerance must be >= 0");
-  CU(cudaSetDevice(lg->op->ctx->device));
-  CtxLock lk(lg->op->ctx);
-  lk.use(lg->op->ctx->cur);
-  cudaStream_t st = lg_stream(lg);
-  CU(cudaMemcpyAsync(lg->y, y, lg->m * lg->eb, cudaMemcpyHostToDevice, st));
-  CU(cudaMemsetAsync(lg->scal, 0, 16 * 8, st));
-  CU(cudaStreamSynchronize(st));
-  // ||y||^2 (fp64, in the order a single thread would sum)
-  double yy = 0.0;
-  if (lg->dtype == FMP_C128) {
-    const double* v = (const double*)y;
-    for (int64_t i = 0; i < 2 * lg->m; ++i) yy += v[i] * v[i];
-  } else {
-    const float* v = (const float*)y;
-    for (int64_t i = 0; i < 2 * lg->m; ++i) yy += (double)v[i] * v[i];
-  }
-  lg->yy = yy;
-  lg->tol = tol;
-  lg->rn = std::sqrt(yy);
-  lg->rn_explicit = true;
-  lg->t = 0;
-  lg->s = 0;
-  lg->iters = 0;
-  lg->aborted = 0;
-  lg->support.clear();
-  lg->sel.assign((size_t)lg->n, 0);
-  if (lg->rn <= tol) {
-    lg->done = true;
-    *local_best = -1.0;
-    return FMP_OK;
-  }
-  lg->done = false;
-  const double gamma = lg->op->d.kind == fmp::FOURIER ? 0.0 : 0.0;
-  (void)gamma;
-  // scal: [0] gamma = c(1) = M/N, [1] yy, [2] zz
-  std::vector<double> sc(16, 0.0);
-  sc[0] = (double)lg->m / (double)lg->n;
-  sc[1] = yy;
-  CU(cudaMemcpyAsync(lg->scal, sc.data(), 16 * 8, cudaMemcpyHostToDevice, st));
-  // t = 1: h0 = Phi^H y (full transform, this shard's entries kept)
-  if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->y, lg->hfull, 1, nullptr, st)) return e;
-  CU(fmp::lg_launch_take(lg->dtype, lg->hfull, lg->h0s, lg->np, lg->P, lg->p, st));
-  lg->t = 1;
-  lg->view = 0;
-  CU(cudaStreamSynchronize(st));
-  return lg_local_best(lg, local_best);
-}
-
-int fmp_large_first(fmp_large lg, double global_best, uint64_t* atom, double* h0_at) {
-  if (!lg || !atom || !h0_at) return fail(FMP_EINVAL, "null argument");
-  CU(cudaSetDevice(lg->op->ctx->device));
-  CtxLock lk(lg->op->ctx);
-  lk.use(lg->op->ctx->cur);
-  cudaStream_t st = lg_stream(lg);
-  if (!(lg->first_ready && global_best == lg->first_rec[0])) {
-    const double cut = global_best * (1.0 - 1e-9);  // kTieBandRel, solvers.cpp:40
-    const void* base;
-    int64_t off, stride;
-    lg_view(lg, &base, &off, &stride);
-    // the tile maxima of the last k_lg_max / k_lg_fast over this view
-    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, cut, nullptr, lg->blkmax,
-                            lg->dfirst, st));
-    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
-    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-  }
-  lg->first_ready = false;
-  if (lg->first_rec[1] < 0.0) {
-    *atom = 0;
-    h0_at[0] = h0_at[1] = 0.0;
-    return FMP_OK;
-  }
-  const uint64_t kp = (uint64_t)lg->first_rec[1];
-  *atom = (uint64_t)lg->p + (uint64_t)lg->P * kp + 1;
-  h0_at[0] = lg->first_rec[2];
-  h0_at[1] = lg->first_rec[3];
-  return FMP_OK;
-}
-
-int fmp_large_stop(fmp_large lg) {
-  if (!lg) return fail(FMP_EINVAL, "null argument");
-  if (lg->done) return FMP_OK;
-  lg->done = true;
-  CU(cudaSetDevice(lg->op->ctx->device));
-  CtxLock lk(lg->op->ctx);
-  lk.use(lg->op->ctx->cur);
-  if (!lg->rn_explicit) {
-    if (int e = lg_residual(lg, &lg->rn)) return e;
-    lg->rn_explicit = true;
-  }
-  return FMP_OK;
-}
-
-// One shard (fmp_large_solve): one host round trip per iteration.  LS, the
-// explicit residual a conventional next row needs, the next correlation,
-// its band pick and every scalar the host decides on are enqueued together;
-// the correlation is speculative (wasted on the last iteration, an abort or
-// a halt), which the single synchronisation pays for many times over.  Same
-// kernels in the same order as fmp_large_advance + lg_local_best, so the
-// results are bitwise those of the two-round-trip protocol.
-static int lg_advance_fused(fmp_large_s* lg, uint64_t pick, const double* h0_at, int* done,
-                            double* local_best) {
-  cudaStream_t st = lg_stream(lg);
-  CtxLock lk(lg->op->ctx);
-  lk.use(lg->op->ctx->cur);
-  CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
-                       lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
-  const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
-  if (next_conv)
-    if (int e = lg_residual_launch(lg, lg->s + 1)) return e;
-  double sc[3] = {0, 0, 0};
-  CU(cudaMemcpyAsync(sc, lg->scal + 2, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(sc + 1, lg->scal + 6, 8, cudaMemcpyDeviceToHost, st));
-  if (next_conv) CU(cudaMemcpyAsync(sc + 2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
-  const bool spec = lg->t < lg->T;
-  int spec_view = lg->view;
-  if (spec) {
-    if ((int64_t)(lg->t + 1) <= lg->fast_until) {
-      CU(fmp::lg_launch_fast(lg->dtype, lg->h0s, lg->hs, lg->gcm, lg->np, lg->P, lg->p, lg->n,
-                             lg->lam, lg->xn, lg->s + 1, lg->blkmax, st));
-      spec_view = 1;
-    } else {
-      if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->r, lg->hfull, 1, nullptr, st)) return e;
-      spec_view = 2;
-    }
-    const int keep = lg->view;
-    lg->view = spec_view;
-    const void* base;
-    int64_t off, stride;
-    lg_view(lg, &base, &off, &stride);
-    lg->view = keep;
-    if (spec_view == 1) CU(fmp::lg_launch_reduce_max(lg->blkmax, lg->dval, st));
-    else CU(fmp::lg_launch_max(lg->dtype, base, off, stride, lg->np, lg->blkmax, lg->dval, st));
-    CU(fmp::lg_launch_first(lg->dtype, base, off, stride, lg->np, 0.0, lg->dval, lg->blkmax,
-                            lg->dfirst, st));
-    CU(fmp::lg_launch_pick(lg->dtype, lg->dval, lg->dfirst, lg->h0s, lg->drec, st));
-    CU(cudaMemcpyAsync(lg->first_rec, lg->drec, 32, cudaMemcpyDeviceToHost, st));
-  }
-  CU(cudaStreamSynchronize(st));
-  if (sc[1] != 0.0) {  // rank deficient: keep the previous state (solvers.cpp:380-385)
-    lg->aborted = 1;
-    lg->done = true;
-    *done = 1;
-    if (next_conv || !lg->rn_explicit) {
-      if (int e = lg_residual(lg, &lg->rn)) return e;
-      lg->rn_explicit = true;
-    }
-    return FMP_OK;
-  }
-  lg->s += 1;
-  lg->support.push_back(pick);
-  lg->sel[pick] = 1;
-  lg->iters = lg->t;
-  const double zz = sc[0];
-  const double r2id = lg->yy - zz;  // residual and halting (solvers.cpp:388-402)
-  const double margin = lg->dtype == FMP_C128 ? 1e-10 : 1e-5;
-  const bool near = !(r2id > lg->tol * lg->tol + margin * lg->yy);
-  if (next_conv) {
-    lg->rn = std::sqrt(sc[2]);
-    lg->rn_explicit = true;
-  } else if (near) {
-    if (int e = lg_residual(lg, &lg->rn)) return e;
-    lg->rn_explicit = true;
-  } else {
-    lg->rn = std::sqrt(std::max(r2id, 0.0));
-    lg->rn_explicit = false;
-  }
-  if ((lg->rn_explicit && lg->rn <= lg->tol) || lg->t >= lg->T) {
-    lg->done = true;
-    *done = 1;
-    if (!lg->rn_explicit) {
-      if (int e = lg_residual(lg, &lg->rn)) return e;
-      lg->rn_explicit = true;
-    }
-    return FMP_OK;
-  }
-  lg->t += 1;
-  lg->view = spec_view;
-  lg->first_ready = true;
-  *local_best = lg->first_rec[0];
-  *done = 0;
-  return FMP_OK;
-}
-
-int fmp_large_advance(fmp_large lg, uint64_t atom, const double* h0_at, int* done,
-                      double* local_best) {
-  if (!lg || !h0_at || !done || !local_best) return fail(FMP_EINVAL, "null argument");
-  if (lg->done) {
-    *done = 1;
-    return FMP_OK;
-  }
-  if (atom < 1 || atom > (uint64_t)lg->n) return fail(FMP_EINVAL, "atom out of range");
-  const uint64_t pick = atom - 1;
-  if (lg->sel[pick]) {  // stagnation guard (solvers.cpp:365-367)
-    *done = 1;
-    return fmp_large_stop(lg);
-  }
-  CU(cudaSetDevice(lg->op->ctx->device));
-  if (lg->fused && !getenv("FMP_LARGE_TWO_TRIPS")) return lg_advance_fused(lg, pick, h0_at, done, local_best);
-  cudaStream_t st = lg_stream(lg);
-  {
-    CtxLock lk(lg->op->ctx);
-    lk.use(lg->op->ctx->cur);
-    // least squares (replicated)
-    CU(fmp::lg_launch_ls(lg->dtype, lg->op->d, lg->W, lg->x, lg->z, lg->l, lg->lam, lg->xn, lg->part,
-                         lg->scal, lg->T, lg->s, (unsigned)pick, make_double2(h0_at[0], h0_at[1]), st));
-    // a conventional next row needs the explicit residual whatever LS gives:
-    // enqueue it now so one round trip returns zz, the abort flag and ||r||^2
-    // (on an abort LS leaves x alone, so r is the previous state's residual)
-    const bool next_conv = lg->t < lg->T && !((int64_t)(lg->t + 1) <= lg->fast_until);
-    if (next_conv)
-      if (int e = lg_residual_launch(lg, lg->s + 1)) return e;
-    double sc[3] = {0, 0, 0};
-    CU(cudaMemcpyAsync(sc, lg->scal + 2, 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(sc + 1, lg->scal + 6, 8, cudaMemcpyDeviceToHost, st));
-    if (next_conv) CU(cudaMemcpyAsync(sc + 2, lg->dval, 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    if (sc[1] != 0.0) {  // rank deficient: keep the previous state (solvers.cpp:380-385)
-      lg->aborted = 1;
-      lg->done = true;
-      *done = 1;
-      if (next_conv || !lg->rn_explicit) {  // (the early residual counted the rejected atom)
-        if (int e = lg_residual(lg, &lg->rn)) return e;
-        lg->rn_explicit = true;
-      }
-      return FMP_OK;
-    }
-    lg->s += 1;
-    lg->support.push_back(pick);
-    lg->sel[pick] = 1;
-    lg->iters = lg->t;
-    const double zz = sc[0];
-    // residual and halting (solvers.cpp:388-402)
-    const double r2id = lg->yy - zz;
-    const double margin = lg->dtype == FMP_C128 ? 1e-10 : 1e-5;
-    const bool near = !(r2id > lg->tol * lg->tol + margin * lg->yy);
-    if (next_conv) {
-      lg->rn = std::sqrt(sc[2]);
-      lg->rn_explicit = true;
-    } else if (near) {
-      if (int e = lg_residual(lg, &lg->rn)) return e;
-      lg->rn_explicit = true;
-    } else {
-      lg->rn = std::sqrt(std::max(r2id, 0.0));
-      lg->rn_explicit = false;
-    }
-    if ((lg->rn_explicit && lg->rn <= lg->tol) || lg->t >= lg->T) {
-      lg->done = true;
-      *done = 1;
-      if (!lg->rn_explicit) {
-        if (int e = lg_residual(lg, &lg->rn)) return e;
-        lg->rn_explicit = true;
-      }
-      return FMP_OK;
-    }
-    // next correlation
-    lg->t += 1;
-    if ((int64_t)lg->t <= lg->fast_until) {
-      const void* xn = lg->xn;
-      CU(fmp::lg_launch_fast(lg->dtype, lg->h0s, lg->hs, lg->gcm, lg->np, lg->P, lg->p, lg->n,
-                             lg->lam, xn, lg->s, lg->blkmax, st));
-      lg->view = 1;
-    } else {
-      if (int e = run_transform(lg->op, lg->dtype, 1, 1, 0, lg->r, lg->hfull, 1, nullptr, st)) return e;
-      lg->view = 2;
-    }
-  }
-  *done = 0;
-  CtxLock lk(lg->op->ctx);
-  lk.use(lg->op->ctx->cur);
-  return lg_local_best(lg, local_best);
-}
-
-int fmp_large_result(fmp_large lg, uint64_t* support, double* coeffs, uint64_t* support_size,
-                     uint64_t* iterations, double* residual, int32_t* aborted) {
-  if (!lg) return fail(FMP_EINVAL, "null argument");
-  CU(cudaSetDevice(lg->op->ctx->device));
-  if (support)
-    for (size_t j = 0; j < lg->support.size(); ++j) support[j] = lg->support[j] + 1;
-  if (coeffs && lg->s) CU(cudaMemcpy(coeffs, lg->x, (size_t)lg->s * 16, cudaMemcpyDeviceToHost));
-  if (support_size) *support_size = (uint64_t)lg->s;
-  if (iterations) *iterations = (uint64_t)lg->iters;
-  if (residual) *residual = lg->rn;
-  if (aborted) *aborted = lg->aborted;
-  return FMP_OK;
-}
-
-int fmp_large_solve(fmp_op op, int dtype, const void* y, const fmp_omp_config* cfg,
-                    fmp_omp_result* out) {
-  if (!op || !y || !cfg || !out) return fail(FMP_EINVAL, "null argument");
-  fmp_large lg = nullptr;
-  if (int e = fmp_large_create(op, dtype, 0, 1, cfg, &lg)) return e;
-  lg->fused = true;
-  double best = 0.0;
-  int st = fmp_large_begin(lg, y, cfg->tolerances ? cfg->tolerances[0] : cfg->tolerance, &best);
-  int done = best < 0.0;
-  while (!st && !done) {
-    if (best == 0.0) {  // nothing left to select (solvers.cpp:363)
-      st = fmp_large_stop(lg);
-      break;
-    }
-    uint64_t atom = 0;
-    double h0[2];
-    if ((st = fmp_large_first(lg, best, &atom, h0))) break;
-    st = fmp_large_advance(lg, atom, h0, &done, &best);
-  }
-  if (!st)
-    st = fmp_large_result(lg, out->support, out->coeffs, out->support_size, out->iterations,
-                          out->residual, out->aborted);
-  fmp_large_destroy(lg);
-  return st;
 }
 
 }  // extern "C"

@@ -74,7 +74,7 @@ struct FsTransform {
   int in_mode;              // 0 dense n, 1 m values at Omega, 2 sparse (lam, xs; batch 1)
   const void* in;
   const uint32_t* lam;      // in_mode 2: 0-based positions
-  const double2* xs;        // in_mode 2: values (fp64)
+  const double2* xs;        // in_mode 2: values (fp64); positions 0xffffffff are skipped
   int cnt;
   void* mid;                // batch x n scratch
   int out_mode;             // 0 dense n, 1 gathered at Omega (m)
@@ -201,30 +201,93 @@ int64_t transform_max_n(int dtype);
 cudaError_t launch_least_squares(const DevOp& op, int dtype, const void* y, const uint32_t* sup,
                                  int s, int64_t batch, double2* x, int64_t* bad, double2* L,
                                  int grid, cudaStream_t st);
-// sharded single-signal solver kernels (fmp_large.cu)
+// ---- sharded single-signal solver (fmp_large.cu; config 5).  Shard p of P
+// owns the correlation entries k = p + P k' (cyclic), k' < np = n / P.
+constexpr int LG_RC = 64;         // candidates per shard carried in an exchange record
+constexpr int LG_LCAP = 1 << 16;  // candidates a shard evaluates in fp64 per identification
+struct LgCand {
+  uint64_t j;    // global 0-based atom
+  double m64;    // fp64 |h_j|^2 = |h0_j - sum_tau x_tau c[(j - lambda_tau) mod N]|^2
+};
+// one shard's identification record (exchanged by all-gather)
+struct LgRec {
+  double best32;       // this shard's maximum of the working-precision |h|^2
+  uint32_t count;      // candidates found (may exceed LG_RC: overflow)
+  uint32_t pad;
+  LgCand c[LG_RC];
+};
+enum LgFlag { LG_ZERO = 1, LG_STAGNANT = 2, LG_OVERFLOW = 4, LG_TOOMANY = 8 };
+// the merged pick (identical on every shard)
+struct LgPick {
+  uint64_t j;    // global 0-based atom
+  double best64;
+  double2 b;     // fp64 h0 at j (least-squares right-hand side)
+  int32_t flags;
+  int32_t pad;
+};
+// device state of one shard (pointers into its GPU's memory)
+struct LgShard {
+  DevOp op;                 // full operator: omega, tw64 / tw32, g64, ...
+  int dtype;                // C64 or C128 (working precision of h and r)
+  int P, p, log2P, T;
+  int64_t n, m, np;
+  const void* gcm;          // kernel, class-major gcm[c][j'] = c[c + P j'] (dtype)
+  void* h0s;                // own class of h0 (dtype)
+  void* hs;                 // own class of the current correlation (dtype)
+  const double2* h0x;       // fp64 h0 = Phi^H y, all n entries (replicated)
+  double* blkmax;           // per-CTA maxima, then one per 128-position tile
+  uint32_t* cand;           // LG_LCAP local candidates k'
+  double* cval;             // their fp64 |h|^2
+  unsigned* ccount;         // [0] candidates found
+  LgRec* rec_send;          // this shard's record
+  LgRec* rec_all;           // the P gathered records
+  LgPick* pick;             // [2]: picks of alternate iterations
+  double* fb;               // fallback scratch: [0] local best64, [1] global best64; u64 [2] first, [3] global first
+  // least squares (replicated)
+  double2 *W, *x, *z, *l;
+  uint32_t* lam;            // T atoms, 0-based
+  void* xn;                 // T, dtype: -x for the fast update
+  double* part;
+  double* scal;             // [0] gamma [1] yy [2] zz [3] d [4..5] znew [6] abort [7] sum|x| [8] max|x| [9] r2 [10] hy
+  uint32_t* selbits;        // n bits: atoms selected
+  // residual
+  const void* y;            // m (dtype)
+  const double2* y64;       // m, fp64 (fp32 data widened; = y for c128)
+  void* r;                  // m (dtype)
+  void* ax;                 // m (dtype or c128): Phi x at Omega, or this shard's partial
+  void* axsum;              // m: sum of the partials over shards (P > 1)
+  uint32_t* lamc;           // T: this shard's atoms as k' (0xffffffff: other class)
+  void* fold;               // np (dtype): folded residual (P > 1)
+  const uint32_t* bin_off;  // np + 1: rows by bin omega mod np (P > 1)
+  const uint32_t* bin_row;  // m
+};
 int lg_grid();
-cudaError_t lg_launch_fast(int dtype, const void* h0s, void* hs, const void* gcm, int64_t np, int P,
-                           int p, int64_t n, const uint32_t* lam, const void* xn, int s,
-                           double* blkmax, cudaStream_t st);
-cudaError_t lg_launch_max(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
-                          double* blkmax, double* out, cudaStream_t st);
-cudaError_t lg_launch_reduce_max(double* blkmax, double* out, cudaStream_t st);
-cudaError_t lg_launch_first(int dtype, const void* base, int64_t off, int64_t stride, int64_t cnt,
-                            double cut, const double* cut_best, const double* blkmax,
-                            unsigned long long* first, cudaStream_t st);
-cudaError_t lg_launch_pick(int dtype, const double* best, const unsigned long long* first,
-                           const void* h0s, double* rec, cudaStream_t st);
-cudaError_t lg_launch_ls(int dtype, const DevOp& op, double2* W, double2* x, double2* z, double2* l,
-                         uint32_t* lam, void* xn, double* part, double* scal, int T, int s,
-                         unsigned pick, double2 bnew, cudaStream_t st);
-cudaError_t lg_launch_scatter_x(int dtype, void* out, const uint32_t* lam, const double2* x, int s,
-                                cudaStream_t st);
-cudaError_t lg_launch_resid(int dtype, const void* y, const void* ax, void* r, int64_t m,
-                            double* part, double* out, cudaStream_t st);
-cudaError_t lg_launch_take(int dtype, const void* src, void* dst, int64_t np, int P, int p,
-                           cudaStream_t st);
-cudaError_t lg_launch_classmajor(int dtype, const void* g, void* gcm, int64_t n, int P,
-                                 cudaStream_t st);
+// correlation rows and the local identification record
+cudaError_t lg_fast(const LgShard& S, int s, cudaStream_t st);                 // hs, tile maxima, best32
+cudaError_t lg_max(const LgShard& S, const void* h, cudaStream_t st);          // tile maxima, best32 of h
+cudaError_t lg_identify(const LgShard& S, const void* h, int s, double ecoef, int prev, cudaStream_t st);
+cudaError_t lg_merge(const LgShard& S, int cur, int prev, cudaStream_t st);     // rec_all -> pick[cur]
+// fallback when a record overflowed: exact max / first over every candidate
+cudaError_t lg_fb_local_best(const LgShard& S, cudaStream_t st);               // fb[0]
+cudaError_t lg_fb_local_first(const LgShard& S, cudaStream_t st);              // u64 fb[2] (reads fb[1])
+cudaError_t lg_fb_pick(const LgShard& S, int cur, cudaStream_t st);             // pick[cur] from fb[1], fb[3]
+// least squares for pick[cur] (skipped when it is flagged), sum|x|, max|x|
+cudaError_t lg_ls(const LgShard& S, int s, int cur, cudaStream_t st);
+// residual pieces
+cudaError_t lg_class_positions(const LgShard& S, int cnt, cudaStream_t st);    // lamc
+cudaError_t lg_scatter_dense(const LgShard& S, int dtype, void* out, int64_t len, int cnt, cudaStream_t st);
+cudaError_t lg_partial(const LgShard& S, int dtype, const void* X, void* out, cudaStream_t st);
+cudaError_t lg_resid(const LgShard& S, int dtype, const void* ax, cudaStream_t st);  // r (dtype runs), scal[9]
+cudaError_t lg_fold(const LgShard& S, cudaStream_t st);                         // fold <- r
+cudaError_t lg_sum_partials(int dtype, const void* const* src, int P, void* dst, int64_t m, cudaStream_t st);
+// setup
+cudaError_t lg_take_narrow(const LgShard& S, cudaStream_t st);                  // h0s <- h0x
+cudaError_t lg_classmajor(int dtype, const void* g, void* gcm, int64_t n, int P, cudaStream_t st);
+cudaError_t lg_reduce_f64(const double* src, int P, int op_max, double* dst, cudaStream_t st);
+cudaError_t lg_reduce_u64_min(const unsigned long long* src, int P, unsigned long long* dst, cudaStream_t st);
+// the merge rule on host records (tests): returns the pick as a LgPick
+void lg_merge_host(const LgRec* recs, int P, const uint32_t* selbits, LgPick* out);
+
 // FMA-pipe throughput (FMAs per second) measured by a calibration kernel
 cudaError_t fma_peak(int is_double, double* fma_per_s);
 // number of kernel launches issued by the last launch_* call on this thread

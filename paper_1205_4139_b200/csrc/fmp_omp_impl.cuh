@@ -500,7 +500,12 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           __syncthreads();
           const int nc = *s_ncand;
           double best64;
-          if (nc <= RCAP) {
+          if (nc == 1) {
+            // a single candidate is the pick: every index whose fp64 |h| is
+            // within the band of the fp64 maximum passes the candidate cut
+            pick = s_cand[0];
+            best64 = best;  // (only its sign is used below)
+          } else if (nc <= RCAP) {
             // one warp per candidate, lanes over the atoms (fixed shuffle tree)
             for (int c = warp; c < nc; c += nw) {
               const unsigned j = s_cand[c];
@@ -698,13 +703,13 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           // residual; an fp32 r is formed only to feed a conventional row
           if (next_conv) residual_explicit(s);
           bool halt;
-          if (fabs(r2id - tol * tol) <= 1e-10 * yy) {
+          rn_explicit = fabs(r2id - tol * tol) <= 1e-10 * yy;  // (rn64 of this state)
+          if (rn_explicit) {
             rn = residual64(s);
             halt = rn <= tol;
           } else {
             halt = r2id <= tol * tol;
           }
-          rn_explicit = false;
           mark(4);
           if (halt) break;
         } else {
@@ -720,8 +725,14 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           if (rn_explicit && rn <= tol) break;
         }
       }
-      if (REFINE) rn = residual64(s);
-      else if (!rn_explicit) rn = residual_explicit(s);
+      if (REFINE) {
+        // the fp64 identity where it resolves ||r|| to ~1e-10 relative, else
+        // the direct fp64 residual
+        const double r2id = yy - zz;
+        if (!rn_explicit) rn = r2id > 1e-6 * yy ? sqrt(r2id) : residual64(s);
+      } else if (!rn_explicit) {
+        rn = residual_explicit(s);
+      }
       mark(4);
     }
     // ---- results (RecoveryResult, solvers.hpp:53-64)

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1) k_fs_a(FsArgs a) {
         int placed = 0;
         for (int e = tid; e < a.cnt; e += nth) {
           const uint32_t pos = a.lam[e];
+          if (pos == 0xffffffffu) continue;  // entry not in this transform (sharded solver)
           const int c = (int)(pos & (N2 - 1)) - c0;
           if (c >= 0 && c < C) {
             buf[c * stride + slot((int)(pos >> L2))] = load_cast<V, HAD>(a.xs[e]);
