@@ -498,10 +498,18 @@ def _config(cfg: SolveConfig, tolerances=None):
 
 
 
-def _host_outs(specs):
+# batches below this size take the library's small-batch path, which stages
+# through the context's own page-locked block: plain numpy result buffers
+_PINNED_MIN_BATCH = 1024
+
+
+def _host_outs(specs, pinned=True):
     """Several result buffers carved from ONE page-locked allocation (one
     trip through torch's host allocator per call instead of one per buffer;
-    each view keeps the block alive).  specs: (shape, dtype, zero) tuples."""
+    each view keeps the block alive).  specs: (shape, dtype, zero) tuples.
+    pinned=False: plain numpy buffers (small batches)."""
+    if not pinned:
+        return [np.zeros(shape, dt) if zero else np.empty(shape, dt) for shape, dt, zero in specs]
     sizes = [int(np.prod(shape, dtype=np.int64)) * np.dtype(dt).itemsize for shape, dt, _ in specs]
     offs, tot = [], 0
     for b in sizes:
@@ -544,7 +552,7 @@ def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
         ((B, T), np.uint64, False), ((B, T), np.complex128, False), ((B,), np.uint64, False),
         ((B,), np.uint64, False), ((B,), np.float64, False), ((B,), np.int32, False),
         ((B, T), np.uint8, True),  # rows past the last iteration stay 0
-        ((B,), np.uint64, False)])
+        ((B,), np.uint64, False)], pinned=B >= _PINNED_MIN_BATCH)
     hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
     tol = None
     if tolerances is not None:

@@ -654,7 +654,7 @@ static int64_t fast_until_of(fmp_op op, const fmp_omp_config* cfg, int dtype, ui
 static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
                           const fmp_omp_config* cfg, const double* dtol, fmp_omp_result* out,
                           cudaStream_t st, int wsset = 0, const int* ready = nullptr,
-                          int64_t ready_chunk = 0) {
+                          int64_t ready_chunk = 0, int* queue_zeroed = nullptr) {
   const int wo = wsset ? S_ALT : 0;  // slot offset of the alternate set
   fmp_ctx_s* ctx = op->ctx;
   const int64_t T = (int64_t)cfg->max_iterations;
@@ -720,10 +720,12 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
     ALLOC(bw, wo + S_BUF, (size_t)a.grid * (n + n / 8) * eb);
     a.buf_ws = bw;
   }
-  int* q;
-  ALLOC(q, wo + S_Q, 64);
+  int* q = queue_zeroed;  // (a caller's copy already cleared it)
+  if (!q) {
+    ALLOC(q, wo + S_Q, 64);
+    CU(cudaMemsetAsync(q, 0, 4, st));
+  }
   a.queue = q;
-  CU(cudaMemsetAsync(q, 0, 4, st));
   if (g_phase_prof) {
     unsigned long long* ph;
     ALLOC(ph, S_PH, 64);
@@ -1033,6 +1035,61 @@ static int omp_host_chunked(fmp_op op, int dtype, const void* y, uint64_t batch,
   return FMP_OK;
 }
 
+// Host buffers, small batches (latency regime, e.g. config 1): the inputs
+// (measurements, tolerances, a zeroed work counter) staged in the context's
+// page-locked block and moved by ONE copy, one launch, every result written
+// to one device block and returned by ONE copy, one synchronisation; the
+// per-call API work is four calls instead of a dozen
+static int omp_host_small(fmp_op op, int dtype, const void* y, uint64_t batch,
+                          const fmp_omp_config* cfg, fmp_omp_result* out, cudaStream_t st) {
+  fmp_ctx_s* ctx = op->ctx;
+  const uint64_t T = cfg->max_iterations, m = (uint64_t)op->d.m;
+  const size_t eb = fmp::elem_bytes(dtype);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  // input block: y | tolerances | work counter
+  const size_t o_tol = al(batch * m * eb), o_q = o_tol + al(batch * 8), in_bytes = o_q + 256;
+  // result block, each array 256-aligned
+  const size_t o_sup = 0, o_co = o_sup + al(batch * T * 8), o_sz = o_co + al(batch * T * 16),
+               o_it = o_sz + al(batch * 8), o_rn = o_it + al(batch * 8), o_ab = o_rn + al(batch * 8),
+               o_md = o_ab + al(batch * 4), o_hl = o_md + al(batch * T),
+               out_bytes = o_hl + al(batch * 8);
+  if (int e = pinned_reserve(ctx, in_bytes + out_bytes)) return e;
+  char* hin = (char*)ctx->pinned;
+  char* hout = hin + in_bytes;
+  std::memcpy(hin, y, batch * m * eb);
+  double* htol = (double*)(hin + o_tol);
+  if (cfg->tolerances) std::memcpy(htol, cfg->tolerances, batch * 8);
+  else std::fill(htol, htol + batch, cfg->tolerance);
+  std::memset(hin + o_q, 0, 4);
+  char* din;
+  ALLOC(din, S_IN, in_bytes + out_bytes);
+  char* dout = din + in_bytes;
+  CU(cudaMemcpyAsync(din, hin, in_bytes, cudaMemcpyHostToDevice, st));
+  fmp_omp_result d{};
+  d.support = (uint64_t*)(dout + o_sup);
+  d.coeffs = (double*)(dout + o_co);
+  d.support_size = (uint64_t*)(dout + o_sz);
+  d.iterations = (uint64_t*)(dout + o_it);
+  d.residual = (double*)(dout + o_rn);
+  d.aborted = (int32_t*)(dout + o_ab);
+  d.modes = out->modes ? (uint8_t*)(dout + o_md) : nullptr;
+  d.history_len = out->history_len ? (uint64_t*)(dout + o_hl) : nullptr;
+  if (int s = omp_dev_locked(op, dtype, din, batch, cfg, (const double*)(din + o_tol), &d, st, 0,
+                             nullptr, 0, (int*)(din + o_q)))
+    return s;
+  CU(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  std::memcpy(out->support, hout + o_sup, batch * T * 8);
+  std::memcpy(out->coeffs, hout + o_co, batch * T * 16);
+  std::memcpy(out->support_size, hout + o_sz, batch * 8);
+  std::memcpy(out->iterations, hout + o_it, batch * 8);
+  std::memcpy(out->residual, hout + o_rn, batch * 8);
+  std::memcpy(out->aborted, hout + o_ab, batch * 4);
+  if (out->modes) std::memcpy(out->modes, hout + o_md, batch * T);
+  if (out->history_len) std::memcpy(out->history_len, hout + o_hl, batch * 8);
+  return FMP_OK;
+}
+
 int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp_omp_config* cfg,
                   fmp_omp_result* out) {
   if (int s = omp_validate(op, dtype, cfg)) return s;
@@ -1066,6 +1123,7 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
       return omp_host_streamed(op, dtype, y, batch, cfg, out, grid);
     return omp_host_chunked(op, dtype, y, batch, cfg, out, std::min<uint64_t>(8, batch / (2 * grid)));
   }
+  if (!cfg->record_correlations && batch <= grid) return omp_host_small(op, dtype, y, batch, cfg, out, st);
   void* dy;
   if (int s = copy_in(ctx, S_IN, y, batch * m * eb, &dy, st)) return s;
   std::vector<double> tv;

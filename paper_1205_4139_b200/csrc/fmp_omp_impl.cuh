@@ -20,6 +20,8 @@
 // while that identity is well away from the tolerance, else an explicit
 // r = y - Phi_Lambda x by one forward transform of the sparse estimate.
 #pragma once
+#include <atomic>
+
 #include "fmp_kcommon.cuh"
 
 namespace fmp {
@@ -820,7 +822,17 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
 template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT>
 void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
   auto f = k_omp<V, HAD, RPT, GMODE, BUFG, NT, CT>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the attribute is per device and only grows: set it when a launch needs
+  // more than this instantiation was last given (saves a driver call per
+  // launch in the latency regime)
+  static std::atomic<int> set_smem[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& cur = set_smem[dev & 63];
+  if ((int)smem > cur.load(std::memory_order_relaxed)) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cur.store((int)smem, std::memory_order_relaxed);
+  }
   f<<<grid, NT, smem, st>>>(k);
 }
 

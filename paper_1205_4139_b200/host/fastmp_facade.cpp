@@ -518,6 +518,75 @@ SolveConfig default_config(std::size_t k, double y_norm) {
   return cfg;
 }
 
+namespace {
+
+// SolveConfig::check_invariants for omp_solve (solvers.cpp:394-401): after
+// every iteration t the support holds t atoms, the residual r_t = y - Phi x_t
+// is orthogonal to the fitted columns (|col_j^H r_t| <= 1e-8 max(1, ||y||),
+// check_residual_orthogonality, solvers.cpp:194-203) and ||r_t|| does not
+// grow by more than 1e-12.  x_t is the solver's own state after t
+// iterations: the fused solver's result with max_iterations = t (its
+// arithmetic does not depend on the cap).  r_t and Phi^H r_t = (col_j^H r_t)_j
+// are computed on the device, all iterations of a problem in one batch.
+void check_omp_invariants(const SensingOperator& op, const cvec& y, const RecoveryResult& res,
+                          const SolveConfig& cfg) {
+  const std::size_t n = op.n(), m = op.m(), T = res.iterations_run;
+  if (T == 0) return;
+  double yn = 0.0;
+  for (const cplx& v : y) yn += std::norm(v);
+  yn = std::sqrt(yn);
+  const double scale = std::max(1.0, yn);
+  cvec xs(T * n, cplx(0.0));
+  for (std::size_t t = 1; t <= T; ++t) {
+    if (res.support_history.size() < t || res.support_history[t - 1].size() != t)
+      throw std::logic_error("solver invariant violated: support size");
+    RecoveryResult cap;
+    if (t == T) {
+      cap = res;
+    } else {
+      SolveConfig c = cfg;
+      c.max_iterations = t;
+      c.check_invariants = false;
+      c.record_correlations = false;
+      cap = omp_solve(op, y, c);
+    }
+    if (cap.support != res.support_history[t - 1])
+      throw std::logic_error("solver invariant violated: support size");
+    for (std::size_t j = 0; j < cap.support.size(); ++j)
+      xs[(t - 1) * n + cap.support[j] - 1] = cap.coeffs[j];
+  }
+  cvec ax(T * m), h(T * n);
+  check(fmp_apply(static_cast<fmp_op>(op.handle()), FMP_C128, raw(xs), T, raw(ax)));
+  for (std::size_t t = 0; t < T; ++t)
+    for (std::size_t i = 0; i < m; ++i) ax[t * m + i] = y[i] - ax[t * m + i];
+  check(fmp_apply_adjoint(static_cast<fmp_op>(op.handle()), FMP_C128, raw(ax), T, raw(h), nullptr));
+  double prev = yn;
+  for (std::size_t t = 1; t <= T; ++t) {
+    for (std::size_t atom : res.support_history[t - 1])
+      if (std::abs(h[(t - 1) * n + atom - 1]) > 1e-8 * scale)
+        throw std::logic_error(
+            "solver invariant violated: residual not orthogonal to the fitted columns");
+    double rn = 0.0;
+    for (std::size_t i = 0; i < m; ++i) rn += std::norm(ax[(t - 1) * m + i]);
+    rn = std::sqrt(rn);
+    if (rn > prev + 1e-12)
+      throw std::logic_error("solver invariant violated: residual norm increased");
+    prev = rn;
+  }
+}
+
+// SolveConfig::check_invariants for cosamp_solve (solvers.cpp:527-533)
+void check_cosamp_invariants(const RecoveryResult& res, std::size_t k) {
+  for (const auto& sup : res.support_history) {
+    if (sup.size() > k) throw std::logic_error("solver invariant violated: support exceeds k");
+    for (std::size_t i = 1; i < sup.size(); ++i)
+      if (sup[i] <= sup[i - 1])
+        throw std::logic_error("solver invariant violated: support not sorted/distinct");
+  }
+}
+
+}  // namespace
+
 std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std::vector<cvec>& ys,
                                             const SolveConfig& cfg) {
   const std::size_t B = ys.size(), T = cfg.max_iterations, n = op.n(), m = op.m();
@@ -612,6 +681,8 @@ std::vector<RecoveryResult> omp_solve_batch(const SensingOperator& op, const std
     res.costs.least_squares_flops = ls_fc.flops();
     res.costs.identification_flops = id_fc.flops();
   }
+  if (cfg.check_invariants)
+    for (std::size_t b = 0; b < B; ++b) check_omp_invariants(op, ys[b], results[b], cfg);
   return results;
 }
 
@@ -756,6 +827,7 @@ std::vector<RecoveryResult> cosamp_solve_batch(const SensingOperator& op,
         res.correlation_history.emplace_back(hist.begin() + (b * T + t - 1) * n,
                                              hist.begin() + (b * T + t) * n);
     }
+    if (cfg.check_invariants) check_cosamp_invariants(res, k);
   }
   return results;
 }

@@ -236,6 +236,56 @@ int main(int argc, char** argv) {
     CHECK(zero.iterations_run == 0 && zero.support.empty() && zero.residual_norm == 0.0);
     CHECK_THROWS_AS(omp_solve(op, cvec(7), default_config(1, 1.0)), std::invalid_argument);
   }
+  // SolveConfig::check_invariants (test_solvers.cpp:88-107, :133-141, :236-250):
+  // the checks run and pass on exact recoveries, past the sparsity with
+  // tolerance 0 (monotone residual), in every mode, and for CoSaMP
+  {
+    for (TransformKind kind : {TransformKind::Fourier, TransformKind::Hadamard})
+      for (CorrelationMode mode : {CorrelationMode::Fast, CorrelationMode::Conventional,
+                                   CorrelationMode::Adaptive}) {
+        SensingOperator op(StructuredUnitary(kind, 64), make_row_selection(64, 32, 11));
+        const ProblemInstance inst = make_instance(op, 3, 0.0, 12);
+        SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
+        cfg.correlation_mode = mode;
+        cfg.check_invariants = true;
+        bool threw = false;
+        RecoveryResult res;
+        try { res = omp_solve(op, inst.y, cfg); } catch (const std::logic_error&) { threw = true; }
+        CHECK(!threw && res.iterations_run == 3);
+        // past the sparsity with tolerance 0 (test_solvers.cpp:133-141's instance)
+        SensingOperator od(StructuredUnitary(kind, 32), make_row_selection(32, 8, 21));
+        const ProblemInstance di = make_instance(od, 4, 0.0, 22);
+        SolveConfig deep = default_config(di.k, l2_norm(di.y));
+        deep.correlation_mode = mode;
+        deep.max_iterations = 8;
+        deep.residual_tolerance = 0.0;
+        deep.check_invariants = true;
+        threw = false;
+        try { res = omp_solve(od, di.y, deep); } catch (const std::logic_error& e) {
+          threw = true;
+          std::fprintf(stderr, "deep (%s, mode %d): %s\n", to_string(kind), (int)mode, e.what());
+        }
+        CHECK(!threw && res.iterations_run >= 4);
+        SensingOperator on(StructuredUnitary(kind, 256), make_row_selection(256, 64, 5));
+        const ProblemInstance noisy = make_instance(on, 6, 0.05, 9);
+        SolveConfig nc = default_config(noisy.k, l2_norm(noisy.y));
+        nc.correlation_mode = mode;
+        nc.max_iterations = 12;
+        nc.residual_tolerance = 0.0;
+        nc.check_invariants = true;
+        threw = false;
+        try { res = omp_solve(on, noisy.y, nc); } catch (const std::logic_error&) { threw = true; }
+        CHECK(!threw && res.iterations_run == 12);
+      }
+    SensingOperator op(StructuredUnitary(TransformKind::Fourier, 64), make_row_selection(64, 32, 51));
+    const ProblemInstance inst = make_instance(op, 4, 0.0, 52);
+    SolveConfig cfg = default_config(inst.k, l2_norm(inst.y));
+    cfg.max_iterations = 8;
+    cfg.check_invariants = true;
+    bool threw = false;
+    try { (void)cosamp_solve(op, inst.y, inst.k, cfg); } catch (const std::logic_error&) { threw = true; }
+    CHECK(!threw);
+  }
   // least squares in both methods (test_solvers.cpp:39-86)
   {
     SensingOperator op(StructuredUnitary(TransformKind::Fourier, 64), make_row_selection(64, 16, 3));

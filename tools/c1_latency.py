@@ -51,6 +51,18 @@ def main():
         fmp.omp_solve_dev(op, yd, cfg, out, tolerances=td)
         torch.cuda.synchronize()
     print(f"device call + synchronize: {timed(dev):.1f} us")
+    st = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+    for a, b in evs:
+        a.record(st)
+        fmp.omp_solve_dev(op, yd, cfg, out, tolerances=td)
+        b.record(st)
+        torch.cuda.synchronize()
+    print(f"device events (warm L2): {np.median([a.elapsed_time(b) for a, b in evs]) * 1e3:.1f} us")
+    def floor():
+        torch.cuda._sleep(0)
+        torch.cuda.synchronize()
+    print(f"empty launch + synchronize: {timed(floor):.1f} us")
 
 
 if __name__ == "__main__":
