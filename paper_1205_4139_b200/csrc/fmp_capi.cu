@@ -715,6 +715,9 @@ static int omp_dev_locked(fmp_op op, int dtype, const void* y, uint64_t batch,
   void* r;
   ALLOC(r, wo + S_R, (size_t)a.grid * m * eb);
   a.r_ws = r;
+  void* ysw;
+  ALLOC(ysw, wo + S_YS, (size_t)a.grid * m * eb);
+  a.ys_ws = ysw;
   if (n > fmp::transform_max_n(dtype) / 2) {
     void* bw;
     ALLOC(bw, wo + S_BUF, (size_t)a.grid * (n + n / 8) * eb);

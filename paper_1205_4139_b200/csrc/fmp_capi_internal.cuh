@@ -73,7 +73,7 @@ struct Workspace {
 
 enum Slot { S_IN, S_OUT, S_AUX, S_SUP, S_CO, S_WORK, S_MAG, S_W, S_H0, S_R, S_Q, S_TOL,
             S_OSUP, S_OCO, S_OSZ, S_OIT, S_ORES, S_OAB, S_OMOD, S_OHL, S_OHIST, S_IDX, S_BUF, S_PH, S_SYNC,
-            S_OHSUP, S_Y64, S_H0X, S_GOFF, S_RST,
+            S_OHSUP, S_Y64, S_H0X, S_GOFF, S_RST, S_YS,
             S_ALT = 64 };  // S_ALT + slot: the alternate per-CTA workspace set
 
 }  // namespace fmpi

@@ -126,6 +126,7 @@ struct OmpArgs {
   void* h0_ws;              // grid x n (data dtype)
   double* mag_ws;           // grid x n
   void* r_ws;               // grid x m (data dtype) when r is not in smem
+  void* ys_ws;              // grid x m (data dtype): y in transform-slot order (no smem maps)
   void* buf_ws;             // grid x (n + n/8) (data dtype): transform buffer when n exceeds smem
   int* queue;               // work counter (zeroed before launch)
   int grid;

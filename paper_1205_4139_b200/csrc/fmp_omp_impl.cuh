@@ -56,6 +56,7 @@ struct OmpK {
   void* h0_ws;
   double* mag_ws;
   void* r_ws;
+  void* ys_ws;  // grid x m: y in transform-slot order (plans without smem maps)
   int* queue;
   // shared-memory plan
   void* buf_ws;  // grid x (n + n/8) when the buffer lives in global memory
@@ -228,6 +229,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
       continue;
     }
     const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
+    // no smem maps: y and r are kept in transform-slot order (ys_ws, r_ws)
+    V* ysl = (!s_map && a.ys_ws) ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
     const double tol = a.tol[prob];
     const X* h0x = REFINE ? h0x_all + prob * n : nullptr;
 
@@ -270,10 +273,23 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth);
       }
       double r2 = 0.0;
-      for (int j = tid; j < m; j += nth) {
-        const V rv = sub(y[j], scale(buf[padx<OLOGP>((int)op.omega[j])], sc));
-        rs[j] = rv;
-        r2 += mag2(rv);
+      if (ysl) {
+        // slot order: r[k] belongs to the row in transform slot scat_pos[k],
+        // y was stored in that order at t = 1; the next conventional row
+        // reads r with coalesced loads (no dependent index -> value chains)
+        for (int k = tid; k < m; k += nth) {
+          const unsigned p = op.scat_pos[k];
+          const int w = HAD ? (int)p : (int)brev_n(p, log2n);
+          const V rv = sub(ysl[k], scale(buf[padx<OLOGP>(w)], sc));
+          rs[k] = rv;
+          r2 += mag2(rv);
+        }
+      } else {
+        for (int j = tid; j < m; j += nth) {
+          const V rv = sub(y[j], scale(buf[padx<OLOGP>((int)op.omega[j])], sc));
+          rs[j] = rv;
+          r2 += mag2(rv);
+        }
       }
       buf_h0 = false;
       return sqrt(block_sum(r2, red));
@@ -350,7 +366,17 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
             __syncthreads();
             // rows in transform-slot order (op.scat_pos ascending): the lanes'
             // stores land on increasing slots instead of bit-reversed ones
-            for (int k = tid; k < m; k += nth) buf[padx<OLOGP>((int)op.scat_pos[k])] = r[op.scat_row[k]];
+            if (!ysl) {
+              for (int k = tid; k < m; k += nth) buf[padx<OLOGP>((int)op.scat_pos[k])] = r[op.scat_row[k]];
+            } else if (t == 1) {
+              for (int k = tid; k < m; k += nth) {
+                const V v = y[op.scat_row[k]];
+                ysl[k] = v;
+                buf[padx<OLOGP>((int)op.scat_pos[k])] = v;
+              }
+            } else {
+              for (int k = tid; k < m; k += nth) buf[padx<OLOGP>((int)op.scat_pos[k])] = rs[k];
+            }
             __syncthreads();
             block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth);
           }
@@ -868,6 +894,7 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.h0_ws = a.h0_ws;
   k.mag_ws = a.mag_ws;
   k.r_ws = a.r_ws;
+  k.ys_ws = p.msm ? nullptr : a.ys_ws;
   k.queue = a.queue;
   k.r_smem = p.rsm;
   k.w_smem = p.wsm;
