@@ -246,6 +246,22 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   OPALLOC(d.scat_pos, m * 4);
   OPALLOC(d.scat_row, m * 4);
   OPALLOC(d.scat_off, noff * 4);
+  std::vector<uint32_t> f16_omt;
+  std::vector<uint16_t> f16_yidx;
+  if (kind == FMP_FOURIER && n == 4096) {
+    std::vector<uint32_t> mask(256, 0), off(257, 0);
+    for (uint64_t i = 0; i < m; ++i) mask[om[i] & 255] |= 1u << (om[i] >> 8);
+    for (int u = 0; u < 256; ++u) off[u + 1] = off[u] + (uint32_t)__builtin_popcount(mask[u]);
+    f16_omt.resize(256);
+    for (int u = 0; u < 256; ++u) f16_omt[u] = (off[u] << 16) | mask[u];
+    f16_yidx.resize(m);
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint32_t u = om[i] & 255, j = om[i] >> 8;
+      f16_yidx[i] = (uint16_t)(off[u] + (uint32_t)__builtin_popcount(mask[u] & ((1u << j) - 1)));
+    }
+    OPALLOC(d.f16_omt, 256 * 4);
+    OPALLOC(d.f16_yidx, m * 2);
+  }
   OPALLOC(d.g64, n * 16);
   if (kind == FMP_FOURIER) {
     OPALLOC(d.tw64, n * 16);
@@ -308,7 +324,9 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
   if ((e = cudaMemcpyAsync(d.omega, om.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(d.scat_pos, spos.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
       (e = cudaMemcpyAsync(d.scat_row, srow.data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d.scat_off, soff.data(), noff * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      (e = cudaMemcpyAsync(d.scat_off, soff.data(), noff * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (d.f16_omt && (e = cudaMemcpyAsync(d.f16_omt, f16_omt.data(), 256 * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) ||
+      (d.f16_yidx && (e = cudaMemcpyAsync(d.f16_yidx, f16_yidx.data(), m * 2, cudaMemcpyHostToDevice, st)) != cudaSuccess))
     return cleanup(fail(FMP_ECUDA, "omega copy: %s", cudaGetErrorString(e)));
   if (kind == FMP_FOURIER) {
     if ((e = fmp::launch_twiddles(d, st)) != cudaSuccess)
@@ -354,7 +372,7 @@ int fmp_operator_destroy(fmp_op op) {
   cudaSetDevice(op->ctx->device);
   cudaStreamSynchronize(op->ctx->cur);
   DevOp& d = op->d;
-  for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.scat_off, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
+  for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.scat_off, (void*)d.f16_omt, (void*)d.f16_yidx, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
                   (void*)d.gr64, (void*)d.glat, (void*)d.fs_aoff, (void*)d.fs_apos, (void*)d.fs_arow,
                   (void*)d.fs_boff, (void*)d.fs_bpos, (void*)d.fs_brow})
     if (p) cudaFree(p);

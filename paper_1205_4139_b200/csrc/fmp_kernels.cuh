@@ -34,6 +34,11 @@ struct DevOp {
   uint32_t* scat_pos = nullptr;  // m, ascending slots
   uint32_t* scat_row = nullptr;  // m, index into the m-vector for each slot
   uint32_t* scat_off = nullptr;  // n/256 + 1: number of slots below 256 i (n >= 256)
+  // the fused solver's F16 rows (Fourier, n = 4096; fmp_omp_impl.cuh): per
+  // thread u < 256 the rows u + 256 j in Omega (mask) and the count of such
+  // rows of threads < u (off << 16), and each row's place in that order
+  uint32_t* f16_omt = nullptr;   // 256
+  uint16_t* f16_yidx = nullptr;  // m
   // two-pass transform (n = N1 N2, N1 = 2^fs_l1; fmp_transform_4s.cu), n >= 2^18:
   // Omega sorted by column (pos mod N2) for the pass-A scatter and by output
   // row k1 for the pass-B gather, each with per-column / per-row offsets

@@ -96,10 +96,78 @@ __device__ __forceinline__ int wofs(int T, int i, int j) {
   return j * T - (j * (j - 1)) / 2 + (i - j);
 }
 
+// ---------------------------------------------------------------- F16 path
+// Config 2's two-CTA solver (Fourier, n = 4096 = 16^3, 256 threads): every
+// transform of a conventional row or residual is three radix-16 passes with
+// one 16-point sub-problem per thread, and both ends stay in registers:
+//   * thread u ends the residual's forward transform holding X[u + 256 j]
+//     (natural order, j = 0..15), forms r at the rows of Omega among them and
+//     keeps those 16 values in registers; the next adjoint's first pass needs
+//     exactly them, because DIT group g = brev8(u) holds the bit-reversed rows
+//     brev12(16 g + j) = u + 256 brev4(j);
+//   * the adjoint's last pass leaves h[u + 256 j] in registers, where the
+//     identification reads |h|^2 (no store, no re-read);
+//   * the sparse estimate enters the forward transform from per-group lists
+//     of atoms (head / next, appended as atoms are selected): no zero-fill.
+// Shared memory moves 64 + 128 + 64 KB per transform instead of the radix-8
+// path's zero-fill, scatter, four read-write passes and gathers.  Padding:
+// p + p/16 + p/512 keeps every pass (and the brev8 store) bank-conflict free.
+__device__ __forceinline__ int pad16(int p) { return p + (p >> 4) + (p >> 9); }
+__device__ __forceinline__ int brev8(int x) { return (int)(__brev((unsigned)x) >> 24); }
+
+// twiddles of a radix-16 DIT sub-problem (offset o in a span 2^logS; the
+// power scheme of pass_one: <= 4 roundings per twiddle), then the 16-point DFT
+template <bool INV, class V, class TW>
+__device__ __forceinline__ void r16_step(V (&v)[16], int o, int logS, int log2n, const TW& tw) {
+  if (logS > 0) {
+    const int step = o << (log2n - logS - 4);
+    V w1 = tw(step);
+    if (INV) w1.y = -w1.y;
+    V p2 = w1, p4 = w1, p8 = w1;
+#pragma unroll
+    for (int q = 1; q < 16; ++q) {
+      V wq;
+      if (q == 1) wq = w1;
+      else if (q == 2) wq = p2 = cmul(w1, w1);
+      else if (q == 4) wq = p4 = cmul(p2, p2);
+      else if (q == 8) wq = p8 = cmul(p4, p4);
+      else {
+        wq = (q & 8) ? p8 : ((q & 4) ? p4 : p2);
+        const int rest = q & ((q & 8) ? 7 : ((q & 4) ? 3 : 1));
+        if (rest & 4) wq = cmul(wq, p4);
+        if (rest & 2) wq = cmul(wq, p2);
+        if (rest & 1) wq = cmul(wq, w1);
+      }
+      v[brev_inv<16>(q)] = cmul(v[brev_inv<16>(q)], wq);
+    }
+  }
+  dft_reg<16, INV>(v);
+}
+
+// passes 2 and 3 of the 4096-point transform (pass 1 stored by the caller;
+// the leading barrier publishes it); v returns X[tid + 256 j]
+template <bool INV, class V, class TW>
+__device__ __forceinline__ void f16_passes23(V* buf, V (&v)[16], const TW& tw, int tid) {
+  __syncthreads();
+  {
+    const int o = tid & 15, base = ((tid >> 4) << 8) + o;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = buf[pad16(base + 16 * j)];
+    r16_step<INV>(v, o, 4, 12, tw);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) buf[pad16(base + 16 * j)] = v[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = buf[pad16(tid + 256 * j)];
+  r16_step<INV>(v, tid, 8, 12, tw);
+}
+
 // GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
 // Fourier only); BUFG: transform buffer in global memory (n beyond smem);
 // NT threads per CTA, CT CTAs resident per SM (launch bounds)
-template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT>
+// F16: the register-resident radix-16 conventional rows (see above)
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT, bool F16 = false>
 __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[96];
@@ -157,7 +225,12 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   double* s_cval = reinterpret_cast<double*>(p); p += 8 * RCAP;
   unsigned* s_cand = reinterpret_cast<unsigned*>(p); p += 4 * RCAP;
   int* s_ncand = reinterpret_cast<int*>(p);
+  // F16 (never REFINE, same region): per 16-slot group the first selected
+  // atom (-1: none) and, per atom, the next one in its group
+  int16_t* s_head = reinterpret_cast<int16_t*>(s_cval);
+  int16_t* s_next = s_head + (F16 ? n / 16 : 0);
   constexpr bool REFINE = sizeof(typename scal<V>::T) == 4;
+  static_assert(!(F16 && REFINE), "F16 is the fp64 path");
   using X = typename wide_t<V>::T;
   const X* h0x_all = reinterpret_cast<const X*>(a.h0x);
 
@@ -189,6 +262,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
       return gram<HAD>(op, ga, gb);
     }
   };
+  // index of transform slot i in buf (padded layouts)
+  auto bp = [](int i) { return F16 ? pad16(i) : padx<OLOGP>(i); };
   const int ntiles = n >= 32 * RPT ? n / (32 * RPT) : 0;
   const bool regs_only = ntiles > 0 && ntiles <= nw;  // every thread owns <= 1 tile
 
@@ -230,7 +305,27 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     }
     const V* y = reinterpret_cast<const V*>(a.y) + prob * m;
     // no smem maps: y and r are kept in transform-slot order (ys_ws, r_ws)
-    V* ysl = (!s_map && a.ys_ws) ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
+    V* ysl = (!F16 && !s_map && a.ys_ws) ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
+    // F16: the measurements of this thread's rows (tid + 256 j in Omega) in
+    // thread order (DevOp::f16_omt / f16_yidx)
+    V* yc = F16 ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
+    // F16: first pass of the adjoint from r of this thread's rows (rr[j]: row
+    // tid + 256 j), stored to DIT group brev8(tid)
+    auto adj_pass1 = [&](V (&rr)[16]) {
+      if constexpr (F16) {
+        const int g = brev8(tid);
+        V v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = rr[brev_small<16>(j)];
+        dft_reg<16, true>(v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) buf[pad16(16 * g + j)] = v[j];
+      }
+    };
+    if constexpr (F16) {
+      for (int g = tid; g < n / 16; g += nth) s_head[g] = -1;
+      for (int j = tid; j < m; j += nth) yc[op.f16_yidx[j]] = y[j];
+    }
     const double tol = a.tol[prob];
     const X* h0x = REFINE ? h0x_all + prob * n : nullptr;
 
@@ -249,6 +344,51 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     // explicit residual r = y - Phi_Lambda x by one forward transform of the
     // sparse estimate (replaces update_residual, solvers.cpp:180-192)
     auto residual_explicit = [&](int cnt) -> double {
+      if constexpr (F16) {
+        __syncthreads();  // buf may still be read (fast rows' h0)
+        {
+          // pass 1 from the atom lists: thread tid owns group tid (slots
+          // 16 tid + j, atom q at slot brev12(lambda_q))
+          V v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = zv;
+          for (int q = s_head[tid]; q >= 0; q = s_next[q]) {
+            const int jj = (int)(brev_n(s_lam[q], log2n) & 15u);
+            V xv;
+            from_c128(s_x[q], xv);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j == jj) v[j] = xv;
+          }
+          dft_reg<16, false>(v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) buf[pad16(16 * tid + j)] = v[j];
+        }
+        V v[16];
+        f16_passes23<false>(buf, v, tw, tid);
+        // r = y - Phi x at this thread's rows of Omega (ascending j); the
+        // next conventional row's first pass follows at once (after the
+        // norm's barriers, which also end every read of this transform), so
+        // r never leaves registers
+        const uint32_t om = op.f16_omt[tid];
+        int c = (int)(om >> 16);
+        double r2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {  // v[j] becomes r of row tid + 256 j
+          if ((om >> j) & 1u) {
+            v[j] = sub(yc[c], scale(v[j], sc));
+            ++c;
+            r2 += mag2(v[j]);
+          } else {
+            v[j] = zv;
+          }
+        }
+        buf_h0 = false;
+        (void)cnt;
+        const double rn_ = sqrt(block_sum(r2, red));
+        adj_pass1(v);
+        return rn_;
+      }
       if (s_xmap && log2n >= OLOGP) {
         __syncthreads();
         first_pass_map8<OLOGP, false, HAD>(
@@ -352,7 +492,45 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         double m2[RPT];
         if (REFINE && tid == 0) *s_ncand = 0;  // read after the barriers below
         mark(5);
-        if (!fast_row) {
+        if (F16 && !fast_row) {
+          // conventional correlation: U^H scatter(r) (sensing.cpp:102-109),
+          // r in registers (t = 1: y)
+          if constexpr (F16) {
+            // (t >= 2: the first pass ran at the end of the previous
+            // iteration's residual)
+            if (t == 1) {
+              const uint32_t om = op.f16_omt[tid];
+              int c = (int)(om >> 16);
+              V rr[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if ((om >> j) & 1u) rr[j] = yc[c++];
+                else rr[j] = zv;
+              }
+              __syncthreads();  // yc was written by other threads; buf may still be read
+              adj_pass1(rr);
+            }
+            V v[16];
+            f16_passes23<true>(buf, v, tw, tid);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              // own slots: h0 (t = 1, kept for the fast rows), else |h|^2 in
+              // the slot's first 8 bytes, re-read by the identification scan
+              const int k = tid + 256 * j;
+              const V hv = scale(v[j], sc);
+              const double mm = mag2(hv);
+              if (t == 1) {
+                buf[pad16(k)] = hv;
+                h0w[k] = hv;
+              } else {
+                reinterpret_cast<double*>(buf)[2 * pad16(k)] = mm;
+              }
+              if (hrow) hrow[k] = hv;
+              best = fmax(best, mm);
+            }
+            buf_h0 = t == 1;
+          }
+        } else if (!fast_row) {
           // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
           const V* r = t == 1 ? y : rs;
           if (s_map && log2n >= OLOGP) {
@@ -397,7 +575,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           // fast correlation (kernel.cpp:209-303) from h0 and the staged c
           if (!buf_h0) {
             __syncthreads();
-            for (int k = tid; k < n; k += nth) buf[padx<OLOGP>(k)] = h0w[k];
+            for (int k = tid; k < n; k += nth) buf[bp(k)] = h0w[k];
             buf_h0 = true;
             __syncthreads();
           }
@@ -406,7 +584,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
               const int i0 = tile * 32 * RPT;
               V acc[RPT];
 #pragma unroll
-              for (int r = 0; r < RPT; ++r) acc[r] = buf[padx<OLOGP>(i0 + lane + 32 * r)];
+              for (int r = 0; r < RPT; ++r) acc[r] = buf[bp(i0 + lane + 32 * r)];
               fast_tile<V, HAD, RPT, GMODE == 2>(acc, i0, lane, n, gF, gH, s_lam, s_xn, s);
 #pragma unroll
               for (int r = 0; r < RPT; ++r) {
@@ -423,7 +601,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
             }
           } else {
             for (int i = tid; i < n; i += nth) {
-              V acc = buf[padx<OLOGP>(i)];
+              V acc = buf[bp(i)];
               fast_point<V, HAD, GMODE == 2>(acc, i, n, gF, gH, s_lam, s_xn, s);
               const double mm = mag2(acc);
               msc[i] = mm;
@@ -493,7 +671,16 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         unsigned pick;
         if constexpr (!REFINE) {
           unsigned first = 0xffffffffu;
-          if (!fast_row) {
+          if (F16 && !fast_row) {
+            if constexpr (F16) {
+              if (my_best >= cut)
+                for (int j = 0; j < 16; ++j) {
+                  const int q = pad16(tid + 256 * j);
+                  const double mm = t == 1 ? mag2(buf[q]) : reinterpret_cast<const double*>(buf)[2 * q];
+                  if (mm >= cut) { first = (unsigned)(tid + 256 * j); break; }
+                }
+            }
+          } else if (!fast_row) {
             // only a thread whose own maximum (over these same indices k) reaches
             // the band can hold the pick
             const double scv = t == 1 ? 1.0 : sc;
@@ -589,7 +776,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         if ((s_sel[pick >> 5] >> (pick & 31)) & 1u) break;
         // b_s = h0[pick], read early so its latency hides behind the row pass
         // (REFINE: the fp64 h0)
-        const V bpre = REFINE ? zv : (buf_h0 ? buf[padx<OLOGP>((int)pick)] : h0w[pick]);
+        const V bpre = REFINE ? zv : (buf_h0 ? buf[bp((int)pick)] : h0w[pick]);
         const double2 bpre64 = REFINE ? to_c128(h0x[pick]) : make_double2(0.0, 0.0);
         mark(2);
 
@@ -712,6 +899,11 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           s_lam[s] = pick;
           s_sel[pick >> 5] |= 1u << (pick & 31);
           if (s_xmap) s_xmap[HAD ? (int)pick : (int)brev_n(pick, log2n)] = (int16_t)s;
+          if constexpr (F16) {
+            const int g = (int)(brev_n(pick, log2n) >> 4);
+            s_next[s] = s_head[g];
+            s_head[g] = (int16_t)s;
+          }
           const double2 xs = make_double2(znew.x * invd, znew.y * invd);
           s_x[s] = xs;
           from_c128(make_double2(xs.x * xscale, xs.y * xscale), s_xn[s]);
@@ -790,12 +982,21 @@ struct OmpPlan {
   int off_g, off_r, off_w, off_tw, off_small, off_map, tw_a;
 };
 
+// the F16 conventional rows apply (config 2's two-CTA solver)
 template <class V, bool HAD>
-OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
+constexpr bool f16_type() { return !HAD && sizeof(V) == 16; }
+template <class V, bool HAD>
+bool f16_ok(const DevOp& op) {
+  return !HAD && sizeof(V) == 16 && op.n == 4096 && op.f16_omt && op.f16_yidx;
+}
+
+template <class V, bool HAD>
+OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   OmpPlan p{};
   const int64_t n = op.n, m = op.m;
   auto al = [](size_t b) { return ((b + 15) / 16) * 16; };
-  const size_t buf = al((size_t)(n + (n >> OLOGP)) * sizeof(V));
+  const size_t buf = f16 ? al((size_t)(n + n / 16 + n / 512) * sizeof(V))
+                         : al((size_t)(n + (n >> OLOGP)) * sizeof(V));
   const size_t gfull = al(HAD ? (size_t)n * 2 : (size_t)n * sizeof(V));
   const size_t ghalf = al((size_t)(n / 2 + 1) * sizeof(V));
   const size_t r = al((size_t)m * sizeof(V));
@@ -807,7 +1008,8 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
   const size_t tw = HAD ? 0 : al((lo_n + hi_n) * sizeof(V));
   const size_t small = al(3 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
                        al(4 * (size_t)((n + 31) / 32)) +
-                       (sizeof(typename scal<V>::T) == 4 ? (size_t)12 * RCAP + 16 : 0);
+                       (sizeof(typename scal<V>::T) == 4 ? (size_t)12 * RCAP + 16 : 0) +
+                       (f16 ? al(2 * (size_t)(n / 16)) + al(2 * (size_t)T) : 0);
   // ctas > 1: the SM's shared memory (optin + 1 KB) split between the CTAs,
   // less each CTA's 1 KB reservation and the kernel's static shared memory
   // (1936 bytes; omp_ctas_v confirms the residency with the occupancy API)
@@ -845,9 +1047,9 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas) {
   return p;
 }
 
-template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT>
+template <class V, bool HAD, int RPT, int GMODE, bool BUFG, int NT, int CT, bool F16 = false>
 void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
-  auto f = k_omp<V, HAD, RPT, GMODE, BUFG, NT, CT>;
+  auto f = k_omp<V, HAD, RPT, GMODE, BUFG, NT, CT, F16>;
   // the attribute is per device and only grows: set it when a launch needs
   // more than this instantiation was last given (saves a driver call per
   // launch in the latency regime)
@@ -862,17 +1064,17 @@ void launch_k(const OmpK& k, int grid, size_t smem, cudaStream_t st) {
   f<<<grid, NT, smem, st>>>(k);
 }
 
-template <class V, bool HAD, int RPT, bool BUFG, int NT, int CT>
+template <class V, bool HAD, int RPT, bool BUFG, int NT, int CT, bool F16 = false>
 void launch_g(const OmpK& k, int gmode, int grid, size_t smem, cudaStream_t st) {
-  if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG, NT, CT>(k, grid, smem, st);
-  else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG, NT, CT>(k, grid, smem, st);
-  else launch_k<V, HAD, RPT, 0, BUFG, NT, CT>(k, grid, smem, st);
+  if (gmode == 1) launch_k<V, HAD, RPT, 1, BUFG, NT, CT, F16>(k, grid, smem, st);
+  else if (!HAD && gmode == 2) launch_k<V, HAD, RPT, 2, BUFG, NT, CT, F16>(k, grid, smem, st);
+  else launch_k<V, HAD, RPT, 0, BUFG, NT, CT, F16>(k, grid, smem, st);
 }
 
-template <class V, bool HAD, int RPT, int NT, int CT>
+template <class V, bool HAD, int RPT, int NT, int CT, bool F16 = false>
 cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   const DevOp& op = *a.op;
-  const OmpPlan p = omp_plan<V, HAD>(op, a.max_iter, CT);
+  const OmpPlan p = omp_plan<V, HAD>(op, a.max_iter, CT, F16);
   if (p.total > (size_t)smem_optin() - 2048) return cudaErrorInvalidConfiguration;
   OmpK k{};
   k.op = op;
@@ -927,7 +1129,11 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
     else launch_g<V, HAD, RPT, false, NT, CT>(k, p.gmode, grid, p.total, st);
   } else {
     if (p.bufg) return cudaErrorInvalidConfiguration;
-    launch_g<V, HAD, RPT, false, NT, CT>(k, p.gmode, grid, p.total, st);
+    if constexpr (F16) {
+      if (!a.ys_ws || p.msm) return cudaErrorInvalidValue;
+      k.ys_ws = a.ys_ws;
+    }
+    launch_g<V, HAD, RPT, false, NT, CT, F16>(k, p.gmode, grid, p.total, st);
   }
   ++g_launches;
   return cudaGetLastError();
@@ -939,17 +1145,27 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
 // fills them; measured on config 2 (B200): 239 k against 227 k recoveries/s at
 // the best switch point of each.  Fourier only (the Hadamard lattice path
 // keeps its kernel table in shared memory).
+// FMP_OMP_F16=0: the radix-8 conventional rows in the two-CTA solver too
+// (timing comparisons)
+inline bool omp_f16_off() {
+  const char* e = getenv("FMP_OMP_F16");
+  return e && atoi(e) == 0;
+}
+
 template <class V, bool HAD>
 int omp_ctas_v(const DevOp& op, int64_t batch, int64_t T) {
   const char* e = getenv("FMP_OMP_CTAS");
   if (e && atoi(e) == 1) return 1;
   if (HAD || sizeof(V) < 8 || op.n < 32 * 8 * 8) return 1;
   if (batch < 2 * (int64_t)num_sms()) return 1;
-  const OmpPlan p = omp_plan<V, HAD>(op, T, 2);
+  const bool f16 = f16_ok<V, HAD>(op) && !omp_f16_off();
+  const OmpPlan p = omp_plan<V, HAD>(op, T, 2, f16);
   if (p.bufg) return 1;
   // the plan must really leave two CTAs resident
   int occ = 0;
   auto f = p.gmode == 2 ? k_omp<V, HAD, 8, 2, false, 256, 2> : k_omp<V, HAD, 8, 0, false, 256, 2>;
+  if constexpr (f16_type<V, HAD>())
+    if (f16) f = p.gmode == 2 ? k_omp<V, HAD, 8, 2, false, 256, 2, true> : k_omp<V, HAD, 8, 0, false, 256, 2, true>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.total);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 256, p.total);
   return occ >= 2 ? 2 : 1;
@@ -964,7 +1180,7 @@ void omp_info_v(const DevOp& op, int64_t batch, int64_t T, int* out4) {
   int nt = ctas == 2 ? 256 : OMP_THREADS;
   const char* e = getenv("FMP_OMP_NT");
   if (ctas == 1 && op.n == 32 * 8 * 4 && batch <= num_sms() && !(e && atoi(e) == 512)) nt = 128;
-  const OmpPlan p = omp_plan<V, HAD>(op, T, ctas);
+  const OmpPlan p = omp_plan<V, HAD>(op, T, ctas, ctas == 2 && f16_ok<V, HAD>(op) && !omp_f16_off());
   out4[0] = ctas;
   out4[1] = nt;
   out4[2] = p.gmode;
@@ -974,7 +1190,11 @@ void omp_info_v(const DevOp& op, int64_t batch, int64_t T, int* out4) {
 template <class V, bool HAD>
 cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
   if constexpr (!HAD && sizeof(V) >= 8) {
-    if (omp_ctas_v<V, HAD>(*a.op, a.batch, a.max_iter) == 2) return launch_omp_t<V, HAD, 8, 256, 2>(a, st);
+    if (omp_ctas_v<V, HAD>(*a.op, a.batch, a.max_iter) == 2) {
+      if constexpr (f16_type<V, HAD>())
+        if (f16_ok<V, HAD>(*a.op) && !omp_f16_off()) return launch_omp_t<V, HAD, 8, 256, 2, true>(a, st);
+      return launch_omp_t<V, HAD, 8, 256, 2>(a, st);
+    }
   }
   // latency regime (no more problems than SMs) at n = 1024: one 4-warp CTA
   // per problem, whose block-wide barriers and reductions are cheaper than
