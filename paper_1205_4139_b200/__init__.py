@@ -26,6 +26,7 @@ leading batch dimension.  ``*_dev`` helpers take torch CUDA tensors.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -59,6 +60,9 @@ def _sig(name, res, *args):
     f.restype = res
     f.argtypes = list(args)
     return f
+
+
+_DP = C.POINTER(C.c_double)
 
 
 class OmpConfig(C.Structure):
@@ -504,10 +508,10 @@ _PINNED_MIN_BATCH = 1024
 
 
 def _host_outs(specs, pinned=True):
-    """Several result buffers carved from ONE page-locked allocation (one
+    """Several result buffers carved from ONE allocation — page-locked (one
     trip through torch's host allocator per call instead of one per buffer;
-    each view keeps the block alive).  specs: (shape, dtype, zero) tuples.
-    pinned=False: plain numpy buffers (small batches)."""
+    each view keeps the block alive) or, pinned=False (small batches), plain
+    numpy arrays.  specs: (shape, dtype, zero) tuples."""
     if not pinned:
         return [np.zeros(shape, dt) if zero else np.empty(shape, dt) for shape, dt, zero in specs]
     sizes = [int(np.prod(shape, dtype=np.int64)) * np.dtype(dt).itemsize for shape, dt, _ in specs]
@@ -547,21 +551,35 @@ def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
     B, T, n = Y.shape[0], int(cfg.max_iterations), op.n
     if T < 1:
         raise InvalidArgument(1, "omp_solve: max_iterations must be >= 1")
-    # every entry of these is written by the solve (support / coeffs zero padded)
-    sup, co, sz, it, rn, ab, md, hl = _host_outs([
-        ((B, T), np.uint64, False), ((B, T), np.complex128, False), ((B,), np.uint64, False),
-        ((B,), np.uint64, False), ((B,), np.float64, False), ((B,), np.int32, False),
-        ((B, T), np.uint8, True),  # rows past the last iteration stay 0
-        ((B,), np.uint64, False)], pinned=B >= _PINNED_MIN_BATCH)
+    # every entry of these is written by the solve (support / coeffs zero
+    # padded, modes 0 past the last iteration)
+    specs = (((B, T), np.uint64), ((B, T), np.complex128), ((B,), np.uint64), ((B,), np.uint64),
+             ((B,), np.float64), ((B,), np.int32), ((B, T), np.uint8), ((B,), np.uint64))
+    if B >= _PINNED_MIN_BATCH:
+        outs = _host_outs([(sh, dt, False) for sh, dt in specs])
+        addr = [o.ctypes.data for o in outs]
+    else:
+        # small batches (the library stages them itself): one plain block,
+        # its address taken once (per-array ctypes lookups cost ~1 us each)
+        offs, tot = [], 0
+        for sh, dt in specs:
+            offs.append(tot)
+            tot += (math.prod(sh) * np.dtype(dt).itemsize + 63) & ~63
+        blk = np.empty(tot, np.uint8)
+        base = blk.ctypes.data
+        outs = [np.ndarray(sh, dt, blk, o) for (sh, dt), o in zip(specs, offs)]
+        addr = [base + o for o in offs]
+    sup, co, sz, it, rn, ab, md, hl = outs
     hist = np.zeros((B, T, n), Y.dtype) if cfg.record_correlations else None
     tol = None
     if tolerances is not None:
-        tarr = np.ascontiguousarray(np.broadcast_to(np.asarray(tolerances, np.float64), (B,)))
-        tol = tarr.ctypes.data_as(C.POINTER(C.c_double))
-    res = OmpResult(_ptr(sup), _ptr(co), _ptr(sz), _ptr(it), _ptr(rn), _ptr(ab), _ptr(md), _ptr(hl),
-                    _ptr(hist) if hist is not None else None)
+        tarr = np.asarray(tolerances, np.float64)
+        if tarr.shape != (B,) or not tarr.flags.c_contiguous:
+            tarr = np.ascontiguousarray(np.broadcast_to(tarr, (B,)))
+        tol = C.cast(tarr.ctypes.data, _DP)
+    res = OmpResult(*addr, hist.ctypes.data if hist is not None else None)
     c = _config(cfg, tol)
-    _check(_lib.fmp_omp_solve(op.handle, DTYPES[Y.dtype], _ptr(Y), B, C.byref(c), C.byref(res)))
+    _check(_lib.fmp_omp_solve(op.handle, DTYPES[Y.dtype], Y.ctypes.data, B, C.byref(c), C.byref(res)))
     return BatchResult(sup, co, sz, it, rn, ab.astype(bool), md, hl, hist)
 
 
