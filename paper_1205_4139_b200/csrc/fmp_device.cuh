@@ -374,10 +374,46 @@ __device__ __forceinline__ unsigned warp_min_u(unsigned v) {
   return v;
 }
 
+// reductions of the per-warp partials held by lanes 0..NWC-1 (the other
+// lanes hold the identity): log2(NWC) butterfly rounds then a broadcast of
+// lane 0, bitwise the same result as the full five-round butterfly (the
+// extra rounds only combine identities).  NWC = 0: unknown, full butterfly.
+template <int NWC>
+__device__ __forceinline__ double xsum_nw(double v) {
+  if constexpr (NWC <= 0 || NWC >= 32) {
+    return warp_sum(v);
+  } else {
+#pragma unroll
+    for (int o = NWC / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+}
+template <int NWC>
+__device__ __forceinline__ double xmax_nw(double v) {
+  if constexpr (NWC <= 0 || NWC >= 32) {
+    return warp_max(v);
+  } else {
+#pragma unroll
+    for (int o = NWC / 2; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+}
+template <int NWC>
+__device__ __forceinline__ unsigned xmin_u_nw(unsigned v) {
+  if constexpr (NWC <= 0 || NWC >= 32) {
+    return warp_min_u(v);
+  } else {
+#pragma unroll
+    for (int o = NWC / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return __shfl_sync(0xffffffffu, v, 0);
+  }
+}
+
 // block-wide reductions; `red` needs 32 doubles of shared scratch.  Every
 // thread receives the result.  Contains two __syncthreads(); LEAD = false
 // drops the leading one when the caller knows `red` is not being read.
-template <bool LEAD = true>
+// NWC: the block's warp count when known at compile time.
+template <bool LEAD = true, int NWC = 0>
 __device__ __forceinline__ double block_max(double v, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   v = warp_max(v);
@@ -385,8 +421,9 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   if (lane == 0) red[w] = v;
   __syncthreads();
   double r = lane < nw ? red[lane] : 0.0;
-  return warp_max(r);
+  return xmax_nw<NWC>(r);
 }
+template <int NWC = 0>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   v = warp_sum(v);
@@ -394,7 +431,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (lane == 0) red[w] = v;
   __syncthreads();
   double r = lane < nw ? red[lane] : 0.0;
-  return warp_sum(r);
+  return xsum_nw<NWC>(r);
 }
 // three sums at once; `red` needs 96 doubles
 __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red) {
@@ -413,7 +450,7 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
   b = warp_sum(lane < nw ? red[32 + lane] : 0.0);
   c = warp_sum(lane < nw ? red[64 + lane] : 0.0);
 }
-template <bool LEAD = true>
+template <bool LEAD = true, int NWC = 0>
 __device__ __forceinline__ unsigned block_min_u(unsigned v, unsigned* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   v = warp_min_u(v);
@@ -421,7 +458,7 @@ __device__ __forceinline__ unsigned block_min_u(unsigned v, unsigned* red) {
   if (lane == 0) red[w] = v;
   __syncthreads();
   unsigned r = lane < nw ? red[lane] : 0xffffffffu;
-  return warp_min_u(r);
+  return xmin_u_nw<NWC>(r);
 }
 
 }  // namespace fmp

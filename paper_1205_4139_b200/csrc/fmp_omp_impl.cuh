@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   __shared__ double red[96];
   __shared__ unsigned redu[32];
   __shared__ int s_prob, s_lost;
+  constexpr int NW = NT / 32;  // warps per CTA (block reductions)
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
       for (int i = tid; i < n; i += nth) s_xmap[i] = -1;
     double yy = 0.0;
     for (int j = tid; j < m; j += nth) yy += mag2(y[j]);
-    yy = block_sum(yy, red);
+    yy = block_sum<NW>(yy, red);
     double rn = sqrt(yy);
     double zz = 0.0;
     int s = 0, iters = 0, aborted = 0, tlast = 0;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         }
         buf_h0 = false;
         (void)cnt;
-        const double rn_ = sqrt(block_sum(r2, red));
+        const double rn_ = sqrt(block_sum<NW>(r2, red));
         adj_pass1(v);
         return rn_;
       }
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         }
       }
       buf_h0 = false;
-      return sqrt(block_sum(r2, red));
+      return sqrt(block_sum<NW>(r2, red));
     };
 
     // REFINE: the fp64 residual norm ||y - Phi_Lambda x|| (solvers.cpp:388-389)
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         const double rr = yv.x - ar * sc, ri = yv.y - ai * sc;
         r2 += rr * rr + ri * ri;
       }
-      return sqrt(block_sum(r2, red));
+      return sqrt(block_sum<NW>(r2, red));
     };
     // REFINE: fp64 correlation h_j = h0_j - sum_tau x_tau c[(j - lambda_tau)
     // mod N] (or c[j ^ lambda_tau]), the reference's fast_update value
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         // `red` was last read before the least-squares pass-2 barrier (or the
         // transform's barriers at t = 1): no leading barrier needed
         const double my_best = best;  // this thread's own maximum
-        best = block_max<false>(best, red);
+        best = block_max<false, NW>(best, red);
         mark(fast_row ? 1 : 0);
         if (!REFINE && best == 0.0) break;
         double cut = best * (1.0 - kTieBandRel);
@@ -705,7 +706,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
             for (int k = tid; k < n; k += nth)
               if (msc[k] >= cut) { first = (unsigned)k; break; }
           }
-          pick = block_min_u<false>(first, redu);  // redu: only used here
+          pick = block_min_u<false, NW>(first, redu);  // redu: only used here
         } else {
           scan([&](unsigned k) {
             const int c = atomicAdd(s_ncand, 1);
@@ -755,14 +756,14 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
             // own qualifying elements serially (max, then first in band)
             double b = 0.0;
             scan([&](unsigned k) { b = fmax(b, h64_serial(k)); return false; });
-            best64 = block_max(b, red);
+            best64 = block_max<true, NW>(b, red);
             const double cut64 = best64 * (1.0 - kTieBandRel);
             unsigned f = 0xffffffffu;
             scan([&](unsigned k) {
               if (h64_serial(k) >= cut64) { f = k; return true; }
               return false;
             });
-            pick = block_min_u(f, redu);
+            pick = block_min_u<true, NW>(f, redu);
           }
           if (a.rstats && tid == 0) {
             atomicAdd(a.rstats, 1ull);
@@ -837,9 +838,9 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         ll = lane < nw ? red[lane] : 0.0;
         lzr = lane < nw ? red[32 + lane] : 0.0;
         lzi = lane < nw ? red[64 + lane] : 0.0;
-        ll = warp_sum(ll);
-        lzr = warp_sum(lzr);
-        lzi = warp_sum(lzi);
+        ll = xsum_nw<NW>(ll);
+        lzr = xsum_nw<NW>(lzr);
+        lzi = xsum_nw<NW>(lzi);
         const double d2 = gamma - ll;
         // pivot floor as the reference's normal-equations path
         // (solvers.cpp:32,144); see DESIGN.md for the QR criterion
@@ -1200,7 +1201,9 @@ cudaError_t launch_omp_v(const OmpArgs& a, cudaStream_t st) {
   // per problem, whose block-wide barriers and reductions are cheaper than
   // those of 16 warps (config 1: 75.8 -> 65.9 us per recovery)
   if (a.op->n == 32 * 8 * 4 && a.batch <= num_sms()) {
-    const char* e = getenv("FMP_OMP_NT");  // FMP_OMP_NT=512: the 16-warp CTA (timing tools)
+    // FMP_OMP_NT=512 / 256: the 16- / 8-warp CTA (timing tools)
+    const char* e = getenv("FMP_OMP_NT");
+    if (e && atoi(e) == 256) return launch_omp_t<V, HAD, 4, 256, 1>(a, st);
     if (!(e && atoi(e) == 512)) return launch_omp_t<V, HAD, 8, 128, 1>(a, st);
   }
   // lanes own RPT outputs; pick RPT so that one tile per warp covers n
