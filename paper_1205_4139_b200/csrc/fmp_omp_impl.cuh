@@ -270,12 +270,13 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
 
   // opt-in phase profile (thread 0's clock between phase boundaries, which
   // all end in a block-wide barrier)
-  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  // (added straight to the global totals: a per-thread array here would
+  // live in local memory, and its loads / stores ran on every call)
   unsigned long long ph_last = clock64();
   auto mark = [&](int phase) {
     if (a.phase_ws && tid == 0) {
       const unsigned long long now = clock64();
-      ph[phase] += now - ph_last;
+      atomicAdd(a.phase_ws + phase, now - ph_last);
       ph_last = now;
     }
   };
@@ -972,8 +973,6 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
       if (a.hlen) a.hlen[prob] = (uint64_t)tlast;
     }
   }
-  if (a.phase_ws && tid == 0)
-    for (int i = 0; i < 6; ++i) atomicAdd(a.phase_ws + i, ph[i]);
 }
 
 struct OmpPlan {

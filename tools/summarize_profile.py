@@ -66,7 +66,7 @@ def main():
     with open(prefix + "_summary.md", "w") as f:
         f.write(f"# round {rnd} — {tag}\n\n")
         f.write(f"bench: {b['value']:.1f} {b['unit']} ({b['ms_per_step']:.3f} ms/step, mode "
-                f"{b['config']['mode']}), clocks {b['clocks']}\n\n")
+                f"{b.get('mode', b['config'].get('mode'))}), clocks {b['clocks']}\n\n")
         f.write("## launch list (ncu gpu__time_duration.sum, cold-cache, serialised)\n\n")
         f.write("| kernel | launches | total us | share |\n|---|---|---|---|\n")
         for r in ll:
