@@ -222,6 +222,13 @@ struct SolveConfig {
   LeastSquaresMethod ls_method = LeastSquaresMethod::IncrementalQR;
   bool fourier_symmetry = false;
   bool record_correlations = false;
+  // verify the solver's state after every iteration and throw
+  // std::logic_error like the reference (solvers.cpp:194-203, :394-401 for
+  // omp_solve: support size, residual orthogonal to the fitted columns to
+  // 1e-8 max(1, ||y||), residual norm not increasing by more than 1e-12;
+  // :527-533 for cosamp_solve: support within k, sorted, distinct).  The OMP
+  // checks recompute each iteration's state on the device after the solve
+  // (see omp_solve_batch); they are a debugging aid, not free
   bool check_invariants = false;
 };
 SolveConfig default_config(std::size_t k, double y_norm);

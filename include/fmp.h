@@ -71,6 +71,13 @@ typedef struct fmp_ctx_s* fmp_ctx;
 typedef struct fmp_op_s* fmp_op;
 
 int fmp_version(void);
+/* number of CUDA devices visible to this process (0 without a GPU) */
+int fmp_device_count(int* out);
+/* page-locked host memory (cudaHostAlloc, portable across devices): host
+ * buffers from here let the host-buffer solves overlap their copies with
+ * the solve (see fmp_omp_solve) */
+int fmp_host_alloc(size_t bytes, void** out);
+int fmp_host_free(void* p);
 /* calibrate the FMA pipe of the context's GPU: FMAs per second (fp64 when
  * is_double, else fp32) — the roofline denominator of the accumulate path */
 int fmp_fma_peak(fmp_ctx ctx, int is_double, double* fma_per_s);
@@ -185,6 +192,19 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch,
                   const fmp_omp_config* cfg, fmp_omp_result* out);
 int fmp_omp_solve_dev(fmp_op op, int dtype, const void* y, uint64_t batch,
                       const fmp_omp_config* cfg, fmp_omp_result* out, void* stream);
+/* The same over several GPUs: ops[i] is the operator built on GPU i's
+ * context (one fmp_operator_create per device, the same kind, n and rows).
+ * The batch is split into nops contiguous blocks (the first batch % nops
+ * one problem larger), each solved by fmp_omp_solve on its device from a
+ * host thread of its own; results land in `out` at their global positions.
+ * The problems are independent: no collective.  This is the multi-device
+ * form of the reference's solve-per-worker pool (fastmp_cli.cpp:276-303);
+ * the seeded command-line driver paper_1205_4139_b200/host/fmp_driver.cpp
+ * runs over it.  The first failing block's status and message are
+ * returned.  Page-locked y and result buffers (fmp_host_alloc) take the
+ * streamed path of fmp_omp_solve. */
+int fmp_omp_solve_multi(const fmp_op* ops, int nops, int dtype, const void* y, uint64_t batch,
+                        const fmp_omp_config* cfg, fmp_omp_result* out);
 
 /* ------------------------------------------------------- CoSaMP (batched) */
 /* cosamp_solve (solvers.hpp:73-78, solvers.cpp:413-544) with sparsity k over

@@ -112,6 +112,11 @@ _sig("fmp_fast_update", C.c_int, _vp, C.c_int, _vp, _vp, _vp, _u64, _u64, _vp, _
 _sig("fmp_fast_update_dev", C.c_int, _vp, C.c_int, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp)
 _sig("fmp_argmax_band", C.c_int, _vp, C.c_int, _vp, _u64, _u64, _vp)
 _sig("fmp_omp_solve", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig), C.POINTER(OmpResult))
+_sig("fmp_omp_solve_multi", C.c_int, _vp, C.c_int, C.c_int, _vp, _u64, C.POINTER(OmpConfig),
+     C.POINTER(OmpResult))
+_sig("fmp_device_count", C.c_int, C.POINTER(C.c_int))
+_sig("fmp_host_alloc", C.c_int, C.c_size_t, C.POINTER(_vp))
+_sig("fmp_host_free", C.c_int, _vp)
 _sig("fmp_omp_solve_dev", C.c_int, _vp, C.c_int, _vp, _u64, C.POINTER(OmpConfig),
      C.POINTER(OmpResult), _vp)
 _sig("fmp_cosamp_solve", C.c_int, _vp, C.c_int, _vp, _u64, _u64, C.POINTER(OmpConfig),
@@ -583,6 +588,38 @@ def omp_solve_batch(op: SensingOperator, Y, cfg: SolveConfig, tolerances=None,
     return BatchResult(sup, co, sz, it, rn, ab.astype(bool), md, hl, hist)
 
 
+def device_count() -> int:
+    """CUDA devices visible to this process (fmp_device_count)."""
+    v = C.c_int(0)
+    _check(_lib.fmp_device_count(C.byref(v)))
+    return int(v.value)
+
+
+def omp_solve_multi(ops, Y, cfg: SolveConfig, tolerances=None) -> BatchResult:
+    """omp_solve over a batch split across several GPUs (fmp_omp_solve_multi):
+    ops[i] is the operator built on GPU i (same kind, n and rows); contiguous
+    blocks of the batch, one host thread per device, no collective."""
+    Y = np.ascontiguousarray(np.asarray(Y))
+    if Y.ndim == 1:
+        Y = Y[None]
+    B, T = Y.shape[0], int(cfg.max_iterations)
+    sup = np.zeros((B, T), np.uint64)
+    co = np.zeros((B, T), np.complex128)
+    sz, it = np.zeros(B, np.uint64), np.zeros(B, np.uint64)
+    rn, ab = np.zeros(B), np.zeros(B, np.int32)
+    md, hl = np.zeros((B, T), np.uint8), np.zeros(B, np.uint64)
+    tarr = None
+    if tolerances is not None:
+        tarr = np.ascontiguousarray(np.broadcast_to(np.asarray(tolerances, np.float64), (B,)))
+    res = OmpResult(sup.ctypes.data, co.ctypes.data, sz.ctypes.data, it.ctypes.data, rn.ctypes.data,
+                    ab.ctypes.data, md.ctypes.data, hl.ctypes.data, None)
+    c = _config(cfg, C.cast(tarr.ctypes.data, _DP) if tarr is not None else None)
+    hs = (_vp * len(ops))(*[o.handle for o in ops])
+    _check(_lib.fmp_omp_solve_multi(hs, len(ops), DTYPES[Y.dtype], Y.ctypes.data, B, C.byref(c),
+                                    C.byref(res)))
+    return BatchResult(sup, co, sz, it, rn, ab.astype(bool), md, hl, None)
+
+
 def omp_solve(op: SensingOperator, y, cfg: SolveConfig, dtype=None) -> RecoveryResult:
     """omp_solve (solvers.hpp:70-71) for one measurement vector."""
     r = omp_solve_batch(op, np.asarray(y)[None], cfg, dtype=dtype)
@@ -1000,7 +1037,7 @@ def apply_adjoint_dev(op: SensingOperator, r, h_out=None, argmax_out=None,
 __all__ = [
     "Context", "SensingOperator", "CorrelationKernel", "compute_kernel", "fast_update",
     "argmax_magnitude", "SolveConfig", "default_config", "RecoveryResult", "omp_solve",
-    "omp_solve_batch", "crossover_iteration", "gpu_crossover", "gpu_crossover_for", "make_row_selection", "make_batch", "make_batch_dev", "dd_eval", "derive_seed",
+    "omp_solve_batch", "omp_solve_multi", "device_count", "crossover_iteration", "gpu_crossover", "gpu_crossover_for", "make_row_selection", "make_batch", "make_batch_dev", "dd_eval", "derive_seed",
     "FmpError", "InvalidArgument", "RankDeficientError", "Unsupported", "LIB_PATH",
     "least_squares", "IncrementalQR", "cosamp_solve", "cosamp_solve_batch", "cosamp_solve_dev", "adaptive_cosamp_uses_fast",
     "LargeShard", "LocalExchange", "sharded_solve", "large_solve",

@@ -24,6 +24,7 @@ _VOUT = os.environ.get("FMP_BUILD_OUT")
 OBJ = os.path.join(PKG, "_build") if not _VOUT else os.path.abspath(_VOUT) + "_obj"
 LIB = os.path.join(PKG, "libfmp_cuda.so") if not _VOUT else os.path.abspath(_VOUT) + ".so"
 FACADE = os.path.join(PKG, "libfastmp_b200.so")
+DRIVER = os.path.join(PKG, "fmp_driver")
 CXX = os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -73,8 +74,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"facade build failed:\n{r.stderr}")
+    # the seeded multi-GPU driver (C ABI only)
+    dsrc = os.path.join(PKG, "host", "fmp_driver.cpp")
+    if force or not os.path.exists(DRIVER) or os.path.getmtime(DRIVER) < max(
+            os.path.getmtime(dsrc), os.path.getmtime(LIB)):
+        cmd = [CXX, "-std=c++17", "-O2", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+               "-o", DRIVER, dsrc, LIB, "-lpthread", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError(f"driver build failed:\n{r.stderr}")
     if verbose:
-        print("built", LIB, "and", FACADE)
+        print("built", LIB, "and", FACADE, "and", DRIVER)
     return LIB
 
 

@@ -12,6 +12,7 @@
 #include <complex>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -33,6 +34,33 @@ thread_local int g_launch_count = 0;
 extern "C" {
 
 int fmp_version(void) { return 1; }
+
+int fmp_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(FMP_EINVAL, "null argument");
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FMP_ENOMEM, "page-locked host allocation (%zu bytes): %s", bytes, cudaGetErrorString(e));
+  }
+  return FMP_OK;
+}
+
+int fmp_host_free(void* p) {
+  if (p) CU(cudaFreeHost(p));
+  return FMP_OK;
+}
+
+int fmp_device_count(int* out) {
+  if (!out) return fail(FMP_EINVAL, "null argument");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *out = n;
+  return FMP_OK;
+}
 
 int fmp_set_phase_profiling(int enabled) {
   g_phase_prof = enabled;
@@ -1175,6 +1203,49 @@ int fmp_omp_solve(fmp_op op, int dtype, const void* y, uint64_t batch, const fmp
   if (cfg->record_correlations)
     CU(cudaMemcpyAsync(out->history, d.history, batch * T * n * eb, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  return FMP_OK;
+}
+
+// one host thread per device, contiguous blocks of the batch
+int fmp_omp_solve_multi(const fmp_op* ops, int nops, int dtype, const void* y, uint64_t batch,
+                        const fmp_omp_config* cfg, fmp_omp_result* out) {
+  if (!ops || nops < 1 || !cfg || !out) return fail(FMP_EINVAL, "null argument");
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i]) return fail(FMP_EINVAL, "null operator %d", i);
+    if (ops[i]->d.kind != ops[0]->d.kind || ops[i]->d.n != ops[0]->d.n || ops[i]->rows != ops[0]->rows)
+      return fail(FMP_EINVAL, "fmp_omp_solve_multi: operator %d differs from operator 0", i);
+  }
+  if (nops == 1) return fmp_omp_solve(ops[0], dtype, y, batch, cfg, out);
+  if (int s = omp_validate(ops[0], dtype, cfg)) return s;
+  const uint64_t T = cfg->max_iterations, m = (uint64_t)ops[0]->d.m, n = (uint64_t)ops[0]->d.n;
+  const size_t eb = fmp::elem_bytes(dtype);
+  std::vector<int> status(nops, FMP_OK);
+  std::vector<std::string> msg(nops);
+  std::vector<std::thread> th;
+  const uint64_t q = batch / nops, r = batch % nops;
+  for (int i = 0; i < nops; ++i) {
+    const uint64_t b0 = i * q + std::min<uint64_t>(i, r), nb = q + (i < (int)r ? 1 : 0);
+    if (!nb) continue;
+    th.emplace_back([=, &status, &msg]() {
+      fmp_omp_config c = *cfg;
+      if (cfg->tolerances) c.tolerances = cfg->tolerances + b0;
+      fmp_omp_result o = *out;
+      o.support = out->support + b0 * T;
+      o.coeffs = out->coeffs + 2 * b0 * T;
+      o.support_size = out->support_size + b0;
+      o.iterations = out->iterations + b0;
+      o.residual = out->residual + b0;
+      o.aborted = out->aborted + b0;
+      if (out->modes) o.modes = out->modes + b0 * T;
+      if (out->history_len) o.history_len = out->history_len + b0;
+      if (out->history) o.history = (char*)out->history + b0 * T * n * eb;
+      status[i] = fmp_omp_solve(ops[i], dtype, (const char*)y + b0 * m * eb, nb, &c, &o);
+      if (status[i] != FMP_OK) msg[i] = g_err;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < nops; ++i)
+    if (status[i] != FMP_OK) return fail(status[i], "device block %d: %s", i, msg[i].c_str());
   return FMP_OK;
 }
 
