@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     V* ysl = (!F16 && !s_map && a.ys_ws) ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
     // F16: the measurements of this thread's rows (tid + 256 j in Omega) in
     // thread order (DevOp::f16_omt / f16_yidx)
-    V* yc = F16 ? reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m : nullptr;
+    V* yc = F16 ? (a.r_smem ? rs : reinterpret_cast<V*>(a.ys_ws) + (size_t)blockIdx.x * m) : nullptr;
     // F16: first pass of the adjoint from r of this thread's rows (rr[j]: row
     // tid + 256 j), stored to DIT group brev8(tid)
     auto adj_pass1 = [&](V (&rr)[16]) {
@@ -1025,7 +1025,11 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   p.wsm = tot + w + gmin <= cap;  // W next: the least-squares phase is latency bound
   if (p.wsm) tot += w;
   p.gmode = 0;
-  if (!(HAD && !op.glat)) {
+  // F16: the kernel table stays in global memory (read through L1 by the
+  // fast rows and the Gram lookups), which leaves room for r's region, where
+  // the F16 rows keep the problem's measurements (read by every residual)
+  const char* gs = getenv("FMP_F16_GSMEM");
+  if (!(HAD && !op.glat) && !(f16 && !(gs && atoi(gs) == 1))) {
     if (tot + gfull <= cap) { p.gmode = 1; tot += gfull; }
     else if (!HAD && tot + ghalf <= cap) { p.gmode = 2; tot += ghalf; }
     // several CTAs per SM: the conjugate half stays in global memory, where
@@ -1034,7 +1038,7 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   p.rsm = tot + r <= cap;
   if (p.rsm) tot += r;
   const size_t mapb = 2 * al((size_t)((n + 7) / 8) * 8 * 2);  // row map + support map
-  p.msm = !p.bufg && m <= 32767 && T <= 32767 && tot + mapb <= cap;
+  p.msm = !f16 && !p.bufg && m <= 32767 && T <= 32767 && tot + mapb <= cap;
   if (p.msm) tot += mapb;
   p.total = tot;
   size_t off = p.bufg ? 0 : buf;

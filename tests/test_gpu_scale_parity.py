@@ -45,14 +45,24 @@ def _check(res, refs, coeff_tol, check_resid=True):
                 1e-12 * np.linalg.norm(r.coeffs), f"signal {b}"
 
 
-def test_config2_headline_variant(fmp, oracle):
+@pytest.mark.parametrize("variant,env,table", [
+    ("f16", {}, "global"),                                  # the bench kernel
+    ("f16_gsmem", {"FMP_F16_GSMEM": "1"}, "smem_conj_half"),  # F16 rows, table in smem
+    ("radix8", {"FMP_OMP_F16": "0"}, "smem_conj_half"),       # round 1's conventional rows
+])
+def test_config2_headline_variant(fmp, oracle, monkeypatch, variant, env, table):
     """bench.py's step: config 2 (N=4096, M=1024, K=64, c128) with a batch
-    large enough for two CTAs per SM; every 8th signal against the oracle."""
+    large enough for two CTAs per SM; every 8th signal against the oracle.
+    The default is the register-resident radix-16 conventional rows (F16)
+    with the kernel table read through L1 and y staged in shared memory; the
+    other two plans stay selectable (timing comparisons) and are checked too."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
     n, m, k, B = 4096, 1024, 64, 512
     rows = fmp.make_row_selection(n, m, fmp.derive_seed(2, 1 << 40))
     op = fmp.SensingOperator("fourier", n, rows)
     info = fmp.omp_plan_info(op, np.complex128, B, k)
-    assert info == {"ctas_per_sm": 2, "threads": 256, "kernel_table": "smem_conj_half",
+    assert info == {"ctas_per_sm": 2, "threads": 256, "kernel_table": table,
                     "buffer_in_global": False}
     Y, X, _ = fmp.make_batch("fourier", n, rows, k, B, base_seed=2, want_x=True)
     tol = 1e-9 * np.linalg.norm(Y, axis=1)
