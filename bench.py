@@ -77,6 +77,10 @@ def parse():
     p.add_argument("--batch", type=int, default=0)
     p.add_argument("--no-c3", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true",
+                   help="skip the host-buffer leg (profiling runs: under ncu's serialised "
+                        "kernels the streamed path's solver would wait for copies that "
+                        "cannot run beside it)")
     p.add_argument("--cpu-sample", type=int, default=0)
     p.add_argument("--solver", default="omp", choices=["omp", "cosamp"],
                    help="cosamp: CoSaMP with sparsity K on the same workload (SURVEY §8 f1)")
@@ -616,29 +620,31 @@ def our_arm(args, ws, rank, local):
                 "algorithmic": "Table-I correlation flops of the iterations actually run"}
 
     # end to end through the host-buffer C-ABI call (pinned input)
-    y_pin = torch.from_numpy(Y).pin_memory()
-    Yp = y_pin.numpy()
-    cfg = fmp.SolveConfig(max_iterations=T, residual_tolerance=0.0, correlation_mode=mname,
-                          fast_until=fu)
-    ctx.set_stream(None)
-    for _ in range(2):  # warm (page-locked result buffers, staging)
-        e2e_res = fmp.omp_solve_batch(op, Yp, cfg, tolerances=tol_h)
-    # each call timed on its own (host wall clock around the blocking call);
-    # the median over E2E_STEPS calls, max over ranks
-    e2e_t = []
-    for _ in range(E2E_STEPS):
-        barrier(ws)
-        t0 = time.perf_counter()
-        e2e_res = fmp.omp_solve_batch(op, Yp, cfg, tolerances=tol_h)
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_s = allreduce_max(float(np.median(e2e_t)), ws)
-    eb = Y.dtype.itemsize
-    e2e = {"value": B_all / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": int(B * m * eb + B * 8),
-           "d2h_bytes_per_step": int(B * T * 8 + B * T * 16 + B * 8 * 3 + B * 4),
-           "per": "rank (bytes per step on each GPU)",
-           "api": "fmp_omp_solve (host buffers, pinned y)",
-           "timing": f"median of {E2E_STEPS} calls, wall clock around each blocking call"}
+    e2e, e2e_res = None, None
+    if not args.no_e2e:
+        y_pin = torch.from_numpy(Y).pin_memory()
+        Yp = y_pin.numpy()
+        cfg = fmp.SolveConfig(max_iterations=T, residual_tolerance=0.0, correlation_mode=mname,
+                              fast_until=fu)
+        ctx.set_stream(None)
+        for _ in range(2):  # warm (page-locked result buffers, staging)
+            e2e_res = fmp.omp_solve_batch(op, Yp, cfg, tolerances=tol_h)
+        # each call timed on its own (host wall clock around the blocking call);
+        # the median over E2E_STEPS calls, max over ranks
+        e2e_t = []
+        for _ in range(E2E_STEPS):
+            barrier(ws)
+            t0 = time.perf_counter()
+            e2e_res = fmp.omp_solve_batch(op, Yp, cfg, tolerances=tol_h)
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_s = allreduce_max(float(np.median(e2e_t)), ws)
+        eb = Y.dtype.itemsize
+        e2e = {"value": B_all / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(B * m * eb + B * 8),
+               "d2h_bytes_per_step": int(B * T * 8 + B * T * 16 + B * 8 * 3 + B * 4),
+               "per": "rank (bytes per step on each GPU)",
+               "api": "fmp_omp_solve (host buffers, pinned y)",
+               "timing": f"median of {E2E_STEPS} calls, wall clock around each blocking call"}
 
     c3 = None
     if not args.no_c3 and rank == 0 and args.config == 2:
@@ -650,8 +656,11 @@ def our_arm(args, ws, rank, local):
         threads = cpu_threads()
         sample = args.cpu_sample or 32 * threads  # wraps around small batches
         v, dt, kind, res = run_cpu(Y, tol_h, rows, sample, "fast", threads)
-        same = float(np.mean([list(res[i].support) ==
-                              list(e2e_res.support[i % B, :int(e2e_res.support_size[i % B])])
+        if e2e_res is not None:
+            gsup, gsz = e2e_res.support, e2e_res.support_size
+        else:  # (--no-e2e) the device-resident solve's results
+            gsup, gsz = out["support"].cpu().numpy(), out["support_size"].cpu().numpy()
+        same = float(np.mean([list(res[i].support) == list(gsup[i % B, :int(gsz[i % B])])
                               for i in range(sample)]))
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"{sample} solves over the first {min(sample, B)} signals of the batch, reference omp_solve Fast mode, "

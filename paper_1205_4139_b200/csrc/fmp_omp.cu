@@ -8,6 +8,7 @@ cudaError_t launch_omp_c64(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_f64(const OmpArgs& a, cudaStream_t st);
 cudaError_t launch_omp_f32(const OmpArgs& a, cudaStream_t st);
 int omp_ctas_c128(const DevOp& op, int64_t batch, int64_t T);
+int omp_f16_c128(const DevOp& op, int64_t batch, int64_t T);
 int omp_ctas_c64(const DevOp& op, int64_t batch, int64_t T);
 
 void omp_info_c128(const DevOp& op, int64_t batch, int64_t T, int* out4);
@@ -44,6 +45,9 @@ int omp_gpu_fast_until(const DevOp& op, int dtype, int64_t batch, int64_t T) {
   // 4 log2(N) / 3; the Hadamard FWHT needs no twiddles
   const int64_t logn = op.log2n;
   if (op.kind == HADAMARD) return (int)(2 * logn);
+  // the two-CTA solver's F16 conventional rows (kernel table through L1):
+  // 2 log2(N) / 3 (config 2: custom:8 measured fastest of 1..16, 307 k/s)
+  if (dtype == C128 && omp_f16_c128(op, batch, T)) return (int)(2 * logn / 3);
   return (int)((omp_ctas(op, dtype, batch, T) == 2 ? 4 : 8) * logn / 3);
 }
 
