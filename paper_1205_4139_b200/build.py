@@ -33,15 +33,17 @@ SOURCES = ["fmp_omp_c128.cu", "fmp_omp_c64.cu", "fmp_omp_f64.cu", "fmp_omp_f32.c
 HEADERS = ["fmp_device.cuh", "fmp_kernels.cuh", "fmp_kcommon.cuh", "fmp_omp_impl.cuh", "fmp_capi_internal.cuh"]
 
 
-def _newest_dep() -> float:
-    deps = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "fmp.h")]
+def _newest_dep(src: str) -> float:
+    # fmp_omp_impl.cuh is included by the fmp_omp_<dtype>.cu units only
+    hs = [h for h in HEADERS if h != "fmp_omp_impl.cuh" or src.startswith("fmp_omp_")]
+    deps = [os.path.join(CSRC, h) for h in hs] + [os.path.join(ROOT, "include", "fmp.h")]
     return max(os.path.getmtime(d) for d in deps)
 
 
 def _compile(src: str, force: bool) -> str:
     path = os.path.join(CSRC, src)
     obj = os.path.join(OBJ, src + ".o")
-    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), _newest_dep()):
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), _newest_dep(src)):
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
     if src.endswith(".cpp"):

@@ -33,8 +33,14 @@ constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
 #define FMP_OLOGP 3
 #endif
 constexpr int OLOGP = FMP_OLOGP;  // transform-buffer padding period 2^OLOGP
-constexpr int LSG = 8;  // threads per row / column in the least-squares passes
-constexpr int LSU = 4;  // loads per thread issued together in those passes
+#ifndef FMP_LSG
+#define FMP_LSG 8
+#endif
+#ifndef FMP_LSU
+#define FMP_LSU 4
+#endif
+constexpr int LSG = FMP_LSG;  // threads per row / column in the least-squares passes
+constexpr int LSU = FMP_LSU;  // loads per thread issued together in those passes
 
 struct OmpK {
   DevOp op;
@@ -115,13 +121,23 @@ __device__ __forceinline__ int wofs(int T, int i, int j) {
 __device__ __forceinline__ int pad16(int p) { return p + (p >> 4) + (p >> 9); }
 __device__ __forceinline__ int brev8(int x) { return (int)(__brev((unsigned)x) >> 24); }
 
-// twiddles of a radix-16 DIT sub-problem (offset o in a span 2^logS; the
-// power scheme of pass_one: <= 4 roundings per twiddle), then the 16-point DFT
-template <bool INV, class V, class TW>
-__device__ __forceinline__ void r16_step(V (&v)[16], int o, int logS, int log2n, const TW& tw) {
-  if (logS > 0) {
-    const int step = o << (log2n - logS - 4);
-    V w1 = tw(step);
+// F16 twiddle tables in shared memory: lo[k] = W^k (k < 64), hi[k] = W^(64 k)
+// (k < 4): W^k = lo[k & 63] hi[k >> 6]
+template <class V>
+struct TwF16 {
+  const V* lo;
+  const V* hi;
+};
+
+// twiddles of a radix-16 DIT sub-problem (offset o in a span 2^LOGS of the
+// 4096-point transform): W^(o 2^(8 - LOGS)) from the two-level table, its
+// powers by products (the power scheme of pass_one: <= 4 roundings per
+// twiddle), then the 16-point DFT
+template <bool INV, int LOGS, class V>
+__device__ __forceinline__ void r16_step(V (&v)[16], int o, const TwF16<V>& tw) {
+  if constexpr (LOGS > 0) {
+    const int k = o << (8 - LOGS);
+    V w1 = cmul(tw.lo[k & 63], tw.hi[k >> 6]);
     if (INV) w1.y = -w1.y;
     V p2 = w1, p4 = w1, p8 = w1;
 #pragma unroll
@@ -145,22 +161,26 @@ __device__ __forceinline__ void r16_step(V (&v)[16], int o, int logS, int log2n,
 }
 
 // passes 2 and 3 of the 4096-point transform (pass 1 stored by the caller;
-// the leading barrier publishes it); v returns X[tid + 256 j]
-template <bool INV, class V, class TW>
-__device__ __forceinline__ void f16_passes23(V* buf, V (&v)[16], const TW& tw, int tid) {
-  __syncthreads();
+// the leading barrier publishes it); v returns X[tid + 256 j].
+// WARP1: pass 1 was stored by group = thread (the forward transform's atom
+// lists), so the 16 groups a middle-pass thread reads come from its own
+// half-warp and a warp barrier publishes them
+template <bool INV, bool WARP1, class V>
+__device__ __forceinline__ void f16_passes23(V* buf, V (&v)[16], const TwF16<V>& tw, int tid) {
+  if (WARP1) __syncwarp();
+  else __syncthreads();
   {
     const int o = tid & 15, base = ((tid >> 4) << 8) + o;
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = buf[pad16(base + 16 * j)];
-    r16_step<INV>(v, o, 4, 12, tw);
+    r16_step<INV, 4>(v, o, tw);
 #pragma unroll
     for (int j = 0; j < 16; ++j) buf[pad16(base + 16 * j)] = v[j];
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = buf[pad16(tid + 256 * j)];
-  r16_step<INV>(v, tid, 8, 12, tw);
+  r16_step<INV, 8>(v, tid, tw);
 }
 
 // GMODE: kernel table source (0 global, 1 smem full, 2 smem conjugate half,
@@ -172,6 +192,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ double red[96];
   __shared__ unsigned redu[32];
+  __shared__ double red2[F16 ? 32 : 1];  // F16: the residual norm's partials
   __shared__ int s_prob, s_lost;
   constexpr int NW = NT / 32;  // warps per CTA (block reductions)
   const DevOp& op = a.op;
@@ -201,7 +222,16 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   }
   // two-level twiddles (Fourier): lo[k] = W^k, hi[k] = W^(k 2^a)
   TwTwoLevel<V> tw{nullptr, nullptr, a.tw_a};
-  if constexpr (!HAD) {
+  TwF16<V> tw16{nullptr, nullptr};
+  if constexpr (F16) {
+    V* lo = reinterpret_cast<V*>(sm + a.off_tw);
+    V* hi = lo + 64;
+    const V* full = twiddles<V>(op);
+    for (int k = tid; k < 64; k += nth) lo[k] = full[k];
+    for (int k = tid; k < 4; k += nth) hi[k] = full[64 * k];
+    tw16.lo = lo;
+    tw16.hi = hi;
+  } else if constexpr (!HAD) {
     V* lo = reinterpret_cast<V*>(sm + a.off_tw);
     V* hi = lo + TwTwoLevel<V>::pad(1 << a.tw_a) + 1;
     const V* full = twiddles<V>(op);
@@ -347,7 +377,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
     // sparse estimate (replaces update_residual, solvers.cpp:180-192)
     auto residual_explicit = [&](int cnt) -> double {
       if constexpr (F16) {
-        __syncthreads();  // buf may still be read (fast rows' h0)
+        // (every earlier read of buf - fast rows, the identification scan -
+        // is followed by a block-wide barrier on every path that gets here)
         {
           // pass 1 from the atom lists: thread tid owns group tid (slots
           // 16 tid + j, atom q at slot brev12(lambda_q))
@@ -367,7 +398,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           for (int j = 0; j < 16; ++j) buf[pad16(16 * tid + j)] = v[j];
         }
         V v[16];
-        f16_passes23<false>(buf, v, tw, tid);
+        f16_passes23<false, true>(buf, v, tw16, tid);
         // r = y - Phi x at this thread's rows of Omega (ascending j); the
         // next conventional row's first pass follows at once (after the
         // norm's barriers, which also end every read of this transform), so
@@ -387,7 +418,13 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         }
         buf_h0 = false;
         (void)cnt;
-        const double rn_ = sqrt(block_sum<NW>(r2, red));
+        // one barrier: it ends every read of this transform's buffer before
+        // the next first pass overwrites it, and publishes the norm's
+        // per-warp partials
+        r2 = warp_sum(r2);
+        if (lane == 0) red2[warp] = r2;
+        __syncthreads();
+        const double rn_ = sqrt(xsum_nw<NW>(lane < NW ? red2[lane] : 0.0));
         adj_pass1(v);
         return rn_;
       }
@@ -513,22 +550,34 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
               adj_pass1(rr);
             }
             V v[16];
-            f16_passes23<true>(buf, v, tw, tid);
+            f16_passes23<true, false>(buf, v, tw16, tid);
+            if (t != 1 && !hrow) {
+              // |h|^2 into the slot's first 8 bytes, re-read by the
+              // identification scan; 1/sqrt N = 2^-6 here, so scaling |v|^2
+              // by 1/N gives bitwise the |h|^2 of the scaled h
+              const double s2 = sc * sc;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              // own slots: h0 (t = 1, kept for the fast rows), else |h|^2 in
-              // the slot's first 8 bytes, re-read by the identification scan
-              const int k = tid + 256 * j;
-              const V hv = scale(v[j], sc);
-              const double mm = mag2(hv);
-              if (t == 1) {
-                buf[pad16(k)] = hv;
-                h0w[k] = hv;
-              } else {
-                reinterpret_cast<double*>(buf)[2 * pad16(k)] = mm;
+              for (int j = 0; j < 16; ++j) {
+                const double mm = mag2(v[j]) * s2;
+                reinterpret_cast<double*>(buf)[2 * pad16(tid + 256 * j)] = mm;
+                best = fmax(best, mm);
               }
-              if (hrow) hrow[k] = hv;
-              best = fmax(best, mm);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                // own slots: h0 (t = 1, kept for the fast rows), else |h|^2
+                const int k = tid + 256 * j;
+                const V hv = scale(v[j], sc);
+                const double mm = mag2(hv);
+                if (t == 1) {
+                  buf[pad16(k)] = hv;
+                  h0w[k] = hv;
+                } else {
+                  reinterpret_cast<double*>(buf)[2 * pad16(k)] = mm;
+                }
+                if (hrow) hrow[k] = hv;
+                best = fmax(best, mm);
+              }
             }
             buf_h0 = t == 1;
           }
@@ -1005,7 +1054,8 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   // two-level twiddle tables, each padded i + i/8 (TwTwoLevel)
   const size_t lo_n = ((size_t)1 << p.tw_a) + ((size_t)1 << p.tw_a) / 8 + 1;
   const size_t hi_n = ((size_t)n >> p.tw_a) + ((size_t)n >> p.tw_a) / 8 + 1;
-  const size_t tw = HAD ? 0 : al((lo_n + hi_n) * sizeof(V));
+  // (F16: 64 + 4 two-level entries, unpadded)
+  const size_t tw = HAD ? 0 : (f16 ? al((size_t)68 * sizeof(V)) : al((lo_n + hi_n) * sizeof(V)));
   const size_t small = al(3 * 16 * (size_t)T) + al(sizeof(V) * (size_t)T) + al(4 * (size_t)T) +
                        al(4 * (size_t)((n + 31) / 32)) +
                        (sizeof(typename scal<V>::T) == 4 ? (size_t)12 * RCAP + 16 : 0) +
@@ -1022,14 +1072,18 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   const size_t gmin = HAD ? gfull : ghalf;
   p.bufg = tot + buf > cap;
   if (!p.bufg) tot += buf;
-  p.wsm = tot + w + gmin <= cap;  // W next: the least-squares phase is latency bound
+  // W next: the least-squares phase is latency bound.  F16 leaves the kernel
+  // table in global memory (read through L1 by the fast rows and the Gram
+  // lookups) and gives W the room; the problem's measurements (thread order,
+  // 16 KB) then stay in the CTA's global workspace, read once per residual
+  // (measured on config 2: W in smem / y in L2 318 k recoveries/s, y in smem
+  // / W in L2 308 k)
+  const char* gs = getenv("FMP_F16_GSMEM");
+  const bool f16g = f16 && !(gs && atoi(gs) == 1);  // F16 with the table in global memory
+  p.wsm = f16g ? tot + w <= cap : tot + w + gmin <= cap;
   if (p.wsm) tot += w;
   p.gmode = 0;
-  // F16: the kernel table stays in global memory (read through L1 by the
-  // fast rows and the Gram lookups), which leaves room for r's region, where
-  // the F16 rows keep the problem's measurements (read by every residual)
-  const char* gs = getenv("FMP_F16_GSMEM");
-  if (!(HAD && !op.glat) && !(f16 && !(gs && atoi(gs) == 1))) {
+  if (!(HAD && !op.glat) && !f16g) {
     if (tot + gfull <= cap) { p.gmode = 1; tot += gfull; }
     else if (!HAD && tot + ghalf <= cap) { p.gmode = 2; tot += ghalf; }
     // several CTAs per SM: the conjugate half stays in global memory, where

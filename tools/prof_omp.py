@@ -20,6 +20,7 @@ def main():
     p.add_argument("--batch", type=int, default=512)
     p.add_argument("--dtype", default="f64")
     p.add_argument("--reps", type=int, default=2)
+    p.add_argument("--fu", type=int, default=12)
     a = p.parse_args()
     import torch
     import paper_1205_4139_b200 as fmp
@@ -35,7 +36,7 @@ def main():
         y = torch.from_numpy(Y).cuda()
         tol = torch.from_numpy(1e-9 * np.linalg.norm(Y, axis=1)).cuda()
         out = fmp.alloc_dev_result(a.batch, k)
-        cfg = fmp.SolveConfig(k, 0.0, a.mode, fast_until=12)
+        cfg = fmp.SolveConfig(k, 0.0, a.mode, fast_until=a.fu)
         for _ in range(a.reps):
             fmp.omp_solve_dev(op, y, cfg, out, tolerances=tol, stream=st.cuda_stream)
     else:

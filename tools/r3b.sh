@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_scale_parity.py tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/r3b_tests.log 2>&1; tail -3 gpurun_out/r3b_tests.log
+cp paper_1205_4139_b200/libfmp_cuda.so /tmp/base.so
+for v in _variants/*.so; do
+  cp "$v" paper_1205_4139_b200/libfmp_cuda.so
+  echo "== $v"; timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-c3 --no-e2e --mode gpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'])"
+done
+cp /tmp/base.so paper_1205_4139_b200/libfmp_cuda.so
+echo "== new default"; timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu --no-c3 --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['mode_step_ms'])"
+timeout 300 python tools/phases.py 1184 --modes custom:8,custom:12,custom:16,conventional 2>&1 | tail -4
