@@ -33,14 +33,15 @@ constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
 #define FMP_OLOGP 3
 #endif
 constexpr int OLOGP = FMP_OLOGP;  // transform-buffer padding period 2^OLOGP
-#ifndef FMP_LSG
-#define FMP_LSG 8
+// least-squares passes: LSG threads per row / column, LSU loads per thread
+// issued together.  W in L2 or 512 threads: 8 / 4 (measured best, round 1);
+// the F16 plan (256 threads, W in smem, T <= 64 rows in one sweep): 4 / 4
+#ifndef FMP_LSG16
+#define FMP_LSG16 4
 #endif
-#ifndef FMP_LSU
-#define FMP_LSU 4
+#ifndef FMP_LSU16
+#define FMP_LSU16 4
 #endif
-constexpr int LSG = FMP_LSG;  // threads per row / column in the least-squares passes
-constexpr int LSU = FMP_LSU;  // loads per thread issued together in those passes
 
 struct OmpK {
   DevOp op;
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   __shared__ double red2[F16 ? 32 : 1];  // F16: the residual norm's partials
   __shared__ int s_prob, s_lost;
   constexpr int NW = NT / 32;  // warps per CTA (block reductions)
+  constexpr int LSG = F16 ? FMP_LSG16 : 8, LSU = F16 ? FMP_LSU16 : 4;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
