@@ -333,8 +333,21 @@ int fmp_operator_create(fmp_ctx ctx, int kind, uint64_t n, const uint64_t* rows,
       OPALLOC(d.fold_off[q], (rows_per_block + 1) * 4);
     }
   }
+  std::vector<uint2> om_wr;
+  if (kind == FMP_HADAMARD && n >= 4096) {
+    om_wr.assign(n / 32, make_uint2(0u, 0u));
+    for (uint64_t i = 0; i < m; ++i) om_wr[om[i] >> 5].x |= 1u << (om[i] & 31u);
+    uint32_t run = 0;
+    for (uint64_t w = 0; w < n / 32; ++w) {
+      om_wr[w].y = run;
+      run += (uint32_t)__builtin_popcount(om_wr[w].x);
+    }
+    OPALLOC(d.om_wr, (n / 32) * 8);
+  }
 #undef OPALLOC
   cudaStream_t st = ctx->cur;
+  if (d.om_wr && (e = cudaMemcpyAsync(d.om_wr, om_wr.data(), om_wr.size() * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cleanup(fail(FMP_ECUDA, "Omega bitmap: %s", cudaGetErrorString(e)));
   for (int q = 0; q < 4; ++q)
     if (d.fold_tab[q] &&
         ((e = cudaMemcpyAsync(d.fold_tab[q], fold_tab[q].data(), m * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
@@ -402,7 +415,7 @@ int fmp_operator_destroy(fmp_op op) {
   DevOp& d = op->d;
   for (void* p : {(void*)d.omega, (void*)d.scat_pos, (void*)d.scat_row, (void*)d.scat_off, (void*)d.f16_omt, (void*)d.f16_yidx, (void*)d.tw64, (void*)d.tw32, (void*)d.g64, (void*)d.g32,
                   (void*)d.gr64, (void*)d.glat, (void*)d.fs_aoff, (void*)d.fs_apos, (void*)d.fs_arow,
-                  (void*)d.fs_boff, (void*)d.fs_bpos, (void*)d.fs_brow})
+                  (void*)d.fs_boff, (void*)d.fs_bpos, (void*)d.fs_brow, (void*)d.om_wr})
     if (p) cudaFree(p);
   for (int q = 0; q < 4; ++q) {
     if (d.fold_tab[q]) cudaFree(d.fold_tab[q]);

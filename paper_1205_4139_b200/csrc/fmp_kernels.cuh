@@ -55,6 +55,11 @@ struct DevOp {
   // m | ih << 20 | j << 26, with B/32 + 1 per-row offsets; null if unused
   uint32_t* fold_tab[4] = {};
   uint32_t* fold_off[4] = {};
+  // Hadamard, n >= 2^12: Omega as a bitmap with running counts, per word w of
+  // 32 positions {mask of the positions in Omega, number of Omega's rows
+  // below 32 w}: a row of 32 inputs is r[rank .. rank + popc(mask)) (Omega is
+  // ascending), which the register fold walks without any table
+  uint2* om_wr = nullptr;  // n / 32
 };
 
 struct TransformArgs {

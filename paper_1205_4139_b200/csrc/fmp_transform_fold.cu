@@ -42,6 +42,83 @@ __device__ __forceinline__ void wht_regs(V* v) {
   }
 }
 
+// packed fp32 pairs (Blackwell FADD2: two IEEE adds per instruction)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(reinterpret_cast<unsigned long long&>(a)), "l"(reinterpret_cast<unsigned long long&>(b)));
+  return reinterpret_cast<float2&>(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(reinterpret_cast<unsigned long long&>(a)), "l"(reinterpret_cast<unsigned long long&>(b)));
+  return reinterpret_cast<float2&>(r);
+}
+
+// N elements of one register tile.  The generic tile is a plain array; the
+// f32 tile keeps elements 2k, 2k + 1 as one packed pair, so every butterfly
+// stage above the first is one FADD2 per two outputs, and the c64 tile adds
+// its (re, im) pairs the same way.  get / set take compile-time indices
+// (callers unroll), so everything stays in registers.
+template <class V, int N>
+struct Tile {
+  V v[N];
+  __device__ __forceinline__ V get(int j) const { return v[j]; }
+  __device__ __forceinline__ void set(int j, V x) { v[j] = x; }
+  template <int R>
+  __device__ __forceinline__ void wht() { wht_regs<R>(v); }
+};
+template <int N>
+struct Tile<float2, N> {
+  float2 v[N];
+  __device__ __forceinline__ float2 get(int j) const { return v[j]; }
+  __device__ __forceinline__ void set(int j, float2 x) { v[j] = x; }
+  template <int R>
+  __device__ __forceinline__ void wht() {
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+#pragma unroll
+      for (int j = 0; j < (1 << R); ++j) {
+        if (j & (1 << s)) continue;
+        const float2 a = v[j], b = v[j + (1 << s)];
+        v[j] = add2(a, b);
+        v[j + (1 << s)] = sub2(a, b);
+      }
+    }
+  }
+};
+template <int N>
+struct Tile<float, N> {
+  float2 p[N / 2];
+  __device__ __forceinline__ float get(int j) const { return (j & 1) ? p[j >> 1].y : p[j >> 1].x; }
+  __device__ __forceinline__ void set(int j, float x) {
+    if (j & 1) p[j >> 1].y = x;
+    else p[j >> 1].x = x;
+  }
+  template <int R>
+  __device__ __forceinline__ void wht() {
+#pragma unroll
+    for (int k = 0; k < (1 << R) / 2; ++k) {
+      const float a = p[k].x, b = p[k].y;
+      p[k].x = a + b;
+      p[k].y = a - b;
+    }
+#pragma unroll
+    for (int s = 1; s < R; ++s) {
+#pragma unroll
+      for (int k = 0; k < (1 << R) / 2; ++k) {
+        if (k & (1 << (s - 1))) continue;
+        const float2 a = p[k], b = p[k + (1 << (s - 1))];
+        p[k] = add2(a, b);
+        p[k + (1 << (s - 1))] = sub2(a, b);
+      }
+    }
+  }
+};
+
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
@@ -56,18 +133,18 @@ __device__ __forceinline__ void fold_pass(V* z, V* __restrict__ out, double sc, 
   for (int g = tid; g < G; g += NTH) {
     const int gl = g & ((1 << LO) - 1), gh = g >> LO;
     const int base = (gh << (LO + R)) + gl;
-    V v[1 << R];
+    // LO >= R1: element j sits (j << LO) + (j << (LO - R1)) padded slots
+    // after the group's first (compile-time offsets)
+    static_assert(LO >= R1, "pass bits start above the row bits");
+    V* zp = z + base + (base >> R1);
+    Tile<V, 1 << R> v;
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) v.set(j, zp[(j << LO) + (j << (LO - R1))]);
+    v.template wht<R>();
 #pragma unroll
     for (int j = 0; j < (1 << R); ++j) {
-      const int i = base + (j << LO);
-      v[j] = z[i + (i >> R1)];
-    }
-    wht_regs<R>(v);
-#pragma unroll
-    for (int j = 0; j < (1 << R); ++j) {
-      const int i = base + (j << LO);
-      if constexpr (LAST) st_stream(out + i, scale(v[j], sc));
-      else z[i + (i >> R1)] = v[j];
+      if constexpr (LAST) st_stream(out + base + (j << LO), scale(v.get(j), sc));
+      else zp[(j << LO) + (j << (LO - R1))] = v.get(j);
     }
   }
 }
@@ -249,6 +326,147 @@ __global__ void __launch_bounds__(NTH, 1) k_wht_fold(const uint32_t* __restrict_
   }
 }
 
+// Register fold (f32, S = 2^LS <= 8 input blocks).  Thread
+// g still owns row g of every block, but walks no table: Omega is ascending,
+// so the inputs of row g in input block ih are the contiguous run
+// r[rank, rank + popc(mask)) of DevOp::om_wr[ih B/32 + g], whose two words
+// per block the thread keeps in registers for the whole launch.  One walk
+// visits the S x 32 (block, position) slots with predicated loads and adds
+// (no data-dependent control flow, signs known at compile time), forming the
+// rows of NZ output blocks in registers, where the first register pass
+// follows at once; sums run in ascending input block order like k_wht_fold,
+// so the two kernels agree bitwise.
+template <class V, int LOGB, int R2, int R3, int NTH, int NZ, int LS>
+__global__ void __launch_bounds__(NTH, 1) k_wht_fold_reg(const uint2* __restrict__ om_wr, int m,
+                                                         const V* __restrict__ in, V* __restrict__ out,
+                                                         int64_t batch, double sc, int use_bulk) {
+  constexpr int R1 = 5, S = 1 << LS;
+  static_assert(R1 + R2 + R3 == LOGB && NTH == (1 << (LOGB - R1)) && S % NZ == 0, "pass widths");
+  constexpr int B = 1 << LOGB;
+  constexpr int ZN = B + (B >> R1);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t mbar;
+  V* z = reinterpret_cast<V*>(smem_raw);  // NZ blocks
+  V* rb = z + NZ * ZN;                    // m values (+ one pad element)
+  const int tid = threadIdx.x;
+  const uint32_t rbytes = (uint32_t)m * (uint32_t)sizeof(V);
+  int64_t b = blockIdx.x;
+  if (b >= batch) return;
+  if (tid == 0 && use_bulk) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t wd[S], rk[S];
+#pragma unroll
+  for (int ih = 0; ih < S; ++ih) {
+    const uint2 e = om_wr[ih * NTH + tid];
+    wd[ih] = e.x;
+    rk[ih] = e.y;
+  }
+  __syncthreads();
+  if (use_bulk) {
+    if (tid == 0) bulk_load(rb, in + b * m, rbytes, &mbar);
+  } else {
+    for (int k = tid; k < m; k += NTH) rb[k] = in[b * m + k];
+    __syncthreads();
+  }
+  const V zero = zero_of(V{});
+  for (uint32_t it = 0; b < batch; b += gridDim.x, ++it) {
+    if (use_bulk) mbar_wait(&mbar, it & 1);
+    V* ob = out + b * ((int64_t)S << LOGB);
+#pragma unroll
+    for (int khi0 = 0; khi0 < S; khi0 += NZ) {
+      Tile<V, 32> acc[NZ];
+#pragma unroll
+      for (int w = 0; w < NZ; ++w)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[w].set(j, zero);
+#pragma unroll
+      for (int ih = 0; ih < S; ++ih) {
+        const V* rp = rb + rk[ih];
+        const uint32_t wdi = wd[ih];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (wdi & (1u << j)) {
+            const V x = *rp++;
+#pragma unroll
+            for (int w = 0; w < NZ; ++w)
+              acc[w].set(j, (__builtin_popcount((unsigned)((khi0 + w) & ih)) & 1) ? sub(acc[w].get(j), x)
+                                                                                 : add(acc[w].get(j), x));
+          }
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < NZ; ++w) {
+        acc[w].template wht<R1>();
+        V* row = z + w * ZN + tid * 33;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) row[j] = acc[w].get(j);
+      }
+      __syncthreads();
+      if (khi0 + NZ >= S) {
+        // every read of this vector's r is done: stage the next one
+        const int64_t nb = b + gridDim.x;
+        if (nb < batch && use_bulk && tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          bulk_load(rb, in + nb * m, rbytes, &mbar);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < NZ; ++w) {
+        V* zw = z + w * ZN;
+        V* o = ob + ((int64_t)(khi0 + w) << LOGB);
+        if constexpr (R3 == 0) {
+          fold_pass<V, LOGB, R1, R1, R2, NTH, true>(zw, o, sc, tid);
+        } else {
+          fold_pass<V, LOGB, R1, R1, R2, NTH, false>(zw, o, sc, tid);
+          __syncthreads();
+          fold_pass<V, LOGB, R1, R1 + R2, R3, NTH, true>(zw, o, sc, tid);
+        }
+      }
+      __syncthreads();
+    }
+    if (!use_bulk) {
+      const int64_t nb = b + gridDim.x;
+      if (nb < batch) {
+        for (int k = tid; k < m; k += NTH) rb[k] = in[nb * m + k];
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <class V, int LOGB, int R2, int R3, int NZ, int LS>
+cudaError_t launch_fold_reg(const TransformArgs& a, cudaStream_t st) {
+  const DevOp& op = *a.op;
+  constexpr int B = 1 << LOGB, NTH = B >> 5;
+  if (!op.om_wr || op.log2n - LOGB != LS || a.batch < 64) return cudaErrorNotSupported;
+  const int64_t m = op.m;
+  const size_t smem = (size_t)NZ * (B + (B >> 5)) * sizeof(V) + (size_t)((m + 4) & ~3) * sizeof(V);
+  if (smem + 1024 > (size_t)smem_optin()) return cudaErrorNotSupported;
+  auto kern = k_wht_fold_reg<V, LOGB, R2, R3, NTH, NZ, LS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = std::min<int64_t>(a.batch, (int64_t)num_sms());
+  const bool bulk = ((uintptr_t)a.in % 16 == 0) && ((m * (int64_t)sizeof(V)) % 16 == 0);
+  kern<<<(unsigned)grid, NTH, smem, st>>>(op.om_wr, (int)m, (const V*)a.in, (V*)a.out, a.batch,
+                                          1.0 / sqrt((double)op.n), bulk ? 1 : 0);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// the register fold for the block counts it is built for, else the table walk
+template <class V, int LOGB, int R2, int R3, int NZ>
+cudaError_t launch_fold_reg_any(const TransformArgs& a, cudaStream_t st) {
+  const int ls = a.op->log2n - LOGB;
+  const char* fe = getenv("FMP_FOLD");  // FMP_FOLD=4: the table walk (timing tools)
+  if (fe && atoi(fe) == 4) return cudaErrorNotSupported;
+  if (ls == 1) return launch_fold_reg<V, LOGB, R2, R3, (NZ > 2 ? 2 : NZ), 1>(a, st);
+  if (ls == 2) return launch_fold_reg<V, LOGB, R2, R3, NZ, 2>(a, st);
+  if (ls == 3) return launch_fold_reg<V, LOGB, R2, R3, NZ, 3>(a, st);
+  return cudaErrorNotSupported;
+}
+
 template <class V, int LOGB, int R2, int R3, int NZ>
 cudaError_t launch_fold_k(const TransformArgs& a, cudaStream_t st) {
   const DevOp& op = *a.op;
@@ -299,6 +517,14 @@ cudaError_t launch_wht_fold(const TransformArgs& a, cudaStream_t st) {
   const char* e = getenv("FMP_FOLD");  // FMP_FOLD=-1: job queue instead (timing tools)
   if (e && atoi(e) < 0) return cudaErrorNotSupported;
   const int plan = e ? atoi(e) : 0;
+  if (a.dtype == F32) {
+    // register fold (no table walk), when built for this block count.  f32
+    // only: with 8-byte elements one walk feeds a single output block and
+    // the 32-element accumulator tile spills (config 3: f64 0.39 vs 0.26 ms,
+    // c64 0.40 vs 0.27 ms for the table walk)
+    const cudaError_t r = launch_fold_reg_any<float, 14, 5, 4, 2>(a, st);
+    if (r != cudaErrorNotSupported) return r;
+  }
   if (a.dtype == F32) {
     if (plan != 1) {  // FMP_FOLD=1: one block per walk (timing tools)
       const cudaError_t r = launch_fold_k<float, 14, 5, 4, 2>(a, st);
