@@ -77,6 +77,41 @@ def test_config2_headline_variant(fmp, oracle, monkeypatch, variant, env, table)
             r.residual_norm <= 1e-9 * np.linalg.norm(Y[b])
 
 
+def test_config2_headline_variant_near_ties(fmp, oracle):
+    """The F16 rows' one-barrier identification keeps the reference's tie rule
+    (first index within 1e-9 of the maximum, solvers.cpp:90-101) when the
+    band holds entries of different warps: conjugate-symmetric real signals
+    (x[l] = x[N - l]) make y real, so |h[k]| = |h[N - k]| up to rounding at
+    every iteration, and k, N - k belong to different threads of the CTA."""
+    n, m, k, B = 4096, 1024, 64, 320
+    rows = fmp.make_row_selection(n, m, fmp.derive_seed(2, 1 << 40))
+    op = fmp.SensingOperator("fourier", n, rows)
+    assert fmp.omp_plan_info(op, np.complex128, B, k)["ctas_per_sm"] == 2
+    rng = np.random.default_rng(7)
+    om = np.asarray(rows, dtype=np.int64) - 1
+    Y = np.empty((B, m), dtype=np.complex128)
+    sups = []
+    for b in range(B):
+        lam = rng.choice(np.arange(1, n // 2), size=k // 2, replace=False)
+        c = rng.standard_normal(k // 2) + np.sign(rng.standard_normal(k // 2))
+        pos = np.concatenate([lam, n - lam])
+        x = np.concatenate([c, c])
+        Y[b] = (np.exp(-2j * np.pi * np.outer(om, pos) / n) @ x) / np.sqrt(n)
+        sups.append(sorted(int(p) + 1 for p in pos))
+    assert np.abs(Y.imag).max() < 1e-12 * np.abs(Y.real).max()
+    tol = 1e-9 * np.linalg.norm(Y, axis=1)
+    res = fmp.omp_solve_batch(op, Y, fmp.SolveConfig(k, 0.0, "gpu"), tolerances=tol)
+    refs = _oracle_many(oracle, "fourier", n, rows, Y, k, tol, "fast", list(range(0, B, 8)))
+    _check(res, refs, 1e-9, check_resid=False)
+    ties = 0
+    for b, r in refs.items():
+        # the pair's lower index first, its mirror right after or later
+        first = [int(v) for v in r.support]
+        ties += sum(1 for a, c in zip(first[::2], first[1::2]) if a + c - 2 == n)
+        assert sorted(first) == sups[b]
+    assert ties > 0
+
+
 def _config4(fmp, B):
     n, m, k = 16384, 4096, 128
     sigma = np.sqrt(k / (2 * n * 1e3))
