@@ -68,6 +68,7 @@ struct OmpK {
   // shared-memory plan
   void* buf_ws;  // grid x (n + n/8) when the buffer lives in global memory
   int r_smem, w_smem, map_smem;
+  int w_rows;  // F16: leading rows of W (row-major packed) kept in shared memory
   int off_g, off_r, off_w, off_tw, off_small, off_map;
   int tw_a;       // two-level twiddle split
   double margin;  // relative slack on the residual identity
@@ -246,6 +247,14 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
                    : reinterpret_cast<V*>(a.r_ws) + (size_t)blockIdx.x * m;
   double2* W = a.w_smem ? reinterpret_cast<double2*>(sm + a.off_w)
                        : a.w_ws + (size_t)blockIdx.x * ((size_t)T * (T + 1) / 2);
+  // F16: W row-major packed (row i at i (i + 1) / 2), split by rows: the
+  // first R0 in shared memory, the later (shorter-lived) ones in the CTA's
+  // global workspace.  R0 is a multiple of 8 or covers every row, so the 8
+  // rows a warp takes in the first least-squares pass lie on one side.
+  double2* const Ws = reinterpret_cast<double2*>(sm + a.off_w);
+  double2* const Wg = a.w_ws + (size_t)blockIdx.x * ((size_t)T * (T + 1) / 2);
+  const int R0 = a.w_rows;
+  auto tri = [](int i) { return (i * (i + 1)) >> 1; };
   unsigned char* p = sm + a.off_small;
   double2* s_x = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
   double2* s_z = reinterpret_cast<double2*>(p); p += 16 * (size_t)T;
@@ -842,7 +851,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         for (int base = 0; base < s; base += nth / LSG) {
           const int i = base + tid / LSG, q = tid % LSG;
           double ar = 0.0, ai = 0.0;
-          if (i < s)
+          // wat(j) = W(i, j)
+          auto dot_row = [&](auto&& wat) {
             for (int j0 = q; j0 <= i; j0 += LSG * LSU) {
               // fixed-size predicated chunk: all loads issue before the FMAs
               double2 w[LSU], v[LSU];
@@ -850,7 +860,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
               for (int u = 0; u < LSU; ++u) {
                 const int j = j0 + LSG * u;
                 if (j <= i) {
-                  w[u] = W[wofs(T, i, j)];
+                  w[u] = wat(j);
                   v[u] = gram_of(s_lam[j], pick);
                 } else {
                   w[u] = make_double2(0.0, 0.0);
@@ -863,6 +873,21 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
                 ai = fma(w[u].x, v[u].y, fma(w[u].y, v[u].x, ai));
               }
             }
+          };
+          if (i < s) {
+            if constexpr (F16) {
+              // (two call sites: shared and global loads stay distinct)
+              if (i < R0) {
+                const double2* Wr = Ws + tri(i);
+                dot_row([&](int j) { return Wr[j]; });
+              } else {
+                const double2* Wr = Wg + tri(i);
+                dot_row([&](int j) { return Wr[j]; });
+              }
+            } else {
+              dot_row([&](int j) { return W[wofs(T, i, j)]; });
+            }
+          }
 #pragma unroll
           for (int o = LSG / 2; o; o >>= 1) {
             ar += __shfl_xor_sync(0xffffffffu, ar, o);
@@ -918,7 +943,12 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
                 const int i = i0 + LSG * u;
                 if (i < s) {
                   l[u] = s_l[i];
-                  w[u] = Wc[i - j];
+                  if constexpr (F16) {
+                    if (i < R0) w[u] = Ws[tri(i) + j];
+                    else w[u] = Wg[tri(i) + j];
+                  } else {
+                    w[u] = Wc[i - j];
+                  }
                 } else {
                   l[u] = make_double2(0.0, 0.0);
                   w[u] = l[u];
@@ -938,7 +968,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           }
           if (j < s && q == 0) {
             const double2 wn = make_double2(-ar * invd, -ai * invd);
-            W[wofs(T, s, j)] = wn;
+            if constexpr (F16) (s < R0 ? Ws : Wg)[tri(s) + j] = wn;
+            else W[wofs(T, s, j)] = wn;
             const double2 xo = s_x[j];
             const double xr = xo.x + wn.x * znew.x + wn.y * znew.y;
             const double xi = xo.y + wn.x * znew.y - wn.y * znew.x;
@@ -947,7 +978,8 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
           }
         }
         if (tid == 0) {
-          W[wofs(T, s, s)] = make_double2(invd, 0.0);
+          if constexpr (F16) (s < R0 ? Ws : Wg)[tri(s) + s] = make_double2(invd, 0.0);
+          else W[wofs(T, s, s)] = make_double2(invd, 0.0);
           s_z[s] = znew;
           s_lam[s] = pick;
           s_sel[pick >> 5] |= 1u << (pick & 31);
@@ -1030,6 +1062,7 @@ struct OmpPlan {
   size_t total;
   int gmode;
   bool rsm, wsm, bufg, msm;
+  int wrows;  // F16: rows of W in shared memory (wsm: at least one)
   int off_g, off_r, off_w, off_tw, off_small, off_map, tw_a;
 };
 
@@ -1076,14 +1109,34 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   if (!p.bufg) tot += buf;
   // W next: the least-squares phase is latency bound.  F16 leaves the kernel
   // table in global memory (read through L1 by the fast rows and the Gram
-  // lookups) and gives W the room; the problem's measurements (thread order,
-  // 16 KB) then stay in the CTA's global workspace, read once per residual
-  // (measured on config 2: W in smem / y in L2 318 k recoveries/s, y in smem
-  // / W in L2 308 k)
+  // lookups); the problem's measurements (16 KB, read by every residual)
+  // come first and W takes what is left, by rows: the leading rows - read by
+  // every later iteration - in shared memory, the last ones in the CTA's
+  // global workspace (config 2: rows 0..47 of 64).  Measured on config 2:
+  // y in smem / W in L2 308 k, W in smem / y in L2 322 k recoveries/s (the
+  // residual then waits ~10 % of the time on its measurements)
   const char* gs = getenv("FMP_F16_GSMEM");
   const bool f16g = f16 && !(gs && atoi(gs) == 1);  // F16 with the table in global memory
-  p.wsm = f16g ? tot + w <= cap : tot + w + gmin <= cap;
-  if (p.wsm) tot += w;
+  size_t wbytes = w;
+  p.wrows = 0;
+  if (f16g) {
+    p.rsm = tot + r <= cap;
+    if (p.rsm) tot += r;
+    int R = (int)T;
+    auto trib = [&](int rr) { return al((size_t)rr * (rr + 1) / 2 * 16); };
+    if (tot + trib(R) > cap) {
+      R &= ~7;
+      while (R > 0 && tot + trib(R) > cap) R -= 8;
+    }
+    const char* wr = getenv("FMP_F16_WROWS");  // timing tools: cap the rows kept in smem
+    if (wr && atoi(wr) >= 0 && atoi(wr) < R) R = atoi(wr) & ~7;
+    p.wrows = R;
+    p.wsm = R > 0;
+    wbytes = trib(R);
+  } else {
+    p.wsm = tot + w + gmin <= cap;
+  }
+  if (p.wsm) tot += wbytes;
   p.gmode = 0;
   if (!(HAD && !op.glat) && !f16g) {
     if (tot + gfull <= cap) { p.gmode = 1; tot += gfull; }
@@ -1091,15 +1144,17 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
     // several CTAs per SM: the conjugate half stays in global memory, where
     // the L1 left beside the CTAs' shared memory keeps it resident
   }
-  p.rsm = tot + r <= cap;
-  if (p.rsm) tot += r;
+  if (!f16g) {
+    p.rsm = tot + r <= cap;
+    if (p.rsm) tot += r;
+  }
   const size_t mapb = 2 * al((size_t)((n + 7) / 8) * 8 * 2);  // row map + support map
   p.msm = !f16 && !p.bufg && m <= 32767 && T <= 32767 && tot + mapb <= cap;
   if (p.msm) tot += mapb;
   p.total = tot;
   size_t off = p.bufg ? 0 : buf;
   p.off_tw = (int)off; off += tw;
-  p.off_w = (int)off; if (p.wsm) off += w;
+  p.off_w = (int)off; if (p.wsm) off += wbytes;
   p.off_g = (int)off; off += p.gmode == 1 ? gfull : (p.gmode == 2 ? ghalf : 0);
   p.off_r = (int)off; if (p.rsm) off += r;
   p.off_map = (int)off; if (p.msm) off += mapb;
@@ -1160,6 +1215,7 @@ cudaError_t launch_omp_t(const OmpArgs& a, cudaStream_t st) {
   k.queue = a.queue;
   k.r_smem = p.rsm;
   k.w_smem = p.wsm;
+  k.w_rows = p.wrows;
   k.map_smem = p.msm;
   k.off_map = p.off_map;
   k.buf_ws = a.buf_ws;
