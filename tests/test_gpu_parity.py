@@ -101,10 +101,11 @@ def test_apply_adjoint_other_dtypes(fmp, oracle, dtype, tol):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64, np.complex64, np.complex128])
-@pytest.mark.parametrize("n,m", [(65536, 8192), (65536, 8191), (1 << 17, 12345)])
+@pytest.mark.parametrize("n,m", [(65536, 8192), (65536, 8191), (1 << 17, 12345), (1 << 15, 4000)])
 def test_apply_adjoint_fold_path(fmp, oracle, n, m, dt):
     """Batched Hadamard adjoint beyond one CTA (batch >= 64): the one-pass
-    fold kernel (fmp_transform_fold.cu; f32 two blocks per walk with r staged
+    fold kernel (fmp_transform_fold.cu; f32: the register fold for 2, 4 or 8
+    input blocks, two output blocks per walk with r staged
     by a bulk copy, 8-byte elements with r read through L1), or the job queue
     (c128); m * 4 bytes not a multiple of 16 takes the plain-load staging."""
     om = oracle.make_row_selection(n, m, 11 + m)
