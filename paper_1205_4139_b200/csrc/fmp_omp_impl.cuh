@@ -28,11 +28,14 @@ namespace fmp {
 namespace {
 
 
-constexpr int ORMAX = 8;  // radix of the in-kernel transform passes
-#ifndef FMP_OLOGP
-#define FMP_OLOGP 3
-#endif
-constexpr int OLOGP = FMP_OLOGP;  // transform-buffer padding period 2^OLOGP
+// Radix of the in-kernel transform passes and the matching padding period
+// of the transform buffer (one pad slot per radix).  Elements of <= 8 bytes
+// (c64, f64, f32) hold a radix-16 sub-problem in <= 32 registers: config 4
+// c64 (n = 2^14) runs 16 16 16 4 instead of 8 8 8 8 4 (31.3 k -> 36.3 k
+// recoveries/s); c128 stays at radix 8 (radix 16 spills at 128 registers;
+// its config-2 solver has the F16 rows instead).
+template <class V> __host__ __device__ constexpr int ormax_v() { return sizeof(V) <= 8 ? 16 : 8; }
+template <class V> __host__ __device__ constexpr int ologp_v() { return sizeof(V) <= 8 ? 4 : 3; }
 // least-squares passes: LSG threads per row / column, LSU loads per thread
 // issued together.  W in L2 or 512 threads: 8 / 4 (measured best, round 1);
 // the F16 plan (256 threads, W in smem, T <= 64 rows in one sweep): 4 / 4
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   __shared__ double red2[F16 ? 32 : 1];  // F16: the residual norm's partials
   __shared__ int s_prob, s_lost;
   constexpr int NW = NT / 32;  // warps per CTA (block reductions)
+  constexpr int ORMAX = ormax_v<V>(), OLOGP = ologp_v<V>();
   constexpr int LSG = F16 ? FMP_LSG16 : 8, LSU = F16 ? FMP_LSU16 : 4;
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         adj_pass1(v);
         return rn_;
       }
-      if (s_xmap && log2n >= OLOGP) {
+      if (s_xmap && log2n >= 3) {
         __syncthreads();
         first_pass_map8<OLOGP, false, HAD>(
             buf, log2n, s_xmap,
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
             },
             tid, nth);
         __syncthreads();
-        block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth, -1, OLOGP);
+        block_transform<ORMAX, false, HAD>(buf, log2n, tw, tid, nth, -1, 3);  // (the mapped pass did 3 bits)
       } else {
         for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
         __syncthreads();
@@ -595,12 +599,12 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
         } else if (!fast_row) {
           // conventional correlation: U^H scatter(r) (sensing.cpp:102-109)
           const V* r = t == 1 ? y : rs;
-          if (s_map && log2n >= OLOGP) {
+          if (s_map && log2n >= 3) {
             __syncthreads();  // buf may still be read (previous argmax / h0)
             first_pass_map8<OLOGP, true, HAD>(
                 buf, log2n, s_map, [&](int q) { return q >= 0 ? r[q] : zv; }, tid, nth);
             __syncthreads();
-            block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth, -1, OLOGP);
+            block_transform<ORMAX, true, HAD>(buf, log2n, tw, tid, nth, -1, 3);
           } else {
             for (int i = tid; i < nbuf; i += nth) buf[i] = zv;
             __syncthreads();
@@ -1080,7 +1084,7 @@ OmpPlan omp_plan(const DevOp& op, int64_t T, int ctas, bool f16 = false) {
   const int64_t n = op.n, m = op.m;
   auto al = [](size_t b) { return ((b + 15) / 16) * 16; };
   const size_t buf = f16 ? al((size_t)(n + n / 16 + n / 512) * sizeof(V))
-                         : al((size_t)(n + (n >> OLOGP)) * sizeof(V));
+                         : al((size_t)(n + (n >> ologp_v<V>())) * sizeof(V));
   const size_t gfull = al(HAD ? (size_t)n * 2 : (size_t)n * sizeof(V));
   const size_t ghalf = al((size_t)(n / 2 + 1) * sizeof(V));
   const size_t r = al((size_t)m * sizeof(V));
