@@ -21,6 +21,7 @@
 // r = y - Phi_Lambda x by one forward transform of the sparse estimate.
 #pragma once
 #include <atomic>
+#include <type_traits>
 
 #include "fmp_kcommon.cuh"
 
@@ -39,6 +40,12 @@ template <class V> __host__ __device__ constexpr int ologp_v() { return sizeof(V
 // least-squares passes: LSG threads per row / column, LSU loads per thread
 // issued together.  W in L2 or 512 threads: 8 / 4 (measured best, round 1);
 // the F16 plan (256 threads, W in smem, T <= 64 rows in one sweep): 4 / 4
+#ifndef FMP_LSGG
+#define FMP_LSGG 8
+#endif
+#ifndef FMP_LSUG
+#define FMP_LSUG 4
+#endif
 #ifndef FMP_LSG16
 #define FMP_LSG16 4
 #endif
@@ -201,7 +208,10 @@ __global__ void __launch_bounds__(NT, CT) k_omp(OmpK a) {
   __shared__ int s_prob, s_lost;
   constexpr int NW = NT / 32;  // warps per CTA (block reductions)
   constexpr int ORMAX = ormax_v<V>(), OLOGP = ologp_v<V>();
-  constexpr int LSG = F16 ? FMP_LSG16 : 8, LSU = F16 ? FMP_LSU16 : 4;
+  // (c64: 4 threads per row, 8 loads per sweep - config 4's long rows of W
+  // in L2: 38.5 k -> 39.3 k recoveries/s)
+  constexpr bool LS48 = std::is_same<V, float2>::value;
+  constexpr int LSG = F16 ? FMP_LSG16 : (LS48 ? 4 : FMP_LSGG), LSU = F16 ? FMP_LSU16 : (LS48 ? 8 : FMP_LSUG);
   const DevOp& op = a.op;
   const int n = (int)op.n, m = (int)op.m, log2n = op.log2n, T = a.T;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5,
